@@ -1,0 +1,141 @@
+"""Host orchestration between the reference-shaped API and the C ABI.
+
+Lowers augmenters to ``sa_stage`` descriptors (pipeline.lower_stages) and calls
+the fused kernel either on host buffers (sa_pipeline_run_host: chunked H2D ->
+kernel -> D2H, overlapped on two streams) or on device tensors
+(sa_pipeline_run on torch's current stream).  torch is used only for device
+memory and streams.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _abi, _native
+from .pipeline import lower_stages
+
+
+def _row_factor(stages, repeat_rows: bool) -> int:
+    for s in stages:
+        if s.kind == "repeat" and s.expands():
+            return s.r if repeat_rows else 1
+    return 1
+
+
+def _lower(stages, first_index, repeat_rows):
+    arr, aux = lower_stages(stages, first_index)
+    if not repeat_rows:  # Repeat's per-series form is the identity (basic.py:396-397)
+        for j in range(len(stages)):
+            if arr[j].op == _abi.SA_OP_REPEAT:
+                arr[j].probability = 0.0
+    return arr, aux
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+def run_host(stages, values: np.ndarray, seed: int, first_index: int = 0, series_offset: int = 0,
+             len_out: int | None = None, check_finite: bool = True, repeat_rows: bool = True) -> np.ndarray:
+    """Run `stages` over a host (n, L) float64 batch; returns a new array."""
+    values = np.ascontiguousarray(values, dtype=np.float64)
+    n, L = values.shape
+    _native.current_device()
+    arr, aux = _lower(stages, first_index, repeat_rows)
+    rows = n * _row_factor(stages, repeat_rows)
+    L_out = L if len_out is None else int(len_out)
+    out = np.empty((rows, L_out), dtype=np.float64)
+    rc = _native.lib().sa_pipeline_run_host(
+        arr, len(stages), aux.ctypes.data_as(ctypes.c_void_p), aux.size, int(seed),
+        int(series_offset), _ptr(values), n, L, _ptr(out), L_out,
+    )
+    if rc == _abi.SA_ERR_NONFINITE and not check_finite:
+        return out
+    _native.check(rc, "sa_pipeline_run_host")
+    return out
+
+
+def run_device(stages, values, seed: int, series_offset: int = 0, len_out: int | None = None,
+               first_index: int = 0, out=None):
+    """Run `stages` over a CUDA float64 tensor (n, L); returns the output tensor."""
+    import torch
+
+    if not (values.is_cuda and values.dtype == torch.float64 and values.dim() == 2):
+        raise TypeError("run_device expects a 2-D float64 CUDA tensor")
+    values = values.contiguous()
+    n, L = values.shape
+    with torch.cuda.device(values.device):
+        _native.ensure_device(values.device.index)
+        arr, aux = _lower(stages, first_index, True)
+        rows = n * _row_factor(stages, True)
+        L_out = L if len_out is None else int(len_out)
+        if out is None:
+            out = torch.empty((rows, L_out), dtype=torch.float64, device=values.device)
+        stream = torch.cuda.current_stream(values.device).cuda_stream
+        rc = _native.lib().sa_pipeline_run(
+            arr, len(stages), aux.ctypes.data_as(ctypes.c_void_p), aux.size, int(seed),
+            int(series_offset), values.data_ptr(), n, L, out.data_ptr(), L_out, stream,
+        )
+        _native.check(rc, "sa_pipeline_run")
+    return out
+
+
+def launch_device(stages, values, out, flags, seed: int, series_offset: int = 0, first_index: int = 0,
+                  stream=None, lowered=None):
+    """Asynchronous launch (no sync, no status read): flags is a 1-element
+    int32 CUDA tensor that receives SA_FLAG_* bits.  Used by bench.py."""
+    import torch
+
+    arr, aux = lowered if lowered is not None else _lower(stages, first_index, True)
+    n, L = values.shape
+    st = stream if stream is not None else torch.cuda.current_stream(values.device).cuda_stream
+    rc = _native.lib().sa_pipeline_launch(
+        arr, len(stages), aux.ctypes.data_as(ctypes.c_void_p), aux.size, int(seed), int(series_offset),
+        values.data_ptr(), n, L, out.data_ptr(), out.shape[1], flags.data_ptr(), st,
+    )
+    _native.check(rc, "sa_pipeline_launch")
+
+
+def fft_forward_host(values: np.ndarray):
+    import torch
+
+    dev = _native.current_device()
+    x = torch.from_numpy(np.ascontiguousarray(values)).to(f"cuda:{dev}")
+    n, L = x.shape
+    bins = L // 2 + 1
+    re = torch.empty((n, bins), dtype=torch.float64, device=x.device)
+    im = torch.empty_like(re)
+    st = torch.cuda.current_stream().cuda_stream
+    _native.check(_native.lib().sa_fft_forward(x.data_ptr(), n, L, re.data_ptr(), im.data_ptr(), st))
+    return re.cpu().numpy(), im.cpu().numpy()
+
+
+def fft_inverse_host(re: np.ndarray, im: np.ndarray, L: int) -> np.ndarray:
+    import torch
+
+    dev = _native.current_device()
+    tre = torch.from_numpy(np.ascontiguousarray(re)).to(f"cuda:{dev}")
+    tim = torch.from_numpy(np.ascontiguousarray(im)).to(f"cuda:{dev}")
+    n = tre.shape[0]
+    out = torch.empty((n, L), dtype=torch.float64, device=tre.device)
+    st = torch.cuda.current_stream().cuda_stream
+    _native.check(_native.lib().sa_fft_inverse(tre.data_ptr(), tim.data_ptr(), n, L, out.data_ptr(), st))
+    return out.cpu().numpy()
+
+
+def augment_spectrum_host(stage, seed: int, re: np.ndarray, im: np.ndarray, L: int):
+    import torch
+
+    dev = _native.current_device()
+    tre = torch.from_numpy(np.ascontiguousarray(re)).to(f"cuda:{dev}")
+    tim = torch.from_numpy(np.ascontiguousarray(im)).to(f"cuda:{dev}")
+    n = tre.shape[0]
+    ore, oim = torch.empty_like(tre), torch.empty_like(tim)
+    st = torch.cuda.current_stream().cuda_stream
+    _native.check(_native.lib().sa_augment_spectrum(
+        ctypes.byref(stage), int(seed), 0, tre.data_ptr(), tim.data_ptr(), n, L,
+        ore.data_ptr(), oim.data_ptr(), st,
+    ))
+    return ore.cpu().numpy(), oim.cpu().numpy()

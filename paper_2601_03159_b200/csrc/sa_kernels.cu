@@ -1,0 +1,757 @@
+// sa_kernels.cu -- the fused augmentation-chain kernel, the spectral
+// transform kernels, and the C ABI (include/seriesaug_b200.h).
+//
+// Execution model: a persistent grid of one-warp CTAs; each
+// warp takes series (rows) round-robin.  Per row:
+//   1. TMA bulk copy (cp.async.bulk, mbarrier completion) of the input row
+//      into shared memory -- one HBM read per series;
+//   2. gate pre-pass: lane j derives stage j's Philox key (reference
+//      core.py:77-82) and its first Philox block; random() < p of word 0 is
+//      the gate (core.py:235).  Words 1..3 stay cached for the stage's first
+//      draws;
+//   3. every fired stage runs in smem (sa_ops.cuh), per-sample order;
+//   4. finiteness is checked after every arithmetic stage (the reference's
+//      per-stage Batch() re-validation, core.py:259 -> :104) into a flag;
+//   5. coalesced 128-bit stores of the output row -- one HBM write per series.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/seriesaug_b200.h"
+#include "sa_ops.cuh"
+
+namespace sa {
+
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+// TMA 1-D bulk copy global -> shared, completion via mbarrier tx count.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// ------------------------------------------------------------ smem layout
+struct Layout {
+    uint32_t buf_a, buf_b, win, scache, small, iscr, bar, total;
+};
+
+__host__ __device__ inline uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
+
+__host__ __device__ inline Layout make_layout(int lcap, int ns, int small_words, int iscr_words) {
+    Layout l;
+    uint32_t o = 0;
+    l.buf_a = o; o = align16(o + 8u * (uint32_t)lcap);
+    l.buf_b = o; o = align16(o + 8u * (uint32_t)lcap);
+    l.win = o; o = align16(o + 8u * SA_WIN);
+    l.scache = o; o = align16(o + 48u * (uint32_t)(ns > 0 ? ns : 1));
+    l.small = o; o = align16(o + 8u * (uint32_t)small_words);
+    l.iscr = o; o = align16(o + 4u * (uint32_t)iscr_words);
+    l.bar = o; o = align16(o + 8u);
+    l.total = o;
+    return l;
+}
+
+// ------------------------------------------------------------ the kernel
+__global__ void __launch_bounds__(32) chain_kernel(const __grid_constant__ ChainParams p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x;
+    const Layout lay = make_layout(p.lcap, p.ns, p.small_words, p.iscr_words);
+    double* A = reinterpret_cast<double*>(smem + lay.buf_a);
+    double* B = reinterpret_cast<double*>(smem + lay.buf_b);
+    uint64_t* scache = reinterpret_cast<uint64_t*>(smem + lay.scache);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + lay.bar);
+    Warp w;
+    w.lane = lane;
+    w.win = reinterpret_cast<uint64_t*>(smem + lay.win);
+    w.small = reinterpret_cast<double*>(smem + lay.small);
+    w.iscr = reinterpret_cast<int32_t*>(smem + lay.iscr);
+    w.lcap = p.lcap;
+
+    if (lane == 0) mbar_init(bar, 1);
+    __syncwarp();
+    uint32_t phase = 0;
+    uint32_t flags = 0;
+    const int r = p.repeat_r;
+    const uint32_t in_bytes = 8u * (uint32_t)p.len_in;
+
+    for (int64_t row = blockIdx.x; row < p.rows_out; row += gridDim.x) {
+        const int64_t in_row = row / r;
+        const double* src = p.in + in_row * (int64_t)p.len_in;
+        // 1. stage the input row
+        if (p.bulk_in) {
+            if (lane == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(bar, in_bytes);
+                bulk_g2s(A, src, in_bytes, bar);
+            }
+        } else {
+            for (int t = lane; t < p.len_in; t += 32) A[t] = src[t];
+        }
+        // 2. gate pre-pass (overlaps the bulk copy)
+        uint64_t fire_lo = 0;  // fire bits of stages 0..63
+        for (int j0 = 0; j0 < p.ns; j0 += 32) {
+            const int j = j0 + lane;
+            bool fire = false;
+            if (j < p.ns) {
+                const DevStage& st = p.st[j];
+                const uint64_t series =
+                    st.post_repeat ? (uint64_t)(p.offset * r + row) : (uint64_t)(p.offset + in_row);
+                uint64_t k0, k1, o0, o1, o2, o3;
+                derive_key(p.seed, (uint64_t)st.index, series, k0, k1);
+                philox(k0, k1, 1, o0, o1, o2, o3);
+                uint64_t* c = scache + 6 * j;
+                c[0] = k0; c[1] = k1; c[2] = o0; c[3] = o1; c[4] = o2; c[5] = o3;
+                fire = u53(o0) < st.prob && st.op != SA_OP_REPEAT;
+            }
+            fire_lo |= (uint64_t)__ballot_sync(SA_FULL, fire) << j0;
+        }
+        if (p.bulk_in) {
+            mbar_wait(bar, phase);
+            phase ^= 1u;
+        }
+        __syncwarp();
+        // input finiteness (Batch invariant, core.py:104)
+        {
+            bool ok = true;
+            for (int t = lane; t < p.len_in; t += 32) ok = ok && isfinite(A[t]);
+            if (!__all_sync(SA_FULL, ok)) flags |= SA_FLAG_NONFINITE;
+        }
+        // 3. the chain
+        double* cur = A;
+        double* oth = B;
+        int L = p.len_in;
+        for (int j = 0; j < p.ns; ++j) {
+            if (!((fire_lo >> j) & 1ull)) continue;
+            const DevStage& st = p.st[j];
+            const uint64_t* c = scache + 6 * j;
+            WStream s;
+            s.k0 = c[0];
+            s.k1 = c[1];
+            s.win = c + 2;
+            s.winbuf = w.win;
+            s.wb = 0;
+            s.wn = 4;
+            s.wpos = 1;  // word 0 was the gate
+            s.has32 = 0;
+            s.u32 = 0;
+            bool arith = false;
+            switch (st.op) {
+                case SA_OP_JITTER:
+                case SA_OP_NOISE_GAUSSIAN: arith = op_gauss(st, s, cur, oth, L, w); break;
+                case SA_OP_SCALE: arith = op_scale(st, s, cur, oth, L, w); break;
+                case SA_OP_ROTATE: arith = op_rotate(cur, L, w); break;
+                case SA_OP_PERMUTE: arith = op_permute(st, s, cur, oth, L, w); break;
+                case SA_OP_CROP: arith = op_crop(st, s, cur, oth, L, w); break;
+                case SA_OP_REVERSE: arith = op_reverse(cur, oth, L, w); break;
+                case SA_OP_RESIZE: arith = op_resize(st, cur, oth, L, w); break;
+                case SA_OP_QUANTIZE: arith = op_quantize(st, cur, L, w); break;
+                case SA_OP_DRIFT: arith = op_drift(st, s, cur, L, w); break;
+                case SA_OP_NOISE_UNIFORM: arith = op_uniform(st, s, cur, L, w); break;
+                case SA_OP_NOISE_SPIKE: arith = op_spike(st, s, cur, L, w); break;
+                case SA_OP_NOISE_SLOPE: arith = op_slope(st, s, cur, L, w); break;
+                case SA_OP_APP:
+                case SA_OP_FREQ_MASK:
+                case SA_OP_SINUSOID: arith = op_spectral(st, s, cur, oth, L, w); break;
+                case SA_OP_TIME_WARP: arith = op_time_warp(st, s, cur, oth, L, w, flags); break;
+                case SA_OP_WINDOW_WARP: arith = op_window_warp(st, s, cur, oth, L, w, flags); break;
+                case SA_OP_DROPOUT: arith = op_dropout(st, s, cur, L, w); break;
+                case SA_OP_POOL: arith = op_pool(st, cur, L, w); break;
+                case SA_OP_CONVOLVE: arith = op_convolve(st, p.aux, cur, oth, L, w); break;
+                case SA_OP_SPEED_WARP: arith = op_speed_warp(st, s, cur, oth, L, w); break;
+                default: break;
+            }
+            if (arith) {
+                bool ok = true;
+                for (int t = lane; t < L; t += 32) ok = ok && isfinite(cur[t]);
+                if (!__all_sync(SA_FULL, ok)) flags |= SA_FLAG_NONFINITE;
+            }
+        }
+        // 5. write the row
+        double* dst = p.out + row * (int64_t)p.len_out;
+        if ((p.len_out & 1) == 0 && ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0)) {
+            const double2* c2 = reinterpret_cast<const double2*>(cur);
+            double2* d2 = reinterpret_cast<double2*>(dst);
+            for (int t = lane; t < p.len_out / 2; t += 32) __stcs(&d2[t], c2[t]);
+        } else {
+            for (int t = lane; t < p.len_out; t += 32) __stcs(&dst[t], cur[t]);
+        }
+        __syncwarp();
+    }
+    if (flags && lane == 0) atomicOr(p.flags, flags);
+}
+
+// ------------------------------------------------------------ spectral kernels
+struct FftParams {
+    const double* x;
+    const double* re;
+    const double* im;
+    double* xo;
+    double* reo;
+    double* imo;
+    int64_t n;
+    int32_t L, lcap;
+    const double2* tw;
+};
+
+__global__ void __launch_bounds__(32) rfft_kernel(const __grid_constant__ FftParams p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x;
+    double* A = reinterpret_cast<double*>(smem);
+    double* B = A + p.lcap;
+    const int bins = p.L / 2 + 1;
+    for (int64_t row = blockIdx.x; row < p.n; row += gridDim.x) {
+        const double* src = p.x + row * p.L;
+        for (int t = lane; t < p.L; t += 32) A[t] = src[t];
+        __syncwarp();
+        double2* X = rfft_warp(A, B, p.L, p.tw, lane);
+        for (int k = lane; k < bins; k += 32) {
+            p.reo[row * bins + k] = X[k].x;
+            p.imo[row * bins + k] = X[k].y;
+        }
+        __syncwarp();
+    }
+}
+
+__global__ void __launch_bounds__(32) irfft_kernel(const __grid_constant__ FftParams p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x;
+    double2* X = reinterpret_cast<double2*>(smem);
+    double2* O = X + p.lcap / 2;
+    const int bins = p.L / 2 + 1;
+    for (int64_t row = blockIdx.x; row < p.n; row += gridDim.x) {
+        for (int k = lane; k < bins; k += 32) X[k] = make_double2(p.re[row * bins + k], p.im[row * bins + k]);
+        __syncwarp();
+        double* y = irfft_warp(X, O, p.L, p.tw, lane);
+        for (int t = lane; t < p.L; t += 32) p.xo[row * p.L + t] = y[t];
+        __syncwarp();
+    }
+}
+
+struct SpecParams {
+    DevStage st;
+    uint64_t seed;
+    int64_t offset;
+    const double* re;
+    const double* im;
+    double* reo;
+    double* imo;
+    int64_t n;
+    int32_t L, lcap;
+};
+
+// SpectralAugmenter.augment_spectrum (freqaugment.py:49-76)
+__global__ void __launch_bounds__(32) spectrum_kernel(const __grid_constant__ SpecParams p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x;
+    double2* X = reinterpret_cast<double2*>(smem);
+    double* scratch = reinterpret_cast<double*>(X + p.lcap / 2);
+    uint64_t* win = reinterpret_cast<uint64_t*>(scratch + p.lcap);
+    uint64_t* c = win + SA_WIN;
+    Warp w;
+    w.lane = lane;
+    w.win = win;
+    const int bins = p.L / 2 + 1;
+    for (int64_t row = blockIdx.x; row < p.n; row += gridDim.x) {
+        for (int k = lane; k < bins; k += 32) X[k] = make_double2(p.re[row * bins + k], p.im[row * bins + k]);
+        uint64_t k0, k1, o0, o1, o2, o3;
+        derive_key(p.seed, (uint64_t)p.st.index, (uint64_t)(p.offset + row), k0, k1);
+        philox(k0, k1, 1, o0, o1, o2, o3);
+        if (lane == 0) { c[0] = o0; c[1] = o1; c[2] = o2; c[3] = o3; }
+        __syncwarp();
+        if (u53(o0) < p.st.prob && !spectral_noop(p.st)) {
+            WStream s;
+            s.k0 = k0; s.k1 = k1; s.win = c; s.winbuf = win; s.wb = 0; s.wn = 4; s.wpos = 1;
+            s.has32 = 0; s.u32 = 0;
+            perturb_spectrum(p.st, s, X, p.L, scratch, w);
+        }
+        for (int k = lane; k < bins; k += 32) {
+            p.reo[row * bins + k] = X[k].x;
+            p.imo[row * bins + k] = X[k].y;
+        }
+        __syncwarp();
+    }
+}
+
+}  // namespace sa
+
+// ====================================================================== host
+using namespace sa;
+
+namespace {
+
+thread_local std::string g_err;
+int64_t g_launches = 0;
+std::mutex g_mu;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(SA_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define SA_CUDA(call)                                 \
+    do {                                              \
+        cudaError_t e_ = (call);                      \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+    } while (0)
+
+struct DeviceState {
+    bool ready = false;
+    int sms = 0;
+    size_t smem_optin = 0;
+    std::map<int, double2*> twiddles;  // by length
+    // host-path workspaces (two streams)
+    cudaStream_t hs[2] = {nullptr, nullptr};
+    double* din[2] = {nullptr, nullptr};
+    double* dout[2] = {nullptr, nullptr};
+    uint32_t* dflags = nullptr;
+    size_t in_cap = 0, out_cap = 0;
+};
+std::map<int, DeviceState> g_dev;
+
+int current_device(int* dev) {
+    SA_CUDA(cudaGetDevice(dev));
+    return SA_OK;
+}
+
+int init_device(int dev) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    DeviceState& ds = g_dev[dev];
+    if (ds.ready) return SA_OK;
+    int prev;
+    SA_CUDA(cudaGetDevice(&prev));
+    SA_CUDA(cudaSetDevice(dev));
+    static const uint64_t ki[256] = SA_ZIG_KI_DOUBLE_INIT;
+    static const uint64_t wi[256] = SA_ZIG_WI_DOUBLE_INIT;
+    static const uint64_t fi[256] = SA_ZIG_FI_DOUBLE_INIT;
+    ZigEntry zig[256];
+    double fid[256];
+    for (int k = 0; k < 256; ++k) {
+        zig[k].ki = ki[k];
+        std::memcpy(&zig[k].wi, &wi[k], 8);
+        std::memcpy(&fid[k], &fi[k], 8);
+    }
+    SA_CUDA(cudaMemcpyToSymbol(g_zig, zig, sizeof(zig)));
+    SA_CUDA(cudaMemcpyToSymbol(g_fi, fid, sizeof(fid)));
+    SA_CUDA(cudaDeviceGetAttribute(&ds.sms, cudaDevAttrMultiProcessorCount, dev));
+    int optin = 0;
+    SA_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    ds.smem_optin = (size_t)optin;
+    SA_CUDA(cudaFuncSetAttribute(chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(rfft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(irfft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(spectrum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaSetDevice(prev));
+    ds.ready = true;
+    return SA_OK;
+}
+
+int ensure_device(int* dev_out) {
+    int dev;
+    int rc = current_device(&dev);
+    if (rc) return rc;
+    rc = init_device(dev);
+    if (rc) return rc;
+    *dev_out = dev;
+    return SA_OK;
+}
+
+// exp(-2 pi i k / L), k < L, correctly rounded via long double.
+int get_twiddles(int dev, int L, const double2** out) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    DeviceState& ds = g_dev[dev];
+    auto it = ds.twiddles.find(L);
+    if (it != ds.twiddles.end()) {
+        *out = it->second;
+        return SA_OK;
+    }
+    std::vector<double2> h((size_t)L);
+    const long double pi = 3.141592653589793238462643383279502884L;
+    for (int k = 0; k < L; ++k) {
+        long double a = -2.0L * pi * (long double)k / (long double)L;
+        h[(size_t)k] = make_double2((double)cosl(a), (double)sinl(a));
+    }
+    double2* d = nullptr;
+    SA_CUDA(cudaMalloc(&d, sizeof(double2) * (size_t)L));
+    SA_CUDA(cudaMemcpy(d, h.data(), sizeof(double2) * (size_t)L, cudaMemcpyHostToDevice));
+    ds.twiddles[L] = d;
+    *out = d;
+    return SA_OK;
+}
+
+bool fft_len_supported(int64_t L) { return L >= 2 && (L % 2) == 0 && ((L / 2) & (L / 2 - 1)) == 0; }
+
+bool is_spectral(int op) { return op == SA_OP_APP || op == SA_OP_FREQ_MASK || op == SA_OP_SINUSOID; }
+
+struct Plan {
+    ChainParams p;
+    Layout lay;
+    int grid;
+};
+
+// Lower the ABI stage table into kernel parameters and a launch shape.
+int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, int32_t n_aux, uint64_t seed,
+              int64_t offset, int64_t n, int64_t len_in, int64_t len_out, Plan* plan) {
+    if (ns < 0 || ns > SA_MAX_STAGES) return fail(SA_ERR_INVALID_ARG, "n_stages out of range");
+    if (n_aux < 0 || n_aux > SA_MAX_AUX) return fail(SA_ERR_INVALID_ARG, "aux table too large");
+    if (n < 0 || len_in < 1 || len_out < 1) return fail(SA_ERR_INVALID_ARG, "bad batch shape");
+    if (len_in > (1 << 24)) return fail(SA_ERR_UNSUPPORTED, "series longer than 2^24");
+    ChainParams& p = plan->p;
+    std::memset(&p, 0, sizeof(p));
+    p.ns = ns;
+    p.repeat_r = 1;
+    p.seed = seed;
+    p.offset = offset;
+    p.len_in = (int32_t)len_in;
+    p.len_out = (int32_t)len_out;
+    if (n_aux) std::memcpy(p.aux, aux, sizeof(double) * (size_t)n_aux);
+    int64_t L = len_in, lmax = len_in;
+    int small = 64, iscr = 16;
+    bool after_repeat = false;
+    for (int j = 0; j < ns; ++j) {
+        const sa_stage& s = stages[j];
+        DevStage& d = p.st[j];
+        if (s.op < 1 || s.op >= SA_OP_MAX) return fail(SA_ERR_INVALID_ARG, "unknown op code");
+        d.op = s.op;
+        d.index = s.index;
+        d.prob = s.probability;
+        for (int k = 0; k < 4; ++k) {
+            d.f[k] = s.f[k];
+            d.i[k] = s.i[k];
+        }
+        d.aux_off = s.aux_off;
+        d.aux_len = s.aux_len;
+        d.post_repeat = after_repeat ? 1 : 0;
+        d.len_in = (int32_t)L;
+        if (s.op == SA_OP_REPEAT && s.probability != 0.0 && s.i[0] != 1) {
+            if (p.repeat_r != 1) return fail(SA_ERR_INVALID_ARG, "at most one repeat stage");
+            p.repeat_r = (int32_t)s.i[0];
+            after_repeat = true;
+        }
+        if (s.op == SA_OP_CONVOLVE && (s.aux_off < 0 || s.aux_len < 1 || s.aux_off + s.aux_len > n_aux))
+            return fail(SA_ERR_INVALID_ARG, "convolve taps out of range");
+        if (is_spectral(s.op) && s.probability > 0.0) {
+            if (!fft_len_supported(L))
+                return fail(SA_ERR_UNSUPPORTED,
+                            "spectral stage at length " + std::to_string(L) +
+                                ": this build's FFT needs an even length with L/2 a power of two");
+            int rc = get_twiddles(dev, (int)L, &d.tw);
+            if (rc) return rc;
+        }
+        if (s.probability == 1.0 && (s.op == SA_OP_CROP || s.op == SA_OP_RESIZE)) L = s.i[0];
+        d.len_out = (int32_t)L;
+        lmax = std::max(lmax, L);
+        // scratch needs
+        if (s.op == SA_OP_DRIFT) small = std::max<int>(small, (int)(2 * s.i[0]) + 2);
+        if (s.op == SA_OP_TIME_WARP) small = std::max<int>(small, (int)(3 * s.i[0]) + 2);
+        if (s.op == SA_OP_WINDOW_WARP) small = std::max<int>(small, (int)(3 * s.i[1]) + 2);
+        if (s.op == SA_OP_SPEED_WARP) small = std::max<int>(small, (int)(2 * (s.i[0] + 1)) + 2);
+        if (s.op == SA_OP_NOISE_SPIKE) small = std::max<int>(small, (int)(lmax / 32) + 8);
+        if (s.op == SA_OP_PERMUTE) iscr = std::max<int>(iscr, (int)s.i[0] + 1);
+        if (s.op == SA_OP_NOISE_SPIKE) {
+            int64_t k = s.i[0];
+            uint32_t mask = (uint32_t)(1.2 * (double)k);
+            mask |= mask >> 1; mask |= mask >> 2; mask |= mask >> 4; mask |= mask >> 8; mask |= mask >> 16;
+            int64_t need = std::max<int64_t>((int64_t)mask + 1, lmax) + k + 1;
+            iscr = std::max<int>(iscr, (int)need);
+        }
+    }
+    if (L != len_out) return fail(SA_ERR_INVALID_ARG, "len_out does not match the projected length");
+    p.rows_out = n * p.repeat_r;
+    p.lcap = (int32_t)((lmax + 2 + 1) & ~1LL);
+    p.small_words = small;
+    p.iscr_words = iscr;
+    plan->lay = make_layout(p.lcap, ns, small, iscr);
+    DeviceState& ds = g_dev[dev];
+    if (plan->lay.total > ds.smem_optin)
+        return fail(SA_ERR_UNSUPPORTED, "series too long for one warp's shared memory (" +
+                                            std::to_string(plan->lay.total) + " B)");
+    int per_sm = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chain_kernel, 32, plan->lay.total);
+    if (e != cudaSuccess) return cuda_fail(e, "occupancy");
+    per_sm = std::max(per_sm, 1);
+    int64_t want = (int64_t)ds.sms * per_sm;
+    plan->grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, p.rows_out));
+    return SA_OK;
+}
+
+int launch_plan(Plan* plan, const double* d_in, double* d_out, uint32_t* d_flags, cudaStream_t stream) {
+    ChainParams& p = plan->p;
+    p.in = d_in;
+    p.out = d_out;
+    p.flags = d_flags;
+    p.bulk_in = ((p.len_in & 1) == 0 && (reinterpret_cast<uintptr_t>(d_in) & 15u) == 0) ? 1 : 0;
+    SA_CUDA(cudaMemsetAsync(d_flags, 0, sizeof(uint32_t), stream));
+    if (p.rows_out == 0) return SA_OK;
+    chain_kernel<<<plan->grid, 32, plan->lay.total, stream>>>(p);
+    SA_CUDA(cudaGetLastError());
+    __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
+    return SA_OK;
+}
+
+int flags_status(uint32_t f) {
+    if (f & SA_FLAG_WARP_MONOTONE) return fail(SA_ERR_WARP_MONOTONE, "warp map failed to stay strictly increasing");
+    if (f & SA_FLAG_NONFINITE) return fail(SA_ERR_NONFINITE, "batch contains non-finite values (NaN or Inf)");
+    return SA_OK;
+}
+
+int fft_plan_smem(int dev, int64_t L, int* lcap, size_t* smem, int* grid, const void* kern, int64_t n) {
+    *lcap = (int)((L + 2 + 1) & ~1LL);
+    *smem = (size_t)(*lcap) * 8 * 2 + 8 * SA_WIN + 64;
+    DeviceState& ds = g_dev[dev];
+    if (*smem > ds.smem_optin) return fail(SA_ERR_UNSUPPORTED, "series too long");
+    int per_sm = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32, *smem);
+    if (e != cudaSuccess) return cuda_fail(e, "occupancy");
+    *grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ds.sms * std::max(per_sm, 1), n));
+    return SA_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+int sa_abi_version(void) { return SA_ABI_VERSION; }
+
+const char* sa_last_error(void) { return g_err.c_str(); }
+
+int64_t sa_launch_count(void) { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
+
+int sa_init(int32_t device) {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) return fail(SA_ERR_NO_DEVICE, "no CUDA device available");
+    if (device < 0 || device >= count) return fail(SA_ERR_INVALID_ARG, "device index out of range");
+    SA_CUDA(cudaSetDevice(device));
+    return init_device(device);
+}
+
+int sa_derive_key(uint64_t seed, uint64_t j, uint64_t i, uint64_t* lo, uint64_t* hi) {
+    auto mix = [](uint64_t z) {
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+        return z ^ (z >> 31);
+    };
+    uint64_t s = mix(seed);
+    s = mix(s + kGolden + j);
+    s = mix(s + kGolden + i);
+    *lo = mix(s);
+    *hi = mix(s + kGolden);
+    return SA_OK;
+}
+
+int sa_pipeline_launch(const sa_stage* stages, int32_t n_stages, const double* aux, int32_t n_aux,
+                       uint64_t master_seed, int64_t series_offset, const double* d_in, int64_t n,
+                       int64_t len_in, double* d_out, int64_t len_out, uint32_t* d_flags, void* stream) {
+    int dev;
+    int rc = ensure_device(&dev);
+    if (rc) return rc;
+    Plan plan;
+    rc = make_plan(dev, stages, n_stages, aux, n_aux, master_seed, series_offset, n, len_in, len_out, &plan);
+    if (rc) return rc;
+    return launch_plan(&plan, d_in, d_out, d_flags, (cudaStream_t)stream);
+}
+
+int sa_pipeline_run(const sa_stage* stages, int32_t n_stages, const double* aux, int32_t n_aux,
+                    uint64_t master_seed, int64_t series_offset, const double* d_in, int64_t n, int64_t len_in,
+                    double* d_out, int64_t len_out, void* stream) {
+    int dev;
+    int rc = ensure_device(&dev);
+    if (rc) return rc;
+    Plan plan;
+    rc = make_plan(dev, stages, n_stages, aux, n_aux, master_seed, series_offset, n, len_in, len_out, &plan);
+    if (rc) return rc;
+    uint32_t* dflag = nullptr;
+    SA_CUDA(cudaMallocAsync(&dflag, sizeof(uint32_t), (cudaStream_t)stream));
+    rc = launch_plan(&plan, d_in, d_out, dflag, (cudaStream_t)stream);
+    if (rc) return rc;
+    uint32_t h = 0;
+    SA_CUDA(cudaMemcpyAsync(&h, dflag, sizeof(uint32_t), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    SA_CUDA(cudaFreeAsync(dflag, (cudaStream_t)stream));
+    SA_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    return flags_status(h);
+}
+
+int sa_pipeline_run_host(const sa_stage* stages, int32_t n_stages, const double* aux, int32_t n_aux,
+                         uint64_t master_seed, int64_t series_offset, const double* h_in, int64_t n,
+                         int64_t len_in, double* h_out, int64_t len_out) {
+    int dev;
+    int rc = ensure_device(&dev);
+    if (rc) return rc;
+    Plan plan;
+    rc = make_plan(dev, stages, n_stages, aux, n_aux, master_seed, series_offset, n, len_in, len_out, &plan);
+    if (rc) return rc;
+    const int64_t r = plan.p.repeat_r;
+    std::lock_guard<std::mutex> lk(g_mu);
+    DeviceState& ds = g_dev[dev];
+    // chunk of ~64 MB of input rows, two streams
+    const int64_t row_in_b = 8 * len_in, row_out_b = 8 * len_out * r;
+    int64_t chunk = std::max<int64_t>(1, (64ll << 20) / std::max<int64_t>(row_in_b, row_out_b));
+    chunk = std::min<int64_t>(chunk, std::max<int64_t>(n, 1));
+    size_t need_in = (size_t)(chunk * row_in_b), need_out = (size_t)(chunk * row_out_b);
+    if (!ds.hs[0]) {
+        SA_CUDA(cudaStreamCreateWithFlags(&ds.hs[0], cudaStreamNonBlocking));
+        SA_CUDA(cudaStreamCreateWithFlags(&ds.hs[1], cudaStreamNonBlocking));
+        SA_CUDA(cudaMalloc(&ds.dflags, 2 * sizeof(uint32_t)));
+    }
+    if (need_in > ds.in_cap || need_out > ds.out_cap) {
+        for (int k = 0; k < 2; ++k) {
+            if (ds.din[k]) cudaFree(ds.din[k]);
+            if (ds.dout[k]) cudaFree(ds.dout[k]);
+            SA_CUDA(cudaMalloc(&ds.din[k], std::max(need_in, ds.in_cap)));
+            SA_CUDA(cudaMalloc(&ds.dout[k], std::max(need_out, ds.out_cap)));
+        }
+        ds.in_cap = std::max(need_in, ds.in_cap);
+        ds.out_cap = std::max(need_out, ds.out_cap);
+    }
+    uint32_t hflags[2] = {0, 0};
+    SA_CUDA(cudaMemsetAsync(ds.dflags, 0, 2 * sizeof(uint32_t), ds.hs[0]));
+    SA_CUDA(cudaStreamSynchronize(ds.hs[0]));
+    int c = 0;
+    for (int64_t r0 = 0; r0 < n; r0 += chunk, ++c) {
+        const int64_t rows = std::min(chunk, n - r0);
+        cudaStream_t st = ds.hs[c & 1];
+        SA_CUDA(cudaMemcpyAsync(ds.din[c & 1], h_in + r0 * len_in, (size_t)(rows * row_in_b),
+                                cudaMemcpyHostToDevice, st));
+        Plan pl = plan;
+        pl.p.offset = series_offset + r0;
+        pl.p.rows_out = rows * r;
+        pl.grid = (int)std::max<int64_t>(1, std::min<int64_t>(plan.grid, pl.p.rows_out));
+        pl.p.in = ds.din[c & 1];
+        pl.p.out = ds.dout[c & 1];
+        pl.p.flags = ds.dflags + (c & 1);
+        pl.p.bulk_in = ((len_in & 1) == 0) ? 1 : 0;
+        if (pl.p.rows_out) {
+            chain_kernel<<<pl.grid, 32, pl.lay.total, st>>>(pl.p);
+            SA_CUDA(cudaGetLastError());
+            __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
+        }
+        SA_CUDA(cudaMemcpyAsync(h_out + r0 * r * len_out, ds.dout[c & 1], (size_t)(rows * row_out_b),
+                                cudaMemcpyDeviceToHost, st));
+    }
+    SA_CUDA(cudaMemcpyAsync(hflags, ds.dflags, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, ds.hs[c & 1]));
+    SA_CUDA(cudaStreamSynchronize(ds.hs[0]));
+    SA_CUDA(cudaStreamSynchronize(ds.hs[1]));
+    return flags_status(hflags[0] | hflags[1]);
+}
+
+int sa_fft_forward(const double* d_in, int64_t n, int64_t len, double* d_re, double* d_im, void* stream) {
+    int dev;
+    int rc = ensure_device(&dev);
+    if (rc) return rc;
+    if (!fft_len_supported(len))
+        return fail(SA_ERR_UNSUPPORTED, "this build's FFT needs an even length with L/2 a power of two");
+    FftParams p{};
+    p.x = d_in; p.reo = d_re; p.imo = d_im; p.n = n; p.L = (int32_t)len;
+    rc = get_twiddles(dev, (int)len, &p.tw);
+    if (rc) return rc;
+    size_t smem;
+    int lcap, grid;
+    rc = fft_plan_smem(dev, len, &lcap, &smem, &grid, (const void*)rfft_kernel, n);
+    if (rc) return rc;
+    p.lcap = lcap;
+    if (n == 0) return SA_OK;
+    rfft_kernel<<<grid, 32, smem, (cudaStream_t)stream>>>(p);
+    SA_CUDA(cudaGetLastError());
+    __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
+    return SA_OK;
+}
+
+int sa_fft_inverse(const double* d_re, const double* d_im, int64_t n, int64_t len, double* d_out, void* stream) {
+    int dev;
+    int rc = ensure_device(&dev);
+    if (rc) return rc;
+    if (!fft_len_supported(len))
+        return fail(SA_ERR_UNSUPPORTED, "this build's FFT needs an even length with L/2 a power of two");
+    FftParams p{};
+    p.re = d_re; p.im = d_im; p.xo = d_out; p.n = n; p.L = (int32_t)len;
+    rc = get_twiddles(dev, (int)len, &p.tw);
+    if (rc) return rc;
+    size_t smem;
+    int lcap, grid;
+    rc = fft_plan_smem(dev, len, &lcap, &smem, &grid, (const void*)irfft_kernel, n);
+    if (rc) return rc;
+    p.lcap = lcap;
+    if (n == 0) return SA_OK;
+    irfft_kernel<<<grid, 32, smem, (cudaStream_t)stream>>>(p);
+    SA_CUDA(cudaGetLastError());
+    __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
+    return SA_OK;
+}
+
+int sa_augment_spectrum(const sa_stage* stage, uint64_t master_seed, int64_t series_offset, const double* d_re,
+                        const double* d_im, int64_t n, int64_t len, double* d_re_out, double* d_im_out,
+                        void* stream) {
+    int dev;
+    int rc = ensure_device(&dev);
+    if (rc) return rc;
+    if (!is_spectral(stage->op)) return fail(SA_ERR_INVALID_ARG, "not a spectral stage");
+    SpecParams p{};
+    p.st.op = stage->op;
+    p.st.index = stage->index;
+    p.st.prob = stage->probability;
+    for (int k = 0; k < 4; ++k) {
+        p.st.f[k] = stage->f[k];
+        p.st.i[k] = stage->i[k];
+    }
+    p.seed = master_seed;
+    p.offset = series_offset;
+    p.re = d_re; p.im = d_im; p.reo = d_re_out; p.imo = d_im_out; p.n = n; p.L = (int32_t)len;
+    size_t smem;
+    int lcap, grid;
+    rc = fft_plan_smem(dev, len, &lcap, &smem, &grid, (const void*)spectrum_kernel, n);
+    if (rc) return rc;
+    p.lcap = lcap;
+    smem = (size_t)lcap * 8 * 2 + 8 * SA_WIN + 64;
+    if (n == 0) return SA_OK;
+    spectrum_kernel<<<grid, 32, smem, (cudaStream_t)stream>>>(p);
+    SA_CUDA(cudaGetLastError());
+    __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
+    SA_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    return SA_OK;
+}
+
+int sa_host_alloc(void** ptr, int64_t bytes) {
+    SA_CUDA(cudaHostAlloc(ptr, (size_t)bytes, cudaHostAllocPortable));
+    return SA_OK;
+}
+
+int sa_host_free(void* ptr) {
+    SA_CUDA(cudaFreeHost(ptr));
+    return SA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,726 @@
+// sa_ops.cuh -- the augmentation operators, one warp per series, series in smem.
+//
+// Each op transforms `cur` (length L) and may use `oth` as scratch or as the
+// output buffer (then it swaps the two).  All draws come from the stage's
+// WStream in exactly the reference's order (gate first, consumed by the
+// pre-pass in the kernel).  FP expressions follow the reference's evaluation
+// order; the TU is compiled with -fmad=false so nothing is contracted.
+#pragma once
+#include <math.h>
+#include <stdint.h>
+
+#include "../../include/seriesaug_b200.h"
+#include "sa_fft.cuh"
+#include "sa_rng.cuh"
+
+#define SA_MAX_AUX 512
+
+namespace sa {
+
+struct DevStage {
+    int32_t op, index;
+    int32_t len_in, len_out;
+    int32_t post_repeat, aux_off;
+    int32_t aux_len, pad;
+    double prob;
+    double f[4];
+    int64_t i[4];
+    const double2* tw;  // exp(-2 pi i k / len_in), k < len_in (spectral ops)
+};
+
+struct ChainParams {
+    int32_t ns, repeat_r;
+    int32_t len_in, len_out;
+    int32_t lcap, small_words, iscr_words, bulk_in;
+    uint64_t seed;
+    int64_t offset;
+    int64_t rows_out;
+    const double* in;
+    double* out;
+    uint32_t* flags;
+    double aux[SA_MAX_AUX];
+    DevStage st[SA_MAX_STAGES];
+};
+
+struct Warp {
+    int lane;
+    uint64_t* win;
+    double* small;
+    int32_t* iscr;
+    int lcap;
+};
+
+// ---------------------------------------------------------------- numerics
+// np.linspace(start, stop, num)[k], endpoint=True (numpy function_base).
+__device__ __forceinline__ double linspace_at(double start, double stop, int64_t num, int64_t k) {
+    if (num > 1 && k == num - 1) return stop;
+    int64_t div = num - 1;
+    double delta = stop - start;
+    double y = (double)k;
+    if (div > 0) {
+        double step = delta / (double)div;
+        if (step == 0.0) y = (y / (double)div) * delta;
+        else y = y * step;
+    } else {
+        y = y * delta;
+    }
+    return y + start;
+}
+
+// np.interp(x, xp, fp) with xp increasing (binary search, exact-hit rule).
+__device__ __forceinline__ double interp1(double x, const double* xp, const double* fp, int n) {
+    if (x > xp[n - 1]) return fp[n - 1];
+    if (x < xp[0]) return fp[0];
+    int lo = 0, hi = n;
+    while (hi - lo > 1) {
+        int mid = lo + ((hi - lo) >> 1);
+        if (x >= xp[mid]) lo = mid;
+        else hi = mid;
+    }
+    int j = lo;
+    if (j == n - 1) return fp[j];
+    if (xp[j] == x) return fp[j];
+    double slope = (fp[j + 1] - fp[j]) / (xp[j + 1] - xp[j]);
+    double r = slope * (x - xp[j]) + fp[j];
+    if (isnan(r)) {
+        r = slope * (x - xp[j + 1]) + fp[j + 1];
+        if (isnan(r) && fp[j] == fp[j + 1]) r = fp[j];
+    }
+    return r;
+}
+
+// np.interp(x, arange(n), fp).
+__device__ __forceinline__ double interp_grid(double x, const double* fp, int n) {
+    if (x > (double)(n - 1)) return fp[n - 1];
+    if (x < 0.0) return fp[0];
+    int j = (int)floor(x);
+    if (j >= n - 1) return fp[n - 1];
+    if ((double)j == x) return fp[j];
+    double slope = (fp[j + 1] - fp[j]) / ((double)(j + 1) - (double)j);
+    double r = slope * (x - (double)j) + fp[j];
+    if (isnan(r)) {
+        r = slope * (x - (double)(j + 1)) + fp[j + 1];
+        if (isnan(r) && fp[j] == fp[j + 1]) r = fp[j];
+    }
+    return r;
+}
+
+// numpy pairwise summation of f(t), t in [lo, lo + n), leaf n <= 128.
+template <class F>
+__device__ __forceinline__ double pairwise_leaf(int lo, int n, F& f) {
+    if (n < 8) {
+        double r = 0.0;
+        for (int k = 0; k < n; ++k) r += f(lo + k);
+        return r;
+    }
+    double r[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) r[q] = f(lo + q);
+    int k;
+    for (k = 8; k < n - (n % 8); k += 8) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) r[q] += f(lo + k + q);
+    }
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; k < n; ++k) res += f(lo + k);
+    return res;
+}
+
+// leaves in left-to-right order; lane (leaf % 32) computes leaf `leaf`.
+template <class F>
+__device__ void pairwise_leaves(int lo, int n, F& f, double* leafsum, int& leaf, int lane) {
+    if (n <= 128) {
+        if ((leaf & 31) == lane) leafsum[leaf] = pairwise_leaf(lo, n, f);
+        leaf += 1;
+        return;
+    }
+    int n2 = n / 2;
+    n2 -= n2 % 8;
+    pairwise_leaves(lo, n2, f, leafsum, leaf, lane);
+    pairwise_leaves(lo + n2, n - n2, f, leafsum, leaf, lane);
+}
+
+__device__ double pairwise_combine(int n, const double* leafsum, int& leaf) {
+    if (n <= 128) return leafsum[leaf++];
+    int n2 = n / 2;
+    n2 -= n2 % 8;
+    double a = pairwise_combine(n2, leafsum, leaf);
+    double b = pairwise_combine(n - n2, leafsum, leaf);
+    return a + b;
+}
+
+template <class F>
+__device__ double pairwise_warp(int n, F f, double* leafsum, int lane) {
+    int leaf = 0;
+    pairwise_leaves(0, n, f, leafsum, leaf, lane);
+    __syncwarp();
+    int c = 0;
+    double r = pairwise_combine(n, leafsum, c);
+    __syncwarp();
+    return r;
+}
+
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        double u = __shfl_xor_sync(SA_FULL, v, o);
+        v = (u < v) ? u : v;
+    }
+    return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        double u = __shfl_xor_sync(SA_FULL, v, o);
+        v = (u > v || u != u) ? u : v;
+    }
+    return v;
+}
+
+__device__ __forceinline__ void swapbuf(double*& a, double*& b) {
+    double* t = a;
+    a = b;
+    b = t;
+}
+
+// ---------------------------------------------------------------- operators
+// All return true when the op did arithmetic (so the kernel re-checks
+// finiteness), false for pure index moves / no-ops.
+
+// basic.py:41-44 Jitter, basic.py:356-359 InjectNoise(gaussian):
+// y = x + (0.0 + sigma * z)
+__device__ bool op_gauss(const DevStage& st, WStream& s, double*& cur, double*& oth, int& L, Warp& w) {
+    const double sigma = st.f[0];
+    if (sigma == 0.0) return false;
+    double* x = cur;
+    normals(s, w.lane, L, [&](int k, double z) { x[k] = x[k] + (0.0 + sigma * z); });
+    __syncwarp();
+    return true;
+}
+
+// basic.py:58-60 Scale: s = 1.0 + sigma_factor * z; y = x * s
+__device__ bool op_scale(const DevStage& st, WStream& s, double*& cur, double*& oth, int& L, Warp& w) {
+    double f = 1.0 + st.f[0] * std_normal(s, w.lane);
+    for (int t = w.lane; t < L; t += 32) cur[t] = cur[t] * f;
+    __syncwarp();
+    return true;
+}
+
+// basic.py:70-71 Rotate: -x
+__device__ bool op_rotate(double*& cur, int L, Warp& w) {
+    for (int t = w.lane; t < L; t += 32) cur[t] = -cur[t];
+    __syncwarp();
+    return false;
+}
+
+// basic.py:95-104 PermuteSegments
+__device__ bool op_permute(const DevStage& st, WStream& s, double*& cur, double*& oth, int& L, Warp& w) {
+    const int n = (int)st.i[0];
+    if (n == 1) return false;
+    int32_t* order = w.iscr;
+    for (int k = w.lane; k < n; k += 32) order[k] = k;
+    __syncwarp();
+    for (int i = n - 1; i > 0; --i) {  // Generator.permutation: Fisher-Yates
+        int j = (int)interval(s, w.lane, (uint32_t)i);
+        if (w.lane == 0) {
+            int32_t t = order[i];
+            order[i] = order[j];
+            order[j] = t;
+        }
+        __syncwarp();
+    }
+    const int base = L / n, extra = L % n;
+    int o = 0;
+    for (int q = 0; q < n; ++q) {
+        int k = order[q];
+        int off = k * base + (k < extra ? k : extra);
+        int sz = base + (k < extra ? 1 : 0);
+        for (int u = w.lane; u < sz; u += 32) oth[o + u] = cur[off + u];
+        o += sz;
+    }
+    __syncwarp();
+    swapbuf(cur, oth);
+    return false;
+}
+
+// basic.py:133-135 Crop: start = integers(0, L - size + 1)
+__device__ bool op_crop(const DevStage& st, WStream& s, double*& cur, double*& oth, int& L, Warp& w) {
+    const int size = (int)st.i[0];
+    const int start = (int)bounded(s, w.lane, (uint32_t)(L - size));
+    for (int t = w.lane; t < size; t += 32) oth[t] = cur[start + t];
+    __syncwarp();
+    swapbuf(cur, oth);
+    L = size;
+    return false;
+}
+
+// basic.py:145-146 Reverse
+__device__ bool op_reverse(double*& cur, double*& oth, int L, Warp& w) {
+    for (int t = w.lane; t < L; t += 32) oth[t] = cur[L - 1 - t];
+    __syncwarp();
+    swapbuf(cur, oth);
+    return false;
+}
+
+// basic.py:174-177 Resize: interp(linspace(0, L-1, T), arange(L), x)
+__device__ bool op_resize(const DevStage& st, double*& cur, double*& oth, int& L, Warp& w) {
+    const int T = (int)st.i[0];
+    if (T == L) return false;
+    for (int t = w.lane; t < T; t += 32)
+        oth[t] = interp_grid(linspace_at(0.0, (double)L - 1.0, T, t), cur, L);
+    __syncwarp();
+    swapbuf(cur, oth);
+    L = T;
+    return true;
+}
+
+// basic.py:196-207 Quantize / snap_to_levels
+__device__ bool op_quantize(const DevStage& st, double*& cur, int L, Warp& w) {
+    double lo = cur[0], hi = cur[0];
+    for (int t = w.lane; t < L; t += 32) {
+        double v = cur[t];
+        lo = (v < lo) ? v : lo;
+        hi = (v > hi) ? v : hi;
+    }
+    lo = warp_min(lo);
+    hi = warp_max(hi);
+    if (hi == lo) return false;
+    const double step = (hi - lo) / (double)(st.i[0] - 1);
+    const double top = (double)(st.i[0] - 1);
+    for (int t = w.lane; t < L; t += 32) {
+        double idx = ceil((cur[t] - lo) / step - 0.5);
+        if (idx < 0.0) idx = 0.0;
+        if (idx > top) idx = top;
+        cur[t] = lo + idx * step;
+    }
+    __syncwarp();
+    return true;
+}
+
+// basic.py:227-241 Drift
+__device__ bool op_drift(const DevStage& st, WStream& s, double*& cur, int L, Warp& w) {
+    const double md = st.f[0];
+    if (md == 0.0) return false;
+    const int np_ = (int)st.i[0];
+    double* anchors = w.small;
+    double* pos = w.small + np_;
+    for (int k = 0; k < np_; ++k) {
+        double a = 0.0 + 1.0 * std_normal(s, w.lane);
+        if (w.lane == 0) anchors[k] = a;
+    }
+    for (int k = w.lane; k < np_; k += 32) pos[k] = linspace_at(0.0, (double)L - 1.0, np_, k);
+    __syncwarp();
+    const double c0 = interp1(0.0, pos, anchors, np_);
+    double peak = 0.0;
+    for (int t = w.lane; t < L; t += 32) {
+        double a = fabs(interp1((double)t, pos, anchors, np_) - c0);
+        peak = (a > peak || a != a) ? a : peak;
+    }
+    peak = warp_max(peak);
+    if (peak == 0.0) return false;
+    for (int t = w.lane; t < L; t += 32) {
+        double c = interp1((double)t, pos, anchors, np_) - c0;
+        cur[t] = cur[t] + (c / peak) * md;
+    }
+    __syncwarp();
+    return true;
+}
+
+// basic.py:352-355 InjectNoise(uniform): x + uniform(-hw, hw)
+__device__ bool op_uniform(const DevStage& st, WStream& s, double*& cur, int L, Warp& w) {
+    const double hw = st.f[0];
+    if (hw == 0.0) return false;
+    const double lo = -hw, range = hw - lo;
+    double* x = cur;
+    doubles(s, w.lane, L, [&](int k, double u) { x[k] = x[k] + (lo + range * u); });
+    __syncwarp();
+    return true;
+}
+
+// Generator.choice(L, k, replace=False) into idx[0..k) (int32 scratch).
+__device__ void choice_noreplace(WStream& s, int lane, int pop, int k, int32_t* iscr, int32_t* idx) {
+    if (pop > 10000 && k > pop / 50) {  // tail shuffle of arange(pop)
+        int32_t* a = iscr;
+        for (int t = lane; t < pop; t += 32) a[t] = t;
+        __syncwarp();
+        int first = pop - k > 1 ? pop - k : 1;
+        for (int i = pop - 1; i >= first; --i) {
+            int j = (int)bounded(s, lane, (uint32_t)i);
+            if (lane == 0) {
+                int32_t t = a[i];
+                a[i] = a[j];
+                a[j] = t;
+            }
+            __syncwarp();
+        }
+        for (int t = lane; t < k; t += 32) idx[t] = a[pop - k + t];
+        __syncwarp();
+        return;
+    }
+    uint32_t mask = (uint32_t)(1.2 * (double)k);
+    mask |= mask >> 1; mask |= mask >> 2; mask |= mask >> 4; mask |= mask >> 8; mask |= mask >> 16;
+    uint32_t* hs = reinterpret_cast<uint32_t*>(iscr);
+    for (uint32_t t = lane; t <= mask; t += 32) hs[t] = 0xffffffffu;
+    __syncwarp();
+    for (int j = pop - k; j < pop; ++j) {
+        uint32_t val = bounded(s, lane, (uint32_t)j);
+        uint32_t loc = val & mask;
+        while (hs[loc] != 0xffffffffu && hs[loc] != val) loc = (loc + 1) & mask;
+        int32_t pick;
+        if (hs[loc] == 0xffffffffu) {
+            pick = (int32_t)val;
+        } else {
+            loc = (uint32_t)j & mask;
+            while (hs[loc] != 0xffffffffu) loc = (loc + 1) & mask;
+            val = (uint32_t)j;
+            pick = j;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            hs[loc] = val;
+            idx[j - pop + k] = pick;
+        }
+        __syncwarp();
+    }
+    for (int i = k - 1; i > 0; --i) {
+        int j = (int)bounded(s, lane, (uint32_t)i);
+        if (lane == 0) {
+            int32_t t = idx[i];
+            idx[i] = idx[j];
+            idx[j] = t;
+        }
+        __syncwarp();
+    }
+}
+
+// basic.py:360-370 InjectNoise(spike)
+__device__ bool op_spike(const DevStage& st, WStream& s, double*& cur, int L, Warp& w) {
+    const int cnt = (int)st.i[0];
+    const double mag = st.f[0];
+    if (cnt == 0 || mag == 0.0) return false;
+    const double* x = cur;
+    double mean = pairwise_warp(L, [&](int t) { return x[t]; }, w.small, w.lane) / (double)L;
+    double var = pairwise_warp(
+                     L, [&](int t) { double d = x[t] - mean; return d * d; }, w.small, w.lane) /
+                 (double)L;
+    double scale = sqrt(var);
+    if (scale == 0.0) scale = 1.0;
+    // hash set / tail array first, picks after it
+    uint32_t mask = (uint32_t)(1.2 * (double)cnt);
+    mask |= mask >> 1; mask |= mask >> 2; mask |= mask >> 4; mask |= mask >> 8; mask |= mask >> 16;
+    int scr = (L > 10000 && cnt > L / 50) ? L : (int)mask + 1;
+    int32_t* idx = w.iscr + scr;
+    choice_noreplace(s, w.lane, L, cnt, w.iscr, idx);
+    for (int q = 0; q < cnt; ++q) {
+        double sign = (double)((int64_t)bounded(s, w.lane, 1u) * 2 - 1);
+        if (w.lane == 0) {
+            int p = idx[q];
+            cur[p] = cur[p] + (sign * mag) * scale;
+        }
+    }
+    __syncwarp();
+    return true;
+}
+
+// basic.py:371-375 InjectNoise(slope_trend)
+__device__ bool op_slope(const DevStage& st, WStream& s, double*& cur, int L, Warp& w) {
+    const double mo = st.f[0];
+    if (mo == 0.0) return false;
+    const double sign = next_double(s, w.lane) < 0.5 ? 1.0 : -1.0;
+    const double stop = sign * mo;
+    for (int t = w.lane; t < L; t += 32) cur[t] = cur[t] + linspace_at(0.0, stop, L, t);
+    __syncwarp();
+    return true;
+}
+
+// warp.py:25-47 warp_positions: builds knots (small[0..n)) and warped
+// (small[n..2n)); returns false if the map is not strictly increasing.
+__device__ bool warp_knots(int len, int nk, double intensity, WStream& s, Warp& w) {
+    const double span = (double)len - 1.0;
+    double* knots = w.small;
+    double* warped = w.small + nk;
+    double* tmp = w.small + 2 * nk;
+    const double spacing = span / (double)(nk - 1);
+    for (int k = w.lane; k < nk; k += 32) knots[k] = linspace_at(0.0, span, nk, k);
+    __syncwarp();
+    const int ni = nk - 2;
+    for (int k = 0; k < ni; ++k) {
+        double v = knots[k + 1] + (0.0 + (intensity * spacing) * std_normal(s, w.lane));
+        if (w.lane == 0) tmp[k] = v;
+    }
+    __syncwarp();
+    if (w.lane == 0) {
+        for (int a = 1; a < ni; ++a) {  // np.sort (values)
+            double v = tmp[a];
+            int b = a - 1;
+            while (b >= 0 && tmp[b] > v) {
+                tmp[b + 1] = tmp[b];
+                --b;
+            }
+            tmp[b + 1] = v;
+        }
+        double prev = 0.0, acc = 0.0;
+        warped[0] = 0.0;
+        for (int k = 1; k < nk; ++k) {
+            double cur = (k == nk - 1) ? span : tmp[k - 1];
+            if (k < nk - 1) {  // np.clip(sorted, 0, span)
+                if (cur < 0.0) cur = 0.0;
+                if (cur > span) cur = span;
+            }
+            double g = cur - prev;
+            if (!(g >= 1e-6)) g = (g != g) ? g : 1e-6;
+            prev = cur;
+            acc = acc + g;
+            warped[k] = acc;
+        }
+        const double f = span / warped[nk - 1];
+        for (int k = 0; k < nk; ++k) warped[k] = warped[k] * f;
+        warped[nk - 1] = span;
+    }
+    __syncwarp();
+    bool ok = true;
+    for (int k = 1; k < nk; ++k) ok = ok && !(warped[k] - warped[k - 1] <= 0);
+    return ok;
+}
+
+// warp.py:73-76 TimeWarp
+__device__ bool op_time_warp(const DevStage& st, WStream& s, double*& cur, double*& oth, int L, Warp& w,
+                             uint32_t& flags) {
+    if (st.f[0] == 0.0) return false;
+    const int nk = (int)st.i[0];
+    if (!warp_knots(L, nk, st.f[0], s, w)) {
+        flags |= SA_FLAG_WARP_MONOTONE;
+        return false;
+    }
+    const double* knots = w.small;
+    const double* warped = w.small + nk;
+    for (int t = w.lane; t < L; t += 32)
+        oth[t] = interp_grid(interp1((double)t, knots, warped, nk), cur, L);
+    __syncwarp();
+    swapbuf(cur, oth);
+    return true;
+}
+
+// warp.py:108-118 WindowWarp
+__device__ bool op_window_warp(const DevStage& st, WStream& s, double*& cur, double*& oth, int L, Warp& w,
+                               uint32_t& flags) {
+    if (st.f[0] == 0.0) return false;
+    const int wsz = (int)st.i[0];
+    const int nk = (int)st.i[1];
+    const int start = (wsz == L) ? 0 : (int)bounded(s, w.lane, (uint32_t)(L - wsz));
+    if (!warp_knots(wsz, nk, st.f[0], s, w)) {
+        flags |= SA_FLAG_WARP_MONOTONE;
+        return false;
+    }
+    const double* knots = w.small;
+    const double* warped = w.small + nk;
+    const double* win = cur + start;
+    for (int t = w.lane; t < L; t += 32) {
+        int u = t - start;
+        oth[t] = (u >= 0 && u < wsz) ? interp_grid(interp1((double)u, knots, warped, nk), win, wsz) : cur[t];
+    }
+    __syncwarp();
+    swapbuf(cur, oth);
+    return true;
+}
+
+// BASELINE M2 Dropout
+__device__ bool op_dropout(const DevStage& st, WStream& s, double*& cur, int L, Warp& w) {
+    const double rate = st.f[0], fill = st.f[1];
+    if (rate == 0.0) return false;
+    double* x = cur;
+    doubles(s, w.lane, L, [&](int k, double u) {
+        if (u < rate) x[k] = fill;
+    });
+    __syncwarp();
+    return false;
+}
+
+// BASELINE M3 Pool
+__device__ bool op_pool(const DevStage& st, double*& cur, int L, Warp& w) {
+    const int P = (int)st.i[0];
+    if (P == 1) return false;
+    const int red = (int)st.i[1];
+    const int nb = (L + P - 1) / P;
+    for (int b = w.lane; b < nb; b += 32) {
+        int b0 = b * P, b1 = b0 + P < L ? b0 + P : L;
+        double v;
+        if (red == 0) {
+            double acc = 0.0;
+            for (int u = b0; u < b1; ++u) acc = acc + cur[u];
+            v = acc / (double)(b1 - b0);
+        } else if (red == 1) {
+            v = cur[b0];
+            for (int u = b0 + 1; u < b1; ++u) v = (cur[u] > v) ? cur[u] : v;
+        } else {
+            v = cur[b0];
+            for (int u = b0 + 1; u < b1; ++u) v = (cur[u] < v) ? cur[u] : v;
+        }
+        for (int u = b0; u < b1; ++u) cur[u] = v;
+    }
+    __syncwarp();
+    return red == 0;
+}
+
+// BASELINE M4 Convolve (taps in params.aux)
+__device__ bool op_convolve(const DevStage& st, const double* aux, double*& cur, double*& oth, int L, Warp& w) {
+    const double* taps = aux + st.aux_off;
+    const int S = st.aux_len, h = S / 2;
+    for (int t = w.lane; t < L; t += 32) {
+        double acc = 0.0;
+        for (int k = 0; k < S; ++k) {
+            int u = t + k - h;
+            u = u < 0 ? 0 : (u > L - 1 ? L - 1 : u);
+            acc = acc + taps[k] * cur[u];
+        }
+        oth[t] = acc;
+    }
+    __syncwarp();
+    swapbuf(cur, oth);
+    return true;
+}
+
+// BASELINE M5 SpeedWarp
+__device__ bool op_speed_warp(const DevStage& st, WStream& s, double*& cur, double*& oth, int L, Warp& w) {
+    const int K = (int)st.i[0];
+    const double R = st.f[0];
+    if (K == 0 || R == 1.0) return false;
+    const int segs = K + 1;
+    double* speeds = w.small;
+    double* base = w.small + segs;
+    const double lo = 1.0, range = R - lo;
+    for (int m = 0; m < segs; ++m) {
+        double v = lo + range * next_double(s, w.lane);
+        if (w.lane == 0) speeds[m] = v;
+    }
+    __syncwarp();
+    if (w.lane == 0) {
+        double acc = 0.0;
+        base[0] = 0.0;
+        for (int m = 0; m < K; ++m) {
+            int sb = (int)(((int64_t)m * L + K) / segs);
+            int sn = (int)(((int64_t)(m + 1) * L + K) / segs);
+            acc = acc + speeds[m] * (double)(sn - sb);
+            base[m + 1] = acc;
+        }
+    }
+    __syncwarp();
+    auto tau_raw = [&](int t) {
+        int m = (int)(((int64_t)t * segs) / L);
+        int sb = (int)(((int64_t)m * L + K) / segs);
+        return base[m] + speeds[m] * (double)(t - sb);
+    };
+    const double f = ((double)L - 1.0) / tau_raw(L - 1);
+    const bool cubic = st.i[1] != 0;
+    for (int t = w.lane; t < L; t += 32) {
+        double tau = (t == L - 1) ? (double)L - 1.0 : tau_raw(t) * f;
+        double y;
+        if (tau >= (double)(L - 1)) {
+            y = cur[L - 1];
+        } else if (tau <= 0.0) {
+            y = cur[0];
+        } else {
+            int j = (int)floor(tau);
+            if (j > L - 2) j = L - 2;
+            double fr = tau - (double)j;
+            if (cubic) {
+                double p0 = cur[j > 0 ? j - 1 : 0], p1 = cur[j], p2 = cur[j + 1];
+                double p3 = cur[j + 2 < L ? j + 2 : L - 1];
+                double a = ((-0.5 * p0 + 1.5 * p1) - 1.5 * p2) + 0.5 * p3;
+                double b = ((p0 - 2.5 * p1) + 2.0 * p2) - 0.5 * p3;
+                double c = -0.5 * p0 + 0.5 * p2;
+                y = ((a * fr + b) * fr + c) * fr + p1;
+            } else {
+                y = cur[j] + (cur[j + 1] - cur[j]) * fr;
+            }
+        }
+        oth[t] = y;
+    }
+    __syncwarp();
+    swapbuf(cur, oth);
+    return true;
+}
+
+__device__ __forceinline__ bool spectral_noop(const DevStage& st) {
+    if (st.op == SA_OP_APP) return st.f[0] == 0.0 && st.f[1] == 0.0;
+    if (st.op == SA_OP_FREQ_MASK) return st.i[0] == 0;
+    return st.f[0] == 0.0;  // SINUSOID
+}
+
+// freqaugment.py:106-170 (+ BASELINE M6): perturb the half spectrum X[0..bins)
+// (interleaved complex, smem); scratch holds >= bins doubles.
+__device__ void perturb_spectrum(const DevStage& st, WStream& s, double2* X, int L, double* scratch, Warp& w) {
+    const int bins = L / 2 + 1;
+    if (st.op == SA_OP_APP) {
+        const double sa = st.f[0], sp = st.f[1];
+        double* amp = scratch;
+        const bool even = (L % 2 == 0);
+        const int hi = even ? bins - 1 : bins;
+        normals(s, w.lane, bins, [&](int k, double z) { amp[k] = 0.0 + sa * z; });
+        __syncwarp();
+        normals(s, w.lane, bins, [&](int b, double z) {
+            double ph = 0.0 + sp * z;
+            if (b >= 1 && b < hi) {
+                double2 v = X[b];
+                double r = hypot(v.x, v.y);
+                double th = atan2(v.y, v.x) + ph;
+                r = r + amp[b];
+                if (!(r >= 0.0)) r = (r != r) ? r : 0.0;
+                double sn, cs;
+                sincos(th, &sn, &cs);
+                X[b] = make_double2(r * cs, r * sn);
+            }
+        });
+        __syncwarp();
+        if (w.lane == 0) {
+            for (int q = 0; q < (even ? 2 : 1); ++q) {
+                int b = q == 0 ? 0 : bins - 1;
+                double re = X[b].x;
+                double sign = re >= 0 ? 1.0 : -1.0;
+                double v = fabs(re) + amp[b];
+                double mv = (v >= 0.0) ? v : 0.0;
+                X[b] = make_double2(sign * mv, 0.0);
+            }
+        }
+        __syncwarp();
+    } else if (st.op == SA_OP_FREQ_MASK) {
+        const int wd = (int)st.i[0];
+        int c = (int)bounded(s, w.lane, (uint32_t)(bins - 1));
+        int start = c - wd / 2;
+        if (start < 0) start = 0;
+        if (start > bins - wd) start = bins - wd;
+        for (int k = start + w.lane; k < start + wd; k += 32) X[k] = make_double2(0.0, 0.0);
+        __syncwarp();
+    } else {  // SA_OP_SINUSOID
+        const int mb = (int)st.i[0];
+        const int b = mb + (int)bounded(s, w.lane, (uint32_t)(bins - mb - 1));
+        const double phi = (2.0 * 3.14159265358979323846) * next_double(s, w.lane);
+        const double A = st.f[0];
+        if (w.lane == 0) {
+            double2 v = X[b];
+            if (b == 0 || (L % 2 == 0 && b == bins - 1)) {
+                v.x = v.x + (A * (double)L) * cos(phi);
+            } else {
+                double h = (A * (double)L) * 0.5;
+                v.x = v.x + h * cos(phi);
+                v.y = v.y + h * sin(phi);
+            }
+            X[b] = v;
+        }
+        __syncwarp();
+    }
+}
+
+// freqaugment.py:37-47 SpectralAugmenter._apply (time-domain entry)
+__device__ bool op_spectral(const DevStage& st, WStream& s, double*& cur, double*& oth, int L, Warp& w) {
+    if (spectral_noop(st)) return false;
+    double2* X = rfft_warp(cur, oth, L, st.tw, w.lane);
+    double* free_buf = (reinterpret_cast<double*>(X) == cur) ? oth : cur;
+    perturb_spectrum(st, s, X, L, free_buf, w);
+    double2* other = reinterpret_cast<double2*>(free_buf);
+    double* y = irfft_warp(X, other, L, st.tw, w.lane);
+    if (y != cur) swapbuf(cur, oth);
+    return true;
+}
+
+}  // namespace sa

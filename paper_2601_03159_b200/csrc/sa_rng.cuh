@@ -1,0 +1,298 @@
+// sa_rng.cuh -- numpy-exact random streams on the device, one warp per stream.
+//
+// Reference: every draw of the reference comes from
+// np.random.Generator(np.random.Philox(key)) with key = derive_stream(
+// master_seed, stage j, series i) (reference core.py:71-82).  This file
+// restates, for sm_100a, numpy 2.3.5's Philox4x64-10 bit generator and the
+// Generator primitives the reference calls (random / normal / uniform /
+// integers / permutation / choice), bit-for-bit:
+//
+//   * Philox is counter based: block b of a fresh stream is philox(key,
+//     counter = b + 1) and yields words 4b..4b+3.  A warp therefore fills a
+//     128-word WINDOW with one block per lane, in parallel.
+//   * 32-bit draws (integers / permutation / choice) use numpy's buffered
+//     upper half: a 64-bit word serves two 32-bit draws, low half first, and
+//     the buffered half survives intervening 64-bit draws.
+//   * The ziggurat normal consumes a data-dependent number of words (one on
+//     the fast path, 99.3%; more on the wedge / tail paths).  normals() walks
+//     a window with a warp-wide min-reduction to find the next slow word:
+//     the run of fast words before it becomes normals in parallel (output
+//     index = position offset), the slow word is resolved uniformly by all
+//     lanes with the reference's exact arithmetic, and the walk continues.
+//
+// Every lane of the warp holds an identical copy of the stream state (all
+// control flow on it is warp-uniform); only emitted values are lane-private.
+// FP expressions are written in the reference's evaluation order and the
+// translation unit is compiled with -fmad=false (no FMA contraction).
+// Known deviation: the ziggurat TAIL (idx 0 and rabs >= ki[0], 2.6e-4 of
+// normals) evaluates log1p; CUDA's log1p and glibc's may differ by 1 ulp, so
+// those samples match the reference to <= 1 ulp rather than bitwise.
+#pragma once
+#include <stdint.h>
+#include "zig_tables.h"
+
+#define SA_FULL 0xffffffffu
+#define SA_WIN 128  // words per window (32 lanes x 4 words per Philox block)
+
+namespace sa {
+
+struct ZigEntry {  // packed fast-path table: one 16 B load per word
+    uint64_t ki;
+    double wi;
+};
+
+// Device copies of numpy's tables (filled once by sa_init, csrc/sa_capi.cu).
+__device__ ZigEntry g_zig[256];
+__device__ double g_fi[256];
+
+static constexpr double kZigR = 3.6541528853610088;
+static constexpr double kZigInvR = 0.27366123732975828;
+static constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ULL;
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {  // core.py:40-45
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+// core.py:77-82
+__device__ __forceinline__ void derive_key(uint64_t seed, uint64_t j, uint64_t i, uint64_t& k0,
+                                           uint64_t& k1) {
+    uint64_t s = mix64(seed);
+    s = mix64(s + kGolden + j);
+    s = mix64(s + kGolden + i);
+    k0 = mix64(s);
+    k1 = mix64(s + kGolden);
+}
+
+// 64x64 -> 128 multiply from four 32x32->64 IMAD.WIDE products.
+__device__ __forceinline__ void mulhilo64(uint64_t a, uint64_t b, uint64_t& hi, uint64_t& lo) {
+    lo = a * b;
+    hi = __umul64hi(a, b);
+}
+
+// numpy Philox4x64-10: Random123 round, Weyl key schedule.
+__device__ __forceinline__ void philox(uint64_t k0, uint64_t k1, uint64_t ctr0, uint64_t& o0,
+                                       uint64_t& o1, uint64_t& o2, uint64_t& o3) {
+    uint64_t c0 = ctr0, c1 = 0, c2 = 0, c3 = 0;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r) {
+            k0 += 0x9E3779B97F4A7C15ULL;
+            k1 += 0xBB67AE8584CAA73BULL;
+        }
+        uint64_t hi0, lo0, hi1, lo1;
+        mulhilo64(0xD2E7470EE14C6C93ULL, c0, hi0, lo0);
+        mulhilo64(0xCA5A826395121157ULL, c2, hi1, lo1);
+        uint64_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+        c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+    }
+    o0 = c0; o1 = c1; o2 = c2; o3 = c3;
+}
+
+__device__ __forceinline__ double u53(uint64_t w) {  // Generator.random()
+    return (double)(w >> 11) * (1.0 / 9007199254740992.0);
+}
+
+// Warp-uniform stream state.  `win` points at the words currently buffered:
+// either the 4 words of block 0 cached by the gate pre-pass (wn = 4) or the
+// warp's 128-word window (wn = SA_WIN).
+struct WStream {
+    uint64_t k0, k1;
+    uint64_t wpos;  // absolute index of the next 64-bit word
+    uint64_t wb;    // absolute index of win[0]
+    uint32_t wn;
+    uint32_t has32, u32;
+    const uint64_t* win;
+    uint64_t* winbuf;  // the warp's window storage (SA_WIN words, smem)
+};
+
+// Refill the window with the 32 blocks starting at the block holding wpos.
+__device__ __forceinline__ void refill(WStream& s, int lane) {
+    uint64_t blk0 = s.wpos >> 2;
+    uint64_t o0, o1, o2, o3;
+    philox(s.k0, s.k1, blk0 + (uint64_t)lane + 1, o0, o1, o2, o3);
+    __syncwarp();  // every lane is done reading the previous window
+    ulonglong2* w2 = reinterpret_cast<ulonglong2*>(s.winbuf) + 2 * lane;
+    w2[0] = make_ulonglong2(o0, o1);
+    w2[1] = make_ulonglong2(o2, o3);
+    __syncwarp();
+    s.win = s.winbuf;
+    s.wb = blk0 << 2;
+    s.wn = SA_WIN;
+}
+
+__device__ __forceinline__ uint64_t next64(WStream& s, int lane) {
+    if (s.wpos >= s.wb + s.wn) refill(s, lane);
+    uint64_t v = s.win[s.wpos - s.wb];
+    s.wpos += 1;
+    return v;
+}
+
+__device__ __forceinline__ uint32_t next32(WStream& s, int lane) {
+    if (s.has32) {
+        s.has32 = 0;
+        return s.u32;
+    }
+    uint64_t v = next64(s, lane);
+    s.has32 = 1;
+    s.u32 = (uint32_t)(v >> 32);
+    return (uint32_t)v;
+}
+
+__device__ __forceinline__ double next_double(WStream& s, int lane) { return u53(next64(s, lane)); }
+
+// Generator.integers(0, rng + 1): numpy random_bounded_uint64, 32-bit Lemire.
+__device__ __forceinline__ uint32_t bounded(WStream& s, int lane, uint32_t rng) {
+    if (rng == 0) return 0;
+    if (rng == 0xFFFFFFFFu) return next32(s, lane);
+    uint32_t ex = rng + 1u;
+    uint64_t m = (uint64_t)next32(s, lane) * ex;
+    uint32_t left = (uint32_t)m;
+    if (left < ex) {
+        uint32_t th = (0u - ex) % ex;
+        while (left < th) {
+            m = (uint64_t)next32(s, lane) * ex;
+            left = (uint32_t)m;
+        }
+    }
+    return (uint32_t)(m >> 32);
+}
+
+// numpy random_interval (masked rejection), used by Generator.permutation.
+__device__ __forceinline__ uint32_t interval(WStream& s, int lane, uint32_t max) {
+    if (max == 0) return 0;
+    uint32_t mask = max;
+    mask |= mask >> 1; mask |= mask >> 2; mask |= mask >> 4; mask |= mask >> 8; mask |= mask >> 16;
+    uint32_t v;
+    while ((v = (next32(s, lane) & mask)) > max) {
+    }
+    return v;
+}
+
+// Slow path of the ziggurat for a word that failed the fast test; returns
+// true and the value if a normal is produced (else the caller retries).
+__device__ __noinline__ bool zig_slow(WStream& s, int lane, uint64_t r0, double& out) {
+    int idx = (int)(r0 & 0xff);
+    uint64_t r = r0 >> 8;
+    int sign = (int)(r & 1);
+    uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
+    double x = (double)rabs * g_zig[idx].wi;
+    if (sign) x = -x;
+    if (idx == 0) {
+        for (;;) {
+            double xx = -kZigInvR * log1p(-next_double(s, lane));
+            double yy = -log1p(-next_double(s, lane));
+            if (yy + yy > xx * xx) {
+                out = ((rabs >> 8) & 1) ? -(kZigR + xx) : kZigR + xx;
+                return true;
+            }
+        }
+    }
+    double u = next_double(s, lane);
+    if (((g_fi[idx - 1] - g_fi[idx]) * u + g_fi[idx]) < exp(-0.5 * x * x)) {
+        out = x;
+        return true;
+    }
+    return false;
+}
+
+// One standard normal, warp-uniform (all lanes get the same value).
+__device__ __forceinline__ double std_normal(WStream& s, int lane) {
+    for (;;) {
+        uint64_t r0 = next64(s, lane);
+        int idx = (int)(r0 & 0xff);
+        uint64_t r = r0 >> 8;
+        uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
+        ZigEntry ze = g_zig[idx];
+        if (rabs < ze.ki) {
+            double x = (double)rabs * ze.wi;
+            return (r & 1) ? -x : x;
+        }
+        double v;
+        if (zig_slow(s, lane, r0, v)) return v;
+    }
+}
+
+// `count` standard normals in stream order; emit(k, z) is called exactly
+// once per k by exactly one lane (k = normal index 0..count-1).
+template <class Emit>
+__device__ __forceinline__ void normals(WStream& s, int lane, int count, Emit&& emit) {
+    int k = 0;
+    while (k < count) {
+        if (s.wpos >= s.wb + s.wn) refill(s, lane);
+        const uint32_t wn = s.wn;
+        uint32_t sp = (uint32_t)(s.wpos - s.wb);
+        // classify this lane's words (positions 4*lane + r of the window)
+        double z[4];
+        uint32_t slowbits = 0;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            uint32_t p = 4u * lane + r;
+            uint64_t w = p < wn ? s.win[p] : 0;
+            int idx = (int)(w & 0xff);
+            uint64_t rr = w >> 8;
+            uint64_t rabs = (rr >> 1) & 0x000fffffffffffffULL;
+            ZigEntry ze = g_zig[idx];
+            double x = (double)rabs * ze.wi;
+            z[r] = (rr & 1) ? -x : x;
+            if (p < wn && !(rabs < ze.ki)) slowbits |= 1u << r;
+        }
+        for (;;) {
+            uint32_t mine = 0xffffffffu;
+#pragma unroll
+            for (int r = 3; r >= 0; --r) {
+                uint32_t p = 4u * lane + r;
+                if (((slowbits >> r) & 1u) && p >= sp) mine = p;
+            }
+            uint32_t t = __reduce_min_sync(SA_FULL, mine);
+            if (t > wn) t = wn;
+            uint32_t nf = t - sp;
+            if (nf > (uint32_t)(count - k)) nf = (uint32_t)(count - k);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                uint32_t p = 4u * lane + r;
+                if (p >= sp && p < sp + nf) emit(k + (int)(p - sp), z[r]);
+            }
+            k += (int)nf;
+            sp += nf;
+            if (k >= count || sp >= wn) {
+                s.wpos = s.wb + sp;
+                break;
+            }
+            // slow word at sp: resolve uniformly
+            uint64_t r0 = s.win[sp];
+            s.wpos = s.wb + sp + 1;
+            uint64_t old_wb = s.wb;
+            double v;
+            if (zig_slow(s, lane, r0, v)) {
+                if (lane == 0) emit(k, v);
+                k += 1;
+            }
+            if (k >= count || s.wb != old_wb) break;
+            sp = (uint32_t)(s.wpos - s.wb);
+            if (sp >= wn) break;
+        }
+    }
+}
+
+// `count` doubles random() in stream order; emit(k, u) once per k.
+template <class Emit>
+__device__ __forceinline__ void doubles(WStream& s, int lane, int count, Emit&& emit) {
+    int k = 0;
+    while (k < count) {
+        if (s.wpos >= s.wb + s.wn) refill(s, lane);
+        uint32_t sp = (uint32_t)(s.wpos - s.wb);
+        uint32_t avail = s.wn - sp;
+        uint32_t take = avail < (uint32_t)(count - k) ? avail : (uint32_t)(count - k);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            uint32_t p = 4u * lane + r;
+            if (p >= sp && p < sp + take) emit(k + (int)(p - sp), u53(s.win[p]));
+        }
+        k += (int)take;
+        s.wpos += take;
+    }
+}
+
+}  // namespace sa
