@@ -1,0 +1,350 @@
+#!/usr/bin/env python
+"""Benchmark of the fused B200 augmentation pipeline (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl b200|reference]
+
+One "step" = one pass of the whole augmentation chain over the batch of the
+chosen BASELINE config (default: config 5, the full pipeline of every
+augmenter at p=0.5 on 1,000,000 x 1,024 float64 series, the configuration the
+metric "pipeline at 1/2/4/8 B200" is quoted on).  The batch is sharded by
+contiguous series ranges across ranks (no data-path collective; torch.distributed
+is used only for the barrier and the max-over-ranks of the timings), so total
+work is fixed as N grows ("strong" scaling).
+
+value  = output points (all ranks) / max-over-ranks device time, inputs resident
+         in HBM, CUDA events on the launching stream.
+e2e    = same metric through the host-buffer C ABI call (sa_pipeline_run_host)
+         from pinned host memory: H2D + kernels + D2H inside the timed region.
+roofline.achieved = algorithmic bytes 8*(n*L_in + n_out*L_out) per launch /
+         mean kernel duration (per GPU); peak = MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline = the C oracle (a restatement of the reference's algorithm) on a
+         bounded sample of the same workload, all host cores, rank 0 at N=1.
+--impl reference times that CPU implementation alone (rank 0) on the same
+         config and prints the same line with "impl": "reference".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "augmented points/sec"
+UNIT = "points/s"
+
+WORKLOADS = {
+    1: "config1: AddNoise/Jitter(sigma=0.05) on 1,000 x 512 sum-of-sinusoids",
+    2: "config2: Crop(819)->Drift->Quantize(16)->Dropout(0.05)->Pool(4)->Reverse (p=0.5) on 10,000 x 1,024 walks",
+    3: "config3: rfft->FrequencyMask(10% bins)->random-phase sinusoid->irfft on 50,000 x 2,048 AR(2)",
+    4: "config4: SpeedWarp(3, 3.0, cubic)->Resize(1500)->Convolve(hann,7) on 100,000 x 1,500 walk+sine",
+    5: "config5: all 20 length-preserving augmenters at p=0.5 on 1,000,000 x 1,024 walks (8.2 GB)",
+}
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(cfg):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        v = d.get(f"config{cfg}")
+        if v:
+            return v
+    return None
+
+
+def cpu_baseline(cfg: int, pipe, L_in: int, target_s: float = 8.0, threads: int | None = None):
+    """The C oracle (reference algorithm restated, oracle/sa_oracle.c) on a
+    bounded sample of the workload, all host threads."""
+    from bench_inputs import host_input
+    from oracle import oracle as O
+
+    threads = threads or os.cpu_count() or 1
+    probe = host_input(cfg, n=max(64, 8 * threads))
+    t0 = time.perf_counter()
+    O.run_pipeline(pipe, probe, threads=threads)
+    per_row = (time.perf_counter() - t0) / probe.shape[0]
+    n = int(min(max(256, target_s / max(per_row, 1e-9)), 200_000))
+    x = host_input(cfg, n=n)
+    t0 = time.perf_counter()
+    out = O.run_pipeline(pipe, x, threads=threads)
+    dt = time.perf_counter() - t0
+    return {"value": out.size / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"first {n} series of {WORKLOADS[cfg].split(':')[0]} ({out.size} output points, {dt:.2f} s)"}
+
+
+def run_reference(args, rank, world):
+    from bench_inputs import CONFIG_SHAPES, host_input, pipeline
+    from oracle import oracle as O
+
+    if rank != 0:
+        return
+    cfg = args.config
+    pipe = pipeline(cfg)
+    N, L = CONFIG_SHAPES[cfg]
+    threads = os.cpu_count() or 1
+    probe = host_input(cfg, n=max(64, 8 * threads))
+    t0 = time.perf_counter()
+    O.run_pipeline(pipe, probe, threads=threads)
+    per_row = (time.perf_counter() - t0) / probe.shape[0]
+    n = int(min(N, max(256, 4.0 / max(per_row, 1e-9))))
+    x = host_input(cfg, n=n)
+    for _ in range(args.warmup):
+        O.run_pipeline(pipe, x, threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        out = O.run_pipeline(pipe, x, threads=threads)
+    dt = (time.perf_counter() - t0) / args.steps
+    v = out.size / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded; BASELINE config shapes)",
+        "config": {"workload": WORKLOADS[cfg], "sample_series": n, "len": L},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"first {n} of {N} series per step"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from bench_inputs import CONFIG_SHAPES, device_walks, host_input, pipeline
+    from paper_2601_03159_b200 import _engine, _native
+
+    cfg = args.config
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    _native.ensure_device(local_rank)
+    N, L = CONFIG_SHAPES[cfg]
+    if args.n_series:
+        N = args.n_series
+    pipe = pipeline(cfg)
+    L_out = pipe.projected_length(L)
+    r0, r1 = N * rank // world, N * (rank + 1) // world
+    n = r1 - r0
+    if cfg == 5:
+        x = device_walks(n, L, 5, dev, row0=r0)
+    else:
+        x = torch.from_numpy(host_input(cfg, n=N)[r0:r1]).to(dev)
+    rows_out = n * pipe.row_factor()
+    out = torch.empty((rows_out, L_out), dtype=torch.float64, device=dev)
+    flags = torch.zeros(1, dtype=torch.int32, device=dev)
+    lowered = _engine._lower(pipe.stages, 0, True)
+    stream = torch.cuda.Stream(device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def step():
+        _engine.launch_device(pipe.stages, x, out, flags, pipe.master_seed, series_offset=r0,
+                              stream=stream.cuda_stream, lowered=lowered)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+    torch.cuda.synchronize()
+    if int(flags.item()):
+        raise RuntimeError(f"kernel flagged {int(flags.item())}")
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)]
+    launches0 = _native.launch_count()
+    barrier()
+    torch.cuda.synchronize()
+    with Clocks(local_rank) as clk:
+        with torch.cuda.stream(stream):
+            for k in range(args.steps):
+                ev[2 * k].record(stream)
+                step()
+                ev[2 * k + 1].record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    launches = _native.launch_count() - launches0
+    step_ms = [ev[2 * k].elapsed_time(ev[2 * k + 1]) for k in range(args.steps)]
+    total_ms = ev[0].elapsed_time(ev[-1])
+    if int(flags.item()):
+        raise RuntimeError(f"kernel flagged {int(flags.item())}")
+
+    # e2e: host-buffer C ABI from pinned memory (H2D + kernel + D2H timed)
+    e2e_s = None
+    h2d = 8 * n * L
+    d2h = 8 * rows_out * L_out
+    if not args.no_e2e:
+        hin = x.cpu().pin_memory()
+        hout = torch.empty((rows_out, L_out), dtype=torch.float64).pin_memory()
+        arr, aux = lowered
+        import ctypes
+
+        def e2e_step():
+            rc = _native.lib().sa_pipeline_run_host(
+                arr, len(pipe.stages), aux.ctypes.data_as(ctypes.c_void_p), aux.size, pipe.master_seed, r0,
+                hin.data_ptr(), n, L, hout.data_ptr(), L_out)
+            _native.check(rc, "sa_pipeline_run_host")
+
+        for _ in range(max(1, min(args.warmup, 2))):
+            e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        e2e_s = (time.perf_counter() - t0) / args.steps
+        barrier()
+        # the e2e result must equal the device result
+        if not torch.equal(hout[: min(64, rows_out)].to(dev), out[: min(64, rows_out)]):
+            raise RuntimeError("e2e output differs from the device-resident output")
+
+    t = torch.tensor([total_ms / args.steps, sum(step_ms) / len(step_ms), e2e_s or 0.0, float(launches)],
+                     dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t[:3], op=dist.ReduceOp.MAX)
+        lt = t[3:].clone()
+        dist.all_reduce(lt, op=dist.ReduceOp.SUM)
+        t[3] = lt[0]
+    ms_per_step, kern_ms, e2e_max, launches_all = [float(v) for v in t.tolist()]
+    if rank != 0:
+        return
+    pts = N * pipe.row_factor() * L_out
+    value = pts / (ms_per_step / 1e3)
+    peak, peak_src = measured_peak()
+    bytes_launch = 8 * (n * L + rows_out * L_out)
+    achieved = bytes_launch / (kern_ms / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded random walks / BASELINE config distributions; no corpus available)",
+        "config": {"workload": WORKLOADS[cfg], "n_series": N, "len_in": L, "len_out": L_out,
+                   "stages": [s.kind for s in pipe.stages], "master_seed": pipe.master_seed,
+                   "parallelism": f"series-range shards x{world}, no collective",
+                   "l2": "inputs larger than L2 (no flush needed)" if 8 * n * L > 256e6 else
+                         "input smaller than L2: repeated steps may hit L2"},
+        "hbm_gbs": achieved,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": ncu_traffic(cfg), "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": bytes_launch, "kernel_ms": kern_ms},
+        "gpu_launches": int(launches_all),
+        "clocks": clk.summary(),
+    }
+    if e2e_s is not None:
+        line["e2e"] = {"value": pts / e2e_max, "unit": UNIT, "h2d_bytes_per_step": h2d * world,
+                       "d2h_bytes_per_step": d2h * world}
+    if world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(cfg, pipe, L)
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n-series", type=int, default=0, help="override the config's series count")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    rank, world, local_rank = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_b200(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

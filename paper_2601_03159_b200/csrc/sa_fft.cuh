@@ -9,7 +9,8 @@
 //                  autosort passes of radix 8/4/2 ping-ponging between two
 //                  smem buffers, then the split step
 //                  X[k] = E[k] + W_L^k O[k], k = 0..M.
-//   irfft:         the inverse split, inverse M-point FFT, 1/M scaling,
+//   irfft:         the inverse split, then the SAME forward passes on the
+//                  conjugate (IFFT(Z) = conj(FFT(conj Z))), 1/M scaling,
 //                  result read back as the real series in place.
 //
 // Twiddles come from a per-length table tw[k] = exp(-2*pi*i*k/L), k < L,
@@ -130,7 +131,7 @@ __device__ double2* fft_pow2(double2* a, double2* b, int M, const double2* tw, i
 // rfft of x (length L = 2M, in buffer xa viewed as complex) into X[0..M]
 // (M + 1 complex).  xb is scratch of the same capacity.  Returns the buffer
 // holding X (one of xa / xb); the other is free afterwards.
-__device__ double2* rfft_warp(double* xa, double* xb, int L, const double2* tw, int lane) {
+__device__ __forceinline__ double2* rfft_warp(double* xa, double* xb, int L, const double2* tw, int lane) {
     const int M = L >> 1;
     double2* za = reinterpret_cast<double2*>(xa);
     double2* zb = reinterpret_cast<double2*>(xb);
@@ -156,8 +157,9 @@ __device__ double2* rfft_warp(double* xa, double* xb, int L, const double2* tw, 
 
 // irfft of X[0..M] (in buffer X) to a real series of length L = 2M.
 // Returns the buffer holding the series (one of X / other).
-__device__ double* irfft_warp(double2* X, double2* other, int L, const double2* tw, int lane) {
+__device__ __forceinline__ double* irfft_warp(double2* X, double2* other, int L, const double2* tw, int lane) {
     const int M = L >> 1;
+    // inverse split; store conj(Z) so the forward passes compute conj(IFFT)
     for (int k = lane; k < M; k += 32) {
         double2 xk = X[k];
         double2 xc = X[M - k];
@@ -168,14 +170,14 @@ __device__ double* irfft_warp(double2* X, double2* other, int L, const double2* 
         double2 w = __ldg(&tw[k]);
         w.y = -w.y;
         double2 o = cmul(make_double2(dr, di), w);
-        other[k] = make_double2(er - o.y, ei + o.x);
+        other[k] = make_double2(er - o.y, -(ei + o.x));
     }
     __syncwarp();
-    double2* Z = fft_pow2<true>(other, X, M, tw, L, lane);
+    double2* Z = fft_pow2<false>(other, X, M, tw, L, lane);
     const double s = 1.0 / (double)M;
     for (int k = lane; k < M; k += 32) {
         double2 z = Z[k];
-        Z[k] = make_double2(z.x * s, z.y * s);
+        Z[k] = make_double2(z.x * s, -(z.y * s));
     }
     __syncwarp();
     return reinterpret_cast<double*>(Z);

@@ -83,10 +83,13 @@ __host__ __device__ inline Layout make_layout(int lcap, int ns, int small_words,
 }
 
 // ------------------------------------------------------------ the kernel
-__global__ void __launch_bounds__(32) chain_kernel(const __grid_constant__ ChainParams p) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    const int lane = threadIdx.x;
+__global__ void __launch_bounds__(512) chain_kernel(const __grid_constant__ ChainParams p) {
+    extern __shared__ __align__(16) unsigned char smem_all[];
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    const int nw = blockDim.x >> 5;
     const Layout lay = make_layout(p.lcap, p.ns, p.small_words, p.iscr_words);
+    unsigned char* smem = smem_all + (size_t)wid * lay.total;  // this warp's slice
     double* A = reinterpret_cast<double*>(smem + lay.buf_a);
     double* B = reinterpret_cast<double*>(smem + lay.buf_b);
     uint64_t* scache = reinterpret_cast<uint64_t*>(smem + lay.scache);
@@ -105,9 +108,15 @@ __global__ void __launch_bounds__(32) chain_kernel(const __grid_constant__ Chain
     const int r = p.repeat_r;
     const uint32_t in_bytes = 8u * (uint32_t)p.len_in;
 
-    for (int64_t row = blockIdx.x; row < p.rows_out; row += gridDim.x) {
-        const int64_t in_row = row / r;
+    // Rows are dealt to warps; the trip count is uniform across the CTA so
+    // the stage-boundary barriers below are reached by every warp.
+    for (int64_t base = (int64_t)blockIdx.x * nw; base < p.rows_out; base += (int64_t)gridDim.x * nw) {
+        const int64_t row = base + wid;
+        const bool active = row < p.rows_out;
+        const int64_t in_row = (active ? row : 0) / r;
         const double* src = p.in + in_row * (int64_t)p.len_in;
+        uint64_t fire_lo = 0;  // fire bits of stages 0..63
+        if (active) {
         // 1. stage the input row
         if (p.bulk_in) {
             if (lane == 0) {
@@ -119,7 +128,6 @@ __global__ void __launch_bounds__(32) chain_kernel(const __grid_constant__ Chain
             for (int t = lane; t < p.len_in; t += 32) A[t] = src[t];
         }
         // 2. gate pre-pass (overlaps the bulk copy)
-        uint64_t fire_lo = 0;  // fire bits of stages 0..63
         for (int j0 = 0; j0 < p.ns; j0 += 32) {
             const int j = j0 + lane;
             bool fire = false;
@@ -147,12 +155,14 @@ __global__ void __launch_bounds__(32) chain_kernel(const __grid_constant__ Chain
             for (int t = lane; t < p.len_in; t += 32) ok = ok && isfinite(A[t]);
             if (!__all_sync(SA_FULL, ok)) flags |= SA_FLAG_NONFINITE;
         }
-        // 3. the chain
+        }
+        // 3. the chain (stage-major across the CTA when sync_every > 0)
         double* cur = A;
         double* oth = B;
         int L = p.len_in;
         for (int j = 0; j < p.ns; ++j) {
-            if (!((fire_lo >> j) & 1ull)) continue;
+            if (p.sync_every && (j % p.sync_every) == 0) __syncthreads();
+            if (!active || !((fire_lo >> j) & 1ull)) continue;
             const DevStage& st = p.st[j];
             const uint64_t* c = scache + 6 * j;
             WStream s;
@@ -178,7 +188,7 @@ __global__ void __launch_bounds__(32) chain_kernel(const __grid_constant__ Chain
                 case SA_OP_QUANTIZE: arith = op_quantize(st, cur, L, w); break;
                 case SA_OP_DRIFT: arith = op_drift(st, s, cur, L, w); break;
                 case SA_OP_NOISE_UNIFORM: arith = op_uniform(st, s, cur, L, w); break;
-                case SA_OP_NOISE_SPIKE: arith = op_spike(st, s, cur, L, w); break;
+                case SA_OP_NOISE_SPIKE: arith = op_spike(st, s, cur, oth, L, w); break;
                 case SA_OP_NOISE_SLOPE: arith = op_slope(st, s, cur, L, w); break;
                 case SA_OP_APP:
                 case SA_OP_FREQ_MASK:
@@ -198,6 +208,7 @@ __global__ void __launch_bounds__(32) chain_kernel(const __grid_constant__ Chain
             }
         }
         // 5. write the row
+        if (!active) continue;
         double* dst = p.out + row * (int64_t)p.len_out;
         if ((p.len_out & 1) == 0 && ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0)) {
             const double2* c2 = reinterpret_cast<const double2*>(cur);
@@ -419,7 +430,14 @@ struct Plan {
     ChainParams p;
     Layout lay;
     int grid;
+    int warps;     // warps (= series in flight) per CTA
+    size_t smem;   // dynamic smem per CTA
 };
+
+int env_int(const char* k, int d) {
+    const char* v = getenv(k);
+    return v && *v ? atoi(v) : d;
+}
 
 // Lower the ABI stage table into kernel parameters and a launch shape.
 int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, int32_t n_aux, uint64_t seed,
@@ -439,6 +457,7 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
     if (n_aux) std::memcpy(p.aux, aux, sizeof(double) * (size_t)n_aux);
     int64_t L = len_in, lmax = len_in;
     int small = 64, iscr = 16;
+    int64_t spike_lcap = 0;
     bool after_repeat = false;
     for (int j = 0; j < ns; ++j) {
         const sa_stage& s = stages[j];
@@ -480,17 +499,17 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
         if (s.op == SA_OP_SPEED_WARP) small = std::max<int>(small, (int)(2 * (s.i[0] + 1)) + 2);
         if (s.op == SA_OP_NOISE_SPIKE) small = std::max<int>(small, (int)(lmax / 32) + 8);
         if (s.op == SA_OP_PERMUTE) iscr = std::max<int>(iscr, (int)s.i[0] + 1);
-        if (s.op == SA_OP_NOISE_SPIKE) {
+        if (s.op == SA_OP_NOISE_SPIKE) {  // choice scratch lives in the second buffer
             int64_t k = s.i[0];
             uint32_t mask = (uint32_t)(1.2 * (double)k);
             mask |= mask >> 1; mask |= mask >> 2; mask |= mask >> 4; mask |= mask >> 8; mask |= mask >> 16;
-            int64_t need = std::max<int64_t>((int64_t)mask + 1, lmax) + k + 1;
-            iscr = std::max<int>(iscr, (int)need);
+            int64_t need_words = ((L > 10000 && k > L / 50) ? L : (int64_t)mask + 1) + k + 1;
+            spike_lcap = std::max<int64_t>(spike_lcap, (need_words + 1) / 2);
         }
     }
     if (L != len_out) return fail(SA_ERR_INVALID_ARG, "len_out does not match the projected length");
     p.rows_out = n * p.repeat_r;
-    p.lcap = (int32_t)((lmax + 2 + 1) & ~1LL);
+    p.lcap = (int32_t)((std::max<int64_t>(lmax + 2, spike_lcap) + 1) & ~1LL);
     p.small_words = small;
     p.iscr_words = iscr;
     plan->lay = make_layout(p.lcap, ns, small, iscr);
@@ -498,12 +517,25 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
     if (plan->lay.total > ds.smem_optin)
         return fail(SA_ERR_UNSUPPORTED, "series too long for one warp's shared memory (" +
                                             std::to_string(plan->lay.total) + " B)");
+    // Stage-major CTAs: `warps` series per CTA walk the chain in lockstep
+    // (a barrier every `sync_every` stages) so the SM works through one
+    // operator's code at a time (the fused kernel is
+    // instruction-fetch bound when warps drift apart).
+    const int per_warp = (int)plan->lay.total;
+    int fit = (int)((ds.smem_optin) / (size_t)per_warp);
+    int warps = env_int("SA_CTA_WARPS", 0);
+    if (warps <= 0) warps = std::min(16, std::max(1, fit));
+    warps = std::max(1, std::min(warps, std::min(16, fit)));
+    plan->warps = warps;
+    plan->smem = (size_t)per_warp * warps;
+    p.sync_every = ns > 1 ? env_int("SA_SYNC_EVERY", 3) : 0;
     int per_sm = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chain_kernel, 32, plan->lay.total);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chain_kernel, 32 * warps, plan->smem);
     if (e != cudaSuccess) return cuda_fail(e, "occupancy");
     per_sm = std::max(per_sm, 1);
+    int64_t ctas_needed = (p.rows_out + warps - 1) / warps;
     int64_t want = (int64_t)ds.sms * per_sm;
-    plan->grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, p.rows_out));
+    plan->grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, ctas_needed));
     return SA_OK;
 }
 
@@ -515,7 +547,7 @@ int launch_plan(Plan* plan, const double* d_in, double* d_out, uint32_t* d_flags
     p.bulk_in = ((p.len_in & 1) == 0 && (reinterpret_cast<uintptr_t>(d_in) & 15u) == 0) ? 1 : 0;
     SA_CUDA(cudaMemsetAsync(d_flags, 0, sizeof(uint32_t), stream));
     if (p.rows_out == 0) return SA_OK;
-    chain_kernel<<<plan->grid, 32, plan->lay.total, stream>>>(p);
+    chain_kernel<<<plan->grid, 32 * plan->warps, plan->smem, stream>>>(p);
     SA_CUDA(cudaGetLastError());
     __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
     return SA_OK;
@@ -649,13 +681,13 @@ int sa_pipeline_run_host(const sa_stage* stages, int32_t n_stages, const double*
         Plan pl = plan;
         pl.p.offset = series_offset + r0;
         pl.p.rows_out = rows * r;
-        pl.grid = (int)std::max<int64_t>(1, std::min<int64_t>(plan.grid, pl.p.rows_out));
+        pl.grid = (int)std::max<int64_t>(1, std::min<int64_t>(plan.grid, (pl.p.rows_out + plan.warps - 1) / plan.warps));
         pl.p.in = ds.din[c & 1];
         pl.p.out = ds.dout[c & 1];
         pl.p.flags = ds.dflags + (c & 1);
         pl.p.bulk_in = ((len_in & 1) == 0) ? 1 : 0;
         if (pl.p.rows_out) {
-            chain_kernel<<<pl.grid, 32, pl.lay.total, st>>>(pl.p);
+            chain_kernel<<<pl.grid, 32 * pl.warps, pl.smem, st>>>(pl.p);
             SA_CUDA(cudaGetLastError());
             __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
         }

@@ -32,6 +32,7 @@ struct ChainParams {
     int32_t ns, repeat_r;
     int32_t len_in, len_out;
     int32_t lcap, small_words, iscr_words, bulk_in;
+    int32_t sync_every, pad2;  // CTA barrier every `sync_every` stages (0: none)
     uint64_t seed;
     int64_t offset;
     int64_t rows_out;
@@ -189,7 +190,7 @@ __device__ __forceinline__ void swapbuf(double*& a, double*& b) {
 
 // basic.py:41-44 Jitter, basic.py:356-359 InjectNoise(gaussian):
 // y = x + (0.0 + sigma * z)
-__device__ bool op_gauss(const DevStage& st, WStream& s, double*& cur, double*& oth, int& L, Warp& w) {
+__device__ __forceinline__ bool op_gauss(const DevStage& st, WStream& s, double*& cur, double*& oth, int& L, Warp& w) {
     const double sigma = st.f[0];
     if (sigma == 0.0) return false;
     double* x = cur;
@@ -199,7 +200,7 @@ __device__ bool op_gauss(const DevStage& st, WStream& s, double*& cur, double*& 
 }
 
 // basic.py:58-60 Scale: s = 1.0 + sigma_factor * z; y = x * s
-__device__ bool op_scale(const DevStage& st, WStream& s, double*& cur, double*& oth, int& L, Warp& w) {
+__device__ __forceinline__ bool op_scale(const DevStage& st, WStream& s, double*& cur, double*& oth, int& L, Warp& w) {
     double f = 1.0 + st.f[0] * std_normal(s, w.lane);
     for (int t = w.lane; t < L; t += 32) cur[t] = cur[t] * f;
     __syncwarp();
@@ -207,14 +208,14 @@ __device__ bool op_scale(const DevStage& st, WStream& s, double*& cur, double*& 
 }
 
 // basic.py:70-71 Rotate: -x
-__device__ bool op_rotate(double*& cur, int L, Warp& w) {
+__device__ __forceinline__ bool op_rotate(double*& cur, int L, Warp& w) {
     for (int t = w.lane; t < L; t += 32) cur[t] = -cur[t];
     __syncwarp();
     return false;
 }
 
 // basic.py:95-104 PermuteSegments
-__device__ bool op_permute(const DevStage& st, WStream& s, double*& cur, double*& oth, int& L, Warp& w) {
+__device__ __forceinline__ bool op_permute(const DevStage& st, WStream& s, double*& cur, double*& oth, int& L, Warp& w) {
     const int n = (int)st.i[0];
     if (n == 1) return false;
     int32_t* order = w.iscr;
@@ -244,7 +245,7 @@ __device__ bool op_permute(const DevStage& st, WStream& s, double*& cur, double*
 }
 
 // basic.py:133-135 Crop: start = integers(0, L - size + 1)
-__device__ bool op_crop(const DevStage& st, WStream& s, double*& cur, double*& oth, int& L, Warp& w) {
+__device__ __forceinline__ bool op_crop(const DevStage& st, WStream& s, double*& cur, double*& oth, int& L, Warp& w) {
     const int size = (int)st.i[0];
     const int start = (int)bounded(s, w.lane, (uint32_t)(L - size));
     for (int t = w.lane; t < size; t += 32) oth[t] = cur[start + t];
@@ -255,7 +256,7 @@ __device__ bool op_crop(const DevStage& st, WStream& s, double*& cur, double*& o
 }
 
 // basic.py:145-146 Reverse
-__device__ bool op_reverse(double*& cur, double*& oth, int L, Warp& w) {
+__device__ __forceinline__ bool op_reverse(double*& cur, double*& oth, int L, Warp& w) {
     for (int t = w.lane; t < L; t += 32) oth[t] = cur[L - 1 - t];
     __syncwarp();
     swapbuf(cur, oth);
@@ -263,7 +264,7 @@ __device__ bool op_reverse(double*& cur, double*& oth, int L, Warp& w) {
 }
 
 // basic.py:174-177 Resize: interp(linspace(0, L-1, T), arange(L), x)
-__device__ bool op_resize(const DevStage& st, double*& cur, double*& oth, int& L, Warp& w) {
+__device__ __forceinline__ bool op_resize(const DevStage& st, double*& cur, double*& oth, int& L, Warp& w) {
     const int T = (int)st.i[0];
     if (T == L) return false;
     for (int t = w.lane; t < T; t += 32)
@@ -275,7 +276,7 @@ __device__ bool op_resize(const DevStage& st, double*& cur, double*& oth, int& L
 }
 
 // basic.py:196-207 Quantize / snap_to_levels
-__device__ bool op_quantize(const DevStage& st, double*& cur, int L, Warp& w) {
+__device__ __forceinline__ bool op_quantize(const DevStage& st, double*& cur, int L, Warp& w) {
     double lo = cur[0], hi = cur[0];
     for (int t = w.lane; t < L; t += 32) {
         double v = cur[t];
@@ -298,7 +299,7 @@ __device__ bool op_quantize(const DevStage& st, double*& cur, int L, Warp& w) {
 }
 
 // basic.py:227-241 Drift
-__device__ bool op_drift(const DevStage& st, WStream& s, double*& cur, int L, Warp& w) {
+__device__ __forceinline__ bool op_drift(const DevStage& st, WStream& s, double*& cur, int L, Warp& w) {
     const double md = st.f[0];
     if (md == 0.0) return false;
     const int np_ = (int)st.i[0];
@@ -327,7 +328,7 @@ __device__ bool op_drift(const DevStage& st, WStream& s, double*& cur, int L, Wa
 }
 
 // basic.py:352-355 InjectNoise(uniform): x + uniform(-hw, hw)
-__device__ bool op_uniform(const DevStage& st, WStream& s, double*& cur, int L, Warp& w) {
+__device__ __forceinline__ bool op_uniform(const DevStage& st, WStream& s, double*& cur, int L, Warp& w) {
     const double hw = st.f[0];
     if (hw == 0.0) return false;
     const double lo = -hw, range = hw - lo;
@@ -338,7 +339,7 @@ __device__ bool op_uniform(const DevStage& st, WStream& s, double*& cur, int L, 
 }
 
 // Generator.choice(L, k, replace=False) into idx[0..k) (int32 scratch).
-__device__ void choice_noreplace(WStream& s, int lane, int pop, int k, int32_t* iscr, int32_t* idx) {
+__device__ __noinline__ void choice_noreplace(WStream& s, int lane, int pop, int k, int32_t* iscr, int32_t* idx) {
     if (pop > 10000 && k > pop / 50) {  // tail shuffle of arange(pop)
         int32_t* a = iscr;
         for (int t = lane; t < pop; t += 32) a[t] = t;
@@ -394,7 +395,7 @@ __device__ void choice_noreplace(WStream& s, int lane, int pop, int k, int32_t* 
 }
 
 // basic.py:360-370 InjectNoise(spike)
-__device__ bool op_spike(const DevStage& st, WStream& s, double*& cur, int L, Warp& w) {
+__device__ __forceinline__ bool op_spike(const DevStage& st, WStream& s, double*& cur, double*& oth, int L, Warp& w) {
     const int cnt = (int)st.i[0];
     const double mag = st.f[0];
     if (cnt == 0 || mag == 0.0) return false;
@@ -405,12 +406,15 @@ __device__ bool op_spike(const DevStage& st, WStream& s, double*& cur, int L, Wa
                  (double)L;
     double scale = sqrt(var);
     if (scale == 0.0) scale = 1.0;
-    // hash set / tail array first, picks after it
+    // hash set / tail array first, picks after it (host sizes lcap for it)
     uint32_t mask = (uint32_t)(1.2 * (double)cnt);
     mask |= mask >> 1; mask |= mask >> 2; mask |= mask >> 4; mask |= mask >> 8; mask |= mask >> 16;
     int scr = (L > 10000 && cnt > L / 50) ? L : (int)mask + 1;
-    int32_t* idx = w.iscr + scr;
-    choice_noreplace(s, w.lane, L, cnt, w.iscr, idx);
+    int32_t* scratch = reinterpret_cast<int32_t*>(oth);  // free during this in-place op
+    int32_t* idx = scratch + scr;
+    WStream t = s;  // by-address copy for the out-of-line helper; s stays in registers
+    choice_noreplace(t, w.lane, L, cnt, scratch, idx);
+    s = t;
     for (int q = 0; q < cnt; ++q) {
         double sign = (double)((int64_t)bounded(s, w.lane, 1u) * 2 - 1);
         if (w.lane == 0) {
@@ -423,7 +427,7 @@ __device__ bool op_spike(const DevStage& st, WStream& s, double*& cur, int L, Wa
 }
 
 // basic.py:371-375 InjectNoise(slope_trend)
-__device__ bool op_slope(const DevStage& st, WStream& s, double*& cur, int L, Warp& w) {
+__device__ __forceinline__ bool op_slope(const DevStage& st, WStream& s, double*& cur, int L, Warp& w) {
     const double mo = st.f[0];
     if (mo == 0.0) return false;
     const double sign = next_double(s, w.lane) < 0.5 ? 1.0 : -1.0;
@@ -435,7 +439,7 @@ __device__ bool op_slope(const DevStage& st, WStream& s, double*& cur, int L, Wa
 
 // warp.py:25-47 warp_positions: builds knots (small[0..n)) and warped
 // (small[n..2n)); returns false if the map is not strictly increasing.
-__device__ bool warp_knots(int len, int nk, double intensity, WStream& s, Warp& w) {
+__device__ __noinline__ bool warp_knots(int len, int nk, double intensity, WStream& s, Warp w) {
     const double span = (double)len - 1.0;
     double* knots = w.small;
     double* warped = w.small + nk;
@@ -484,11 +488,14 @@ __device__ bool warp_knots(int len, int nk, double intensity, WStream& s, Warp& 
 }
 
 // warp.py:73-76 TimeWarp
-__device__ bool op_time_warp(const DevStage& st, WStream& s, double*& cur, double*& oth, int L, Warp& w,
+__device__ __forceinline__ bool op_time_warp(const DevStage& st, WStream& s, double*& cur, double*& oth, int L, Warp& w,
                              uint32_t& flags) {
     if (st.f[0] == 0.0) return false;
     const int nk = (int)st.i[0];
-    if (!warp_knots(L, nk, st.f[0], s, w)) {
+    WStream t = s;
+    const bool ok = warp_knots(L, nk, st.f[0], t, w);
+    s = t;
+    if (!ok) {
         flags |= SA_FLAG_WARP_MONOTONE;
         return false;
     }
@@ -502,13 +509,16 @@ __device__ bool op_time_warp(const DevStage& st, WStream& s, double*& cur, doubl
 }
 
 // warp.py:108-118 WindowWarp
-__device__ bool op_window_warp(const DevStage& st, WStream& s, double*& cur, double*& oth, int L, Warp& w,
+__device__ __forceinline__ bool op_window_warp(const DevStage& st, WStream& s, double*& cur, double*& oth, int L, Warp& w,
                                uint32_t& flags) {
     if (st.f[0] == 0.0) return false;
     const int wsz = (int)st.i[0];
     const int nk = (int)st.i[1];
     const int start = (wsz == L) ? 0 : (int)bounded(s, w.lane, (uint32_t)(L - wsz));
-    if (!warp_knots(wsz, nk, st.f[0], s, w)) {
+    WStream t = s;
+    const bool ok = warp_knots(wsz, nk, st.f[0], t, w);
+    s = t;
+    if (!ok) {
         flags |= SA_FLAG_WARP_MONOTONE;
         return false;
     }
@@ -525,7 +535,7 @@ __device__ bool op_window_warp(const DevStage& st, WStream& s, double*& cur, dou
 }
 
 // BASELINE M2 Dropout
-__device__ bool op_dropout(const DevStage& st, WStream& s, double*& cur, int L, Warp& w) {
+__device__ __forceinline__ bool op_dropout(const DevStage& st, WStream& s, double*& cur, int L, Warp& w) {
     const double rate = st.f[0], fill = st.f[1];
     if (rate == 0.0) return false;
     double* x = cur;
@@ -537,7 +547,7 @@ __device__ bool op_dropout(const DevStage& st, WStream& s, double*& cur, int L, 
 }
 
 // BASELINE M3 Pool
-__device__ bool op_pool(const DevStage& st, double*& cur, int L, Warp& w) {
+__device__ __forceinline__ bool op_pool(const DevStage& st, double*& cur, int L, Warp& w) {
     const int P = (int)st.i[0];
     if (P == 1) return false;
     const int red = (int)st.i[1];
@@ -563,7 +573,7 @@ __device__ bool op_pool(const DevStage& st, double*& cur, int L, Warp& w) {
 }
 
 // BASELINE M4 Convolve (taps in params.aux)
-__device__ bool op_convolve(const DevStage& st, const double* aux, double*& cur, double*& oth, int L, Warp& w) {
+__device__ __forceinline__ bool op_convolve(const DevStage& st, const double* aux, double*& cur, double*& oth, int L, Warp& w) {
     const double* taps = aux + st.aux_off;
     const int S = st.aux_len, h = S / 2;
     for (int t = w.lane; t < L; t += 32) {
@@ -581,7 +591,7 @@ __device__ bool op_convolve(const DevStage& st, const double* aux, double*& cur,
 }
 
 // BASELINE M5 SpeedWarp
-__device__ bool op_speed_warp(const DevStage& st, WStream& s, double*& cur, double*& oth, int L, Warp& w) {
+__device__ __forceinline__ bool op_speed_warp(const DevStage& st, WStream& s, double*& cur, double*& oth, int L, Warp& w) {
     const int K = (int)st.i[0];
     const double R = st.f[0];
     if (K == 0 || R == 1.0) return false;
@@ -648,29 +658,28 @@ __device__ __forceinline__ bool spectral_noop(const DevStage& st) {
 }
 
 // freqaugment.py:106-170 (+ BASELINE M6): perturb the half spectrum X[0..bins)
-// (interleaved complex, smem); scratch holds >= bins doubles.
-__device__ void perturb_spectrum(const DevStage& st, WStream& s, double2* X, int L, double* scratch, Warp& w) {
+// (interleaved complex, smem); scratch holds >= 2 * bins doubles.
+__device__ __forceinline__ void perturb_spectrum(const DevStage& st, WStream& s, double2* X, int L, double* scratch, Warp& w) {
     const int bins = L / 2 + 1;
     if (st.op == SA_OP_APP) {
         const double sa = st.f[0], sp = st.f[1];
         double* amp = scratch;
         const bool even = (L % 2 == 0);
         const int hi = even ? bins - 1 : bins;
+        double* ph = scratch + bins;  // scratch holds >= 2 * bins doubles
         normals(s, w.lane, bins, [&](int k, double z) { amp[k] = 0.0 + sa * z; });
+        normals(s, w.lane, bins, [&](int k, double z) { ph[k] = 0.0 + sp * z; });
         __syncwarp();
-        normals(s, w.lane, bins, [&](int b, double z) {
-            double ph = 0.0 + sp * z;
-            if (b >= 1 && b < hi) {
-                double2 v = X[b];
-                double r = hypot(v.x, v.y);
-                double th = atan2(v.y, v.x) + ph;
-                r = r + amp[b];
-                if (!(r >= 0.0)) r = (r != r) ? r : 0.0;
-                double sn, cs;
-                sincos(th, &sn, &cs);
-                X[b] = make_double2(r * cs, r * sn);
-            }
-        });
+        for (int b = 1 + w.lane; b < hi; b += 32) {
+            double2 v = X[b];
+            double r = hypot(v.x, v.y);
+            double th = atan2(v.y, v.x) + ph[b];
+            r = r + amp[b];
+            if (!(r >= 0.0)) r = (r != r) ? r : 0.0;
+            double sn, cs;
+            sincos(th, &sn, &cs);
+            X[b] = make_double2(r * cs, r * sn);
+        }
         __syncwarp();
         if (w.lane == 0) {
             for (int q = 0; q < (even ? 2 : 1); ++q) {
@@ -712,7 +721,7 @@ __device__ void perturb_spectrum(const DevStage& st, WStream& s, double2* X, int
 }
 
 // freqaugment.py:37-47 SpectralAugmenter._apply (time-domain entry)
-__device__ bool op_spectral(const DevStage& st, WStream& s, double*& cur, double*& oth, int L, Warp& w) {
+__device__ __forceinline__ bool op_spectral(const DevStage& st, WStream& s, double*& cur, double*& oth, int L, Warp& w) {
     if (spectral_noop(st)) return false;
     double2* X = rfft_warp(cur, oth, L, st.tw, w.lane);
     double* free_buf = (reinterpret_cast<double*>(X) == cur) ? oth : cur;

@@ -107,16 +107,23 @@ struct WStream {
     uint64_t* winbuf;  // the warp's window storage (SA_WIN words, smem)
 };
 
-// Refill the window with the 32 blocks starting at the block holding wpos.
-__device__ __forceinline__ void refill(WStream& s, int lane) {
-    uint64_t blk0 = s.wpos >> 2;
+// Fill `winbuf` with the 32 Philox blocks blk0 .. blk0+31 (one per lane).
+// Out of line (one copy of the unrolled rounds); takes plain values so the
+// caller's stream state stays in registers.
+__device__ __noinline__ void fill_window(uint64_t k0, uint64_t k1, uint64_t blk0, uint64_t* winbuf, int lane) {
     uint64_t o0, o1, o2, o3;
-    philox(s.k0, s.k1, blk0 + (uint64_t)lane + 1, o0, o1, o2, o3);
+    philox(k0, k1, blk0 + (uint64_t)lane + 1, o0, o1, o2, o3);
     __syncwarp();  // every lane is done reading the previous window
-    ulonglong2* w2 = reinterpret_cast<ulonglong2*>(s.winbuf) + 2 * lane;
+    ulonglong2* w2 = reinterpret_cast<ulonglong2*>(winbuf) + 2 * lane;
     w2[0] = make_ulonglong2(o0, o1);
     w2[1] = make_ulonglong2(o2, o3);
     __syncwarp();
+}
+
+// Refill the window with the 32 blocks starting at the block holding wpos.
+__device__ __forceinline__ void refill(WStream& s, int lane) {
+    uint64_t blk0 = s.wpos >> 2;
+    fill_window(s.k0, s.k1, blk0, s.winbuf, lane);
     s.win = s.winbuf;
     s.wb = blk0 << 2;
     s.wn = SA_WIN;
@@ -170,31 +177,49 @@ __device__ __forceinline__ uint32_t interval(WStream& s, int lane, uint32_t max)
     return v;
 }
 
-// Slow path of the ziggurat for a word that failed the fast test; returns
-// true and the value if a normal is produced (else the caller retries).
-__device__ __noinline__ bool zig_slow(WStream& s, int lane, uint64_t r0, double& out) {
+// Slow path of the ziggurat for a word that failed the fast test (wedge or
+// tail, reference numpy random_standard_normal): returns true and the value
+// if a normal is produced (else the caller retries with the next word).
+// Out of line and rare; the stream travels by value so callers keep theirs
+// in registers.
+struct ZigSlow {
+    WStream s;
+    double v;
+    bool ok;
+};
+__device__ __noinline__ void zig_slow_impl(WStream s, int lane, uint64_t r0, ZigSlow* res) {
     int idx = (int)(r0 & 0xff);
     uint64_t r = r0 >> 8;
     int sign = (int)(r & 1);
     uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
     double x = (double)rabs * g_zig[idx].wi;
     if (sign) x = -x;
+    res->ok = false;
     if (idx == 0) {
         for (;;) {
             double xx = -kZigInvR * log1p(-next_double(s, lane));
             double yy = -log1p(-next_double(s, lane));
             if (yy + yy > xx * xx) {
-                out = ((rabs >> 8) & 1) ? -(kZigR + xx) : kZigR + xx;
-                return true;
+                res->v = ((rabs >> 8) & 1) ? -(kZigR + xx) : kZigR + xx;
+                res->ok = true;
+                break;
             }
         }
+    } else {
+        double u = next_double(s, lane);
+        if (((g_fi[idx - 1] - g_fi[idx]) * u + g_fi[idx]) < exp(-0.5 * x * x)) {
+            res->v = x;
+            res->ok = true;
+        }
     }
-    double u = next_double(s, lane);
-    if (((g_fi[idx - 1] - g_fi[idx]) * u + g_fi[idx]) < exp(-0.5 * x * x)) {
-        out = x;
-        return true;
-    }
-    return false;
+    res->s = s;
+}
+__device__ __forceinline__ bool zig_slow(WStream& s, int lane, uint64_t r0, double& out) {
+    ZigSlow res;
+    zig_slow_impl(s, lane, r0, &res);
+    s = res.s;
+    out = res.v;
+    return res.ok;
 }
 
 // One standard normal, warp-uniform (all lanes get the same value).
