@@ -100,6 +100,10 @@ __global__ void __launch_bounds__(512) chain_kernel(const __grid_constant__ Chai
     w.small = reinterpret_cast<double*>(smem + lay.small);
     w.iscr = reinterpret_cast<int32_t*>(smem + lay.iscr);
     w.lcap = p.lcap;
+    ZigEntry* zs = reinterpret_cast<ZigEntry*>(smem_all + (size_t)nw * lay.total);  // CTA-shared
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) zs[i] = g_zig[i];
+    w.zig = zs;
+    __syncthreads();
 
     if (lane == 0) mbar_init(bar, 1);
     __syncwarp();
@@ -151,9 +155,10 @@ __global__ void __launch_bounds__(512) chain_kernel(const __grid_constant__ Chai
         __syncwarp();
         // input finiteness (Batch invariant, core.py:104)
         {
-            bool ok = true;
-            for (int t = lane; t < p.len_in; t += 32) ok = ok && isfinite(A[t]);
-            if (!__all_sync(SA_FULL, ok)) flags |= SA_FLAG_NONFINITE;
+            bool bad = false;
+#pragma unroll 4
+            for (int t = lane; t < p.len_in; t += 32) bad |= nonfinite(A[t]);
+            if (__any_sync(SA_FULL, bad)) flags |= SA_FLAG_NONFINITE;
         }
         }
         // 3. the chain (stage-major across the CTA when sync_every > 0)
@@ -186,7 +191,7 @@ __global__ void __launch_bounds__(512) chain_kernel(const __grid_constant__ Chai
                 case SA_OP_REVERSE: arith = op_reverse(cur, oth, L, w); break;
                 case SA_OP_RESIZE: arith = op_resize(st, cur, oth, L, w); break;
                 case SA_OP_QUANTIZE: arith = op_quantize(st, cur, L, w); break;
-                case SA_OP_DRIFT: arith = op_drift(st, s, cur, L, w); break;
+                case SA_OP_DRIFT: arith = op_drift(st, s, cur, oth, L, w); break;
                 case SA_OP_NOISE_UNIFORM: arith = op_uniform(st, s, cur, L, w); break;
                 case SA_OP_NOISE_SPIKE: arith = op_spike(st, s, cur, oth, L, w); break;
                 case SA_OP_NOISE_SLOPE: arith = op_slope(st, s, cur, L, w); break;
@@ -202,9 +207,10 @@ __global__ void __launch_bounds__(512) chain_kernel(const __grid_constant__ Chai
                 default: break;
             }
             if (arith) {
-                bool ok = true;
-                for (int t = lane; t < L; t += 32) ok = ok && isfinite(cur[t]);
-                if (!__all_sync(SA_FULL, ok)) flags |= SA_FLAG_NONFINITE;
+                bool bad = false;
+#pragma unroll 4
+                for (int t = lane; t < L; t += 32) bad |= nonfinite(cur[t]);
+                if (__any_sync(SA_FULL, bad)) flags |= SA_FLAG_NONFINITE;
             }
         }
         // 5. write the row
@@ -291,6 +297,7 @@ __global__ void __launch_bounds__(32) spectrum_kernel(const __grid_constant__ Sp
     uint64_t* c = win + SA_WIN;
     Warp w;
     w.lane = lane;
+    w.zig = g_zig;
     w.win = win;
     const int bins = p.L / 2 + 1;
     for (int64_t row = blockIdx.x; row < p.n; row += gridDim.x) {
@@ -493,11 +500,14 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
         d.len_out = (int32_t)L;
         lmax = std::max(lmax, L);
         // scratch needs
-        if (s.op == SA_OP_DRIFT) small = std::max<int>(small, (int)(2 * s.i[0]) + 2);
+        if (s.op == SA_OP_DRIFT) small = std::max<int>(small, (int)(3 * s.i[0]) + 2);
         if (s.op == SA_OP_TIME_WARP) small = std::max<int>(small, (int)(3 * s.i[0]) + 2);
         if (s.op == SA_OP_WINDOW_WARP) small = std::max<int>(small, (int)(3 * s.i[1]) + 2);
-        if (s.op == SA_OP_SPEED_WARP) small = std::max<int>(small, (int)(2 * (s.i[0] + 1)) + 2);
-        if (s.op == SA_OP_NOISE_SPIKE) small = std::max<int>(small, (int)(lmax / 32) + 8);
+        if (s.op == SA_OP_SPEED_WARP) {
+            small = std::max<int>(small, (int)(2 * (s.i[0] + 1)) + 2);
+            iscr = std::max<int>(iscr, (int)s.i[0] + 2);
+        }
+        if (s.op == SA_OP_NOISE_SPIKE) small = std::max<int>(small, 2 * (int)(lmax / 64 + 2) + 8);
         if (s.op == SA_OP_PERMUTE) iscr = std::max<int>(iscr, (int)s.i[0] + 1);
         if (s.op == SA_OP_NOISE_SPIKE) {  // choice scratch lives in the second buffer
             int64_t k = s.i[0];
@@ -514,7 +524,7 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
     p.iscr_words = iscr;
     plan->lay = make_layout(p.lcap, ns, small, iscr);
     DeviceState& ds = g_dev[dev];
-    if (plan->lay.total > ds.smem_optin)
+    if (plan->lay.total + 256 * sizeof(ZigEntry) > ds.smem_optin)
         return fail(SA_ERR_UNSUPPORTED, "series too long for one warp's shared memory (" +
                                             std::to_string(plan->lay.total) + " B)");
     // Stage-major CTAs: `warps` series per CTA walk the chain in lockstep
@@ -522,12 +532,12 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
     // operator's code at a time (the fused kernel is
     // instruction-fetch bound when warps drift apart).
     const int per_warp = (int)plan->lay.total;
-    int fit = (int)((ds.smem_optin) / (size_t)per_warp);
+    int fit = (int)((ds.smem_optin - 256 * sizeof(ZigEntry)) / (size_t)per_warp);
     int warps = env_int("SA_CTA_WARPS", 0);
     if (warps <= 0) warps = std::min(16, std::max(1, fit));
     warps = std::max(1, std::min(warps, std::min(16, fit)));
     plan->warps = warps;
-    plan->smem = (size_t)per_warp * warps;
+    plan->smem = (size_t)per_warp * warps + 256 * sizeof(ZigEntry);
     p.sync_every = ns > 1 ? env_int("SA_SYNC_EVERY", 3) : 0;
     int per_sm = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chain_kernel, 32 * warps, plan->smem);

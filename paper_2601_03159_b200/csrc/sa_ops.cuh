@@ -45,6 +45,7 @@ struct ChainParams {
 
 struct Warp {
     int lane;
+    const ZigEntry* zig;  // ziggurat fast-path table (smem copy in the chain kernel)
     uint64_t* win;
     double* small;
     int32_t* iscr;
@@ -66,6 +67,52 @@ __device__ __forceinline__ double linspace_at(double start, double stop, int64_t
         y = y * delta;
     }
     return y + start;
+}
+
+// np.linspace(start, stop, num) with its step hoisted out of element loops:
+// element k is (double)k * step + start (step != 0) or ((double)k / div) * delta
+// + start (step == 0), the last element pinned to stop.
+struct Linspace {
+    double start, stop, step, delta;
+    int64_t num, div;
+    bool zero;
+    __device__ __forceinline__ Linspace(double a, double b, int64_t n) : start(a), stop(b), num(n), div(n - 1) {
+        delta = b - a;
+        step = div > 0 ? delta / (double)div : 0.0;
+        zero = div > 0 && step == 0.0;
+    }
+    // the common case (num > 1, step != 0): k * step + start, last = stop
+    __device__ __forceinline__ bool fast() const { return div > 0 && !zero; }
+    __device__ __forceinline__ double at_fast(int k) const {
+        const double y = (double)k * step + start;
+        return k == num - 1 ? stop : y;
+    }
+    __device__ __forceinline__ double at(int64_t k) const {
+        if (num > 1 && k == num - 1) return stop;
+        double y = (double)k;
+        if (div > 0) y = zero ? (y / (double)div) * delta : y * step;
+        else y = y * delta;
+        return y + start;
+    }
+};
+
+// np.interp on a monotone table with precomputed per-interval slopes
+// (numpy precomputes exactly these slopes when len(xp) <= len(x)); the
+// bracketing interval comes from an O(1) guess `hint` refined by compares,
+// which yields the same "largest j with xp[j] <= x" as numpy's search.
+__device__ __forceinline__ double interp_slopes(double x, const double* __restrict__ xp, const double* __restrict__ fp,
+                                                const double* __restrict__ sl, int n, int hint) {
+    int j = hint < 0 ? 0 : (hint > n - 2 ? n - 2 : hint);
+    j = (xp[j + 1] <= x && j < n - 2) ? j + 1 : j;
+    j = (xp[j] > x && j > 0) ? j - 1 : j;
+    while (j < n - 2 && xp[j + 1] <= x) ++j;  // never taken for linspace tables
+    while (j > 0 && xp[j] > x) --j;
+    const double xj = xp[j], fj = fp[j];
+    double r = sl[j] * (x - xj) + fj;
+    r = (xj == x) ? fj : r;
+    r = (x >= xp[n - 1]) ? fp[n - 1] : r;
+    r = (x < xp[0]) ? fp[0] : r;
+    return r;
 }
 
 // np.interp(x, xp, fp) with xp increasing (binary search, exact-hit rule).
@@ -90,6 +137,25 @@ __device__ __forceinline__ double interp1(double x, const double* xp, const doub
     return r;
 }
 
+__device__ __forceinline__ bool nonfinite(double v) {
+    return (__double2hiint(v) & 0x7ff00000) == 0x7ff00000;
+}
+
+// np.interp(x, arange(n), fp) for n >= 2, branch-free.  The reference's NaN
+// fallback (numpy arr_interp) can only trigger for non-finite data, which the
+// kernel rejects (SA_FLAG_NONFINITE), so it is not reproduced here.
+__device__ __forceinline__ double interp_grid_fast(double x, const double* __restrict__ fp, int n) {
+    const double fl = floor(x);
+    int j = (int)fl;
+    j = j < 0 ? 0 : (j > n - 2 ? n - 2 : j);
+    const double a = fp[j], b = fp[j + 1];
+    double r = (b - a) * (x - fl) + a;  // (x - xp[j]) with xp[j] = j = fl in range
+    r = (x == fl) ? a : r;              // exact hit: fp[j]
+    r = (x >= (double)(n - 1)) ? fp[n - 1] : r;
+    r = (x < 0.0) ? fp[0] : r;
+    return r;
+}
+
 // np.interp(x, arange(n), fp).
 __device__ __forceinline__ double interp_grid(double x, const double* fp, int n) {
     if (x > (double)(n - 1)) return fp[n - 1];
@@ -97,7 +163,9 @@ __device__ __forceinline__ double interp_grid(double x, const double* fp, int n)
     int j = (int)floor(x);
     if (j >= n - 1) return fp[n - 1];
     if ((double)j == x) return fp[j];
-    double slope = (fp[j + 1] - fp[j]) / ((double)(j + 1) - (double)j);
+    // xp = arange(n): (j+1) - j == 1.0 exactly and d / 1.0 == d, so the
+    // reference's slope is the plain difference (no division needed)
+    double slope = fp[j + 1] - fp[j];
     double r = slope * (x - (double)j) + fp[j];
     if (isnan(r)) {
         r = slope * (x - (double)(j + 1)) + fp[j + 1];
@@ -106,59 +174,112 @@ __device__ __forceinline__ double interp_grid(double x, const double* fp, int n)
     return r;
 }
 
-// numpy pairwise summation of f(t), t in [lo, lo + n), leaf n <= 128.
+// numpy pairwise summation (np.add.reduce on contiguous float64,
+// pairwise_sum_DOUBLE): n < 8 -> sequential; n <= 128 -> a leaf with 8
+// strided accumulators combined as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) then
+// the n % 8 tail added in order; n > 128 -> split at n2 = n/2 - (n/2) % 8.
+// Leaves are summed in parallel (8 lanes per leaf, one accumulator each) and
+// combined in the recursion's order by an iterative post-order walk.
+struct PwFrame {
+    int n, stage;
+    double left;
+};
+
+__device__ __forceinline__ int pw_split(int n) {
+    int n2 = n / 2;
+    return n2 - n2 % 8;
+}
+
+// Leaves of the recursion over [0, n) in left-to-right order -> (start, len).
+__device__ __noinline__ int pairwise_leaf_list(int n, int2* leaves) {
+    int lo_stack[32], n_stack[32];
+    int sp = 0, cnt = 0;
+    lo_stack[0] = 0;
+    n_stack[0] = n;
+    while (sp >= 0) {
+        const int lo = lo_stack[sp], m = n_stack[sp];
+        --sp;
+        if (m <= 128) {
+            leaves[cnt++] = make_int2(lo, m);
+        } else {
+            const int n2 = pw_split(m);
+            ++sp; lo_stack[sp] = lo + n2; n_stack[sp] = m - n2;  // right, popped second
+            ++sp; lo_stack[sp] = lo; n_stack[sp] = n2;           // left, popped first
+        }
+    }
+    return cnt;
+}
+
+__device__ __noinline__ double pairwise_combine(int n, const double* leafsum) {
+    PwFrame st[32];
+    int sp = 0, leaf = 0;
+    st[0].n = n; st[0].stage = 0; st[0].left = 0.0;
+    for (;;) {
+        PwFrame& f = st[sp];
+        if (f.n <= 128) {
+            double v = leafsum[leaf++];
+            for (;;) {
+                if (sp == 0) return v;
+                --sp;
+                PwFrame& par = st[sp];
+                if (par.stage == 1) {  // left child done: descend right
+                    par.left = v;
+                    par.stage = 2;
+                    ++sp;
+                    st[sp].n = par.n - pw_split(par.n); st[sp].stage = 0; st[sp].left = 0.0;
+                    break;
+                }
+                v = par.left + v;  // right child done
+            }
+        } else {
+            f.stage = 1;
+            const int n2 = pw_split(f.n);
+            ++sp;
+            st[sp].n = n2; st[sp].stage = 0; st[sp].left = 0.0;
+        }
+    }
+}
+
+// Pairwise sum of f(t), t < n.  scratch: >= 2 * (n / 64 + 2) doubles.
 template <class F>
-__device__ __forceinline__ double pairwise_leaf(int lo, int n, F& f) {
+__device__ double pairwise_warp(int n, F f, double* scratch, int lane) {
     if (n < 8) {
         double r = 0.0;
-        for (int k = 0; k < n; ++k) r += f(lo + k);
+        for (int k = 0; k < n; ++k) r += f(k);
         return r;
     }
-    double r[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) r[q] = f(lo + q);
-    int k;
-    for (k = 8; k < n - (n % 8); k += 8) {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) r[q] += f(lo + k + q);
-    }
-    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-    for (; k < n; ++k) res += f(lo + k);
-    return res;
-}
-
-// leaves in left-to-right order; lane (leaf % 32) computes leaf `leaf`.
-template <class F>
-__device__ void pairwise_leaves(int lo, int n, F& f, double* leafsum, int& leaf, int lane) {
-    if (n <= 128) {
-        if ((leaf & 31) == lane) leafsum[leaf] = pairwise_leaf(lo, n, f);
-        leaf += 1;
-        return;
-    }
-    int n2 = n / 2;
-    n2 -= n2 % 8;
-    pairwise_leaves(lo, n2, f, leafsum, leaf, lane);
-    pairwise_leaves(lo + n2, n - n2, f, leafsum, leaf, lane);
-}
-
-__device__ double pairwise_combine(int n, const double* leafsum, int& leaf) {
-    if (n <= 128) return leafsum[leaf++];
-    int n2 = n / 2;
-    n2 -= n2 % 8;
-    double a = pairwise_combine(n2, leafsum, leaf);
-    double b = pairwise_combine(n - n2, leafsum, leaf);
-    return a + b;
-}
-
-template <class F>
-__device__ double pairwise_warp(int n, F f, double* leafsum, int lane) {
-    int leaf = 0;
-    pairwise_leaves(0, n, f, leafsum, leaf, lane);
+    int2* leaves = reinterpret_cast<int2*>(scratch);
+    const int nl_max = n / 64 + 2;
+    double* leafsum = scratch + nl_max;
+    int nl;
+    if (lane == 0) nl = pairwise_leaf_list(n, leaves);
+    nl = __shfl_sync(SA_FULL, nl, 0);
     __syncwarp();
-    int c = 0;
-    double r = pairwise_combine(n, leafsum, c);
+    const int g = lane >> 3, q = lane & 7;
+    for (int l0 = 0; l0 < nl; l0 += 4) {
+        const int l = l0 + g;
+        double acc = 0.0, res = 0.0;
+        int2 lf = make_int2(0, 0);
+        if (l < nl) {
+            lf = leaves[l];
+            const int full = lf.y - lf.y % 8;
+            acc = f(lf.x + q);
+            for (int k = 8 + q; k < full; k += 8) acc += f(lf.x + k);
+        }
+        // gather the group's 8 accumulators to its first lane, numpy's order
+        double r[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) r[u] = __shfl_sync(SA_FULL, acc, (lane & ~7) + u);
+        if (q == 0 && l < nl) {
+            res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+            for (int k = lf.y - lf.y % 8; k < lf.y; ++k) res += f(lf.x + k);
+            leafsum[l] = res;
+        }
+    }
     __syncwarp();
-    return r;
+    double total = pairwise_combine(n, leafsum);
+    __syncwarp();
+    return total;
 }
 
 __device__ __forceinline__ double warp_min(double v) {
@@ -194,7 +315,7 @@ __device__ __forceinline__ bool op_gauss(const DevStage& st, WStream& s, double*
     const double sigma = st.f[0];
     if (sigma == 0.0) return false;
     double* x = cur;
-    normals(s, w.lane, L, [&](int k, double z) { x[k] = x[k] + (0.0 + sigma * z); });
+    normals(s, w.lane, L, w.zig, [&](int k, double z) { x[k] = x[k] + (0.0 + sigma * z); });
     __syncwarp();
     return true;
 }
@@ -267,8 +388,13 @@ __device__ __forceinline__ bool op_reverse(double*& cur, double*& oth, int L, Wa
 __device__ __forceinline__ bool op_resize(const DevStage& st, double*& cur, double*& oth, int& L, Warp& w) {
     const int T = (int)st.i[0];
     if (T == L) return false;
-    for (int t = w.lane; t < T; t += 32)
-        oth[t] = interp_grid(linspace_at(0.0, (double)L - 1.0, T, t), cur, L);
+    const Linspace ls(0.0, (double)L - 1.0, T);
+    if (ls.fast()) {
+#pragma unroll 4
+        for (int t = w.lane; t < T; t += 32) oth[t] = interp_grid_fast(ls.at_fast(t), cur, L);
+    } else {
+        for (int t = w.lane; t < T; t += 32) oth[t] = interp_grid(ls.at(t), cur, L);
+    }
     __syncwarp();
     swapbuf(cur, oth);
     L = T;
@@ -290,39 +416,48 @@ __device__ __forceinline__ bool op_quantize(const DevStage& st, double*& cur, in
     const double top = (double)(st.i[0] - 1);
     for (int t = w.lane; t < L; t += 32) {
         double idx = ceil((cur[t] - lo) / step - 0.5);
-        if (idx < 0.0) idx = 0.0;
-        if (idx > top) idx = top;
+        idx = (idx < 0.0) ? 0.0 : idx;  // np.clip keeps -0.0 (x < 0 is false)
+        idx = (idx > top) ? top : idx;
         cur[t] = lo + idx * step;
     }
     __syncwarp();
     return true;
 }
 
-// basic.py:227-241 Drift
-__device__ __forceinline__ bool op_drift(const DevStage& st, WStream& s, double*& cur, int L, Warp& w) {
+// basic.py:227-241 Drift: anchors ~ N(0,1)^n at linspace(0, L-1, n),
+// curve = interp(arange(L), positions, anchors) - curve[0], scaled so its peak
+// magnitude is max_drift.
+__device__ __forceinline__ bool op_drift(const DevStage& st, WStream& s, double*& cur, double*& oth, int L, Warp& w) {
     const double md = st.f[0];
     if (md == 0.0) return false;
     const int np_ = (int)st.i[0];
     double* anchors = w.small;
     double* pos = w.small + np_;
+    double* sl = w.small + 2 * np_;
     for (int k = 0; k < np_; ++k) {
         double a = 0.0 + 1.0 * std_normal(s, w.lane);
         if (w.lane == 0) anchors[k] = a;
     }
-    for (int k = w.lane; k < np_; k += 32) pos[k] = linspace_at(0.0, (double)L - 1.0, np_, k);
+    const Linspace ls(0.0, (double)L - 1.0, np_);
+    for (int k = w.lane; k < np_; k += 32) pos[k] = ls.at(k);
     __syncwarp();
-    const double c0 = interp1(0.0, pos, anchors, np_);
+    for (int k = w.lane; k < np_ - 1; k += 32) sl[k] = (anchors[k + 1] - anchors[k]) / (pos[k + 1] - pos[k]);
+    __syncwarp();
+    const double inv = ls.step > 0.0 ? 1.0 / ls.step : 0.0;
+    const double c0 = interp_slopes(0.0, pos, anchors, sl, np_, 0);
+    double* curve = oth;  // pass 1: curve - c0 and its peak
     double peak = 0.0;
+#pragma unroll 4
     for (int t = w.lane; t < L; t += 32) {
-        double a = fabs(interp1((double)t, pos, anchors, np_) - c0);
+        const double c = interp_slopes((double)t, pos, anchors, sl, np_, (int)((double)t * inv)) - c0;
+        curve[t] = c;
+        const double a = fabs(c);
         peak = (a > peak || a != a) ? a : peak;
     }
     peak = warp_max(peak);
     if (peak == 0.0) return false;
-    for (int t = w.lane; t < L; t += 32) {
-        double c = interp1((double)t, pos, anchors, np_) - c0;
-        cur[t] = cur[t] + (c / peak) * md;
-    }
+#pragma unroll 4
+    for (int t = w.lane; t < L; t += 32) cur[t] = cur[t] + (curve[t] / peak) * md;
     __syncwarp();
     return true;
 }
@@ -432,7 +567,13 @@ __device__ __forceinline__ bool op_slope(const DevStage& st, WStream& s, double*
     if (mo == 0.0) return false;
     const double sign = next_double(s, w.lane) < 0.5 ? 1.0 : -1.0;
     const double stop = sign * mo;
-    for (int t = w.lane; t < L; t += 32) cur[t] = cur[t] + linspace_at(0.0, stop, L, t);
+    const Linspace ls(0.0, stop, L);
+    if (ls.fast()) {
+#pragma unroll 4
+        for (int t = w.lane; t < L; t += 32) cur[t] = cur[t] + ls.at_fast(t);
+    } else {
+        for (int t = w.lane; t < L; t += 32) cur[t] = cur[t] + ls.at(t);
+    }
     __syncwarp();
     return true;
 }
@@ -445,7 +586,8 @@ __device__ __noinline__ bool warp_knots(int len, int nk, double intensity, WStre
     double* warped = w.small + nk;
     double* tmp = w.small + 2 * nk;
     const double spacing = span / (double)(nk - 1);
-    for (int k = w.lane; k < nk; k += 32) knots[k] = linspace_at(0.0, span, nk, k);
+    const Linspace ls(0.0, span, nk);
+    for (int k = w.lane; k < nk; k += 32) knots[k] = ls.at(k);
     __syncwarp();
     const int ni = nk - 2;
     for (int k = 0; k < ni; ++k) {
@@ -482,6 +624,9 @@ __device__ __noinline__ bool warp_knots(int len, int nk, double intensity, WStre
         warped[nk - 1] = span;
     }
     __syncwarp();
+    double* sl = w.small + 2 * nk;  // interp slopes of the map (tmp no longer needed)
+    for (int k = w.lane; k < nk - 1; k += 32) sl[k] = (warped[k + 1] - warped[k]) / (knots[k + 1] - knots[k]);
+    __syncwarp();
     bool ok = true;
     for (int k = 1; k < nk; ++k) ok = ok && !(warped[k] - warped[k - 1] <= 0);
     return ok;
@@ -501,8 +646,11 @@ __device__ __forceinline__ bool op_time_warp(const DevStage& st, WStream& s, dou
     }
     const double* knots = w.small;
     const double* warped = w.small + nk;
+    const double* sl = w.small + 2 * nk;
+    const double inv = (double)(nk - 1) / ((double)L - 1.0);
+#pragma unroll 4
     for (int t = w.lane; t < L; t += 32)
-        oth[t] = interp_grid(interp1((double)t, knots, warped, nk), cur, L);
+        oth[t] = interp_grid_fast(interp_slopes((double)t, knots, warped, sl, nk, (int)((double)t * inv)), cur, L);
     __syncwarp();
     swapbuf(cur, oth);
     return true;
@@ -524,10 +672,15 @@ __device__ __forceinline__ bool op_window_warp(const DevStage& st, WStream& s, d
     }
     const double* knots = w.small;
     const double* warped = w.small + nk;
+    const double* sl = w.small + 2 * nk;
     const double* win = cur + start;
+    const double inv = (double)(nk - 1) / ((double)wsz - 1.0);
+#pragma unroll 4
     for (int t = w.lane; t < L; t += 32) {
         int u = t - start;
-        oth[t] = (u >= 0 && u < wsz) ? interp_grid(interp1((double)u, knots, warped, nk), win, wsz) : cur[t];
+        oth[t] = (u >= 0 && u < wsz)
+                     ? interp_grid_fast(interp_slopes((double)u, knots, warped, sl, nk, (int)((double)u * inv)), win, wsz)
+                     : cur[t];
     }
     __syncwarp();
     swapbuf(cur, oth);
@@ -615,35 +768,35 @@ __device__ __forceinline__ bool op_speed_warp(const DevStage& st, WStream& s, do
         }
     }
     __syncwarp();
+    int* sbt = reinterpret_cast<int*>(w.iscr);  // segment starts sb[m], m <= K
+    for (int m = w.lane; m <= K; m += 32) sbt[m] = (int)(((int64_t)m * L + K) / segs);
+    __syncwarp();
     auto tau_raw = [&](int t) {
-        int m = (int)(((int64_t)t * segs) / L);
-        int sb = (int)(((int64_t)m * L + K) / segs);
-        return base[m] + speeds[m] * (double)(t - sb);
+        int m = 0;  // floor(t * segs / L) == #{q in 1..K : sb[q] <= t}
+        for (int q = 1; q <= K; ++q) m += (t >= sbt[q]) ? 1 : 0;
+        return base[m] + speeds[m] * (double)(t - sbt[m]);
     };
     const double f = ((double)L - 1.0) / tau_raw(L - 1);
     const bool cubic = st.i[1] != 0;
+#pragma unroll 2
     for (int t = w.lane; t < L; t += 32) {
-        double tau = (t == L - 1) ? (double)L - 1.0 : tau_raw(t) * f;
+        const double tau = (t == L - 1) ? (double)L - 1.0 : tau_raw(t) * f;
+        int j = (int)floor(tau);
+        j = j < 0 ? 0 : (j > L - 2 ? L - 2 : j);
+        const double fr = tau - (double)j;
+        const double p1 = cur[j], p2 = cur[j + 1];
         double y;
-        if (tau >= (double)(L - 1)) {
-            y = cur[L - 1];
-        } else if (tau <= 0.0) {
-            y = cur[0];
+        if (cubic) {
+            const double p0 = cur[j > 0 ? j - 1 : 0], p3 = cur[j + 2 < L ? j + 2 : L - 1];
+            const double a = ((-0.5 * p0 + 1.5 * p1) - 1.5 * p2) + 0.5 * p3;
+            const double b = ((p0 - 2.5 * p1) + 2.0 * p2) - 0.5 * p3;
+            const double c = -0.5 * p0 + 0.5 * p2;
+            y = ((a * fr + b) * fr + c) * fr + p1;
         } else {
-            int j = (int)floor(tau);
-            if (j > L - 2) j = L - 2;
-            double fr = tau - (double)j;
-            if (cubic) {
-                double p0 = cur[j > 0 ? j - 1 : 0], p1 = cur[j], p2 = cur[j + 1];
-                double p3 = cur[j + 2 < L ? j + 2 : L - 1];
-                double a = ((-0.5 * p0 + 1.5 * p1) - 1.5 * p2) + 0.5 * p3;
-                double b = ((p0 - 2.5 * p1) + 2.0 * p2) - 0.5 * p3;
-                double c = -0.5 * p0 + 0.5 * p2;
-                y = ((a * fr + b) * fr + c) * fr + p1;
-            } else {
-                y = cur[j] + (cur[j + 1] - cur[j]) * fr;
-            }
+            y = p1 + (p2 - p1) * fr;
         }
+        y = (tau >= (double)(L - 1)) ? cur[L - 1] : y;
+        y = (tau <= 0.0) ? cur[0] : y;
         oth[t] = y;
     }
     __syncwarp();
@@ -667,8 +820,8 @@ __device__ __forceinline__ void perturb_spectrum(const DevStage& st, WStream& s,
         const bool even = (L % 2 == 0);
         const int hi = even ? bins - 1 : bins;
         double* ph = scratch + bins;  // scratch holds >= 2 * bins doubles
-        normals(s, w.lane, bins, [&](int k, double z) { amp[k] = 0.0 + sa * z; });
-        normals(s, w.lane, bins, [&](int k, double z) { ph[k] = 0.0 + sp * z; });
+        normals(s, w.lane, bins, w.zig, [&](int k, double z) { amp[k] = 0.0 + sa * z; });
+        normals(s, w.lane, bins, w.zig, [&](int k, double z) { ph[k] = 0.0 + sp * z; });
         __syncwarp();
         for (int b = 1 + w.lane; b < hi; b += 32) {
             double2 v = X[b];

@@ -239,45 +239,73 @@ __device__ __forceinline__ double std_normal(WStream& s, int lane) {
     }
 }
 
+// Inline window refill for the bulk walks (the Philox rounds are emitted
+// once per walk instantiation; scalar draws use the out-of-line refill).
+__device__ __forceinline__ void refill_inline(WStream& s, int lane) {
+    const uint64_t blk0 = s.wpos >> 2;
+    uint64_t o0, o1, o2, o3;
+    philox(s.k0, s.k1, blk0 + (uint64_t)lane + 1, o0, o1, o2, o3);
+    __syncwarp();
+    ulonglong2* w2 = reinterpret_cast<ulonglong2*>(s.winbuf) + 2 * lane;
+    w2[0] = make_ulonglong2(o0, o1);
+    w2[1] = make_ulonglong2(o2, o3);
+    __syncwarp();
+    s.win = s.winbuf;
+    s.wb = blk0 << 2;
+    s.wn = SA_WIN;
+}
+
 // `count` standard normals in stream order; emit(k, z) is called exactly
 // once per k by exactly one lane (k = normal index 0..count-1).
+// zig: the fast-path table (shared memory copy of g_zig).
 template <class Emit>
-__device__ __forceinline__ void normals(WStream& s, int lane, int count, Emit&& emit) {
+__device__ __forceinline__ void normals(WStream& s, int lane, int count, const ZigEntry* __restrict__ zig,
+                                        Emit&& emit) {
     int k = 0;
     while (k < count) {
-        if (s.wpos >= s.wb + s.wn) refill(s, lane);
+        if (s.wpos >= s.wb + s.wn) refill_inline(s, lane);
         const uint32_t wn = s.wn;
         uint32_t sp = (uint32_t)(s.wpos - s.wb);
-        // classify this lane's words (positions 4*lane + r of the window)
+        // classify this lane's words (window positions 4*lane + r)
         double z[4];
         uint32_t slowbits = 0;
+        {
+            uint64_t wv[4];
+            if (4u * lane < wn) {
+                const ulonglong2* w2 = reinterpret_cast<const ulonglong2*>(s.win) + 2 * lane;
+                ulonglong2 a = w2[0], b = w2[1];
+                wv[0] = a.x; wv[1] = a.y; wv[2] = b.x; wv[3] = b.y;
+            } else {
+                wv[0] = wv[1] = wv[2] = wv[3] = 0;
+            }
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            uint32_t p = 4u * lane + r;
-            uint64_t w = p < wn ? s.win[p] : 0;
-            int idx = (int)(w & 0xff);
-            uint64_t rr = w >> 8;
-            uint64_t rabs = (rr >> 1) & 0x000fffffffffffffULL;
-            ZigEntry ze = g_zig[idx];
-            double x = (double)rabs * ze.wi;
-            z[r] = (rr & 1) ? -x : x;
-            if (p < wn && !(rabs < ze.ki)) slowbits |= 1u << r;
+            for (int r = 0; r < 4; ++r) {
+                const uint64_t w = wv[r];
+                const uint64_t rr = w >> 8;
+                const uint64_t rabs = (rr >> 1) & 0x000fffffffffffffULL;
+                const ZigEntry ze = zig[w & 0xff];
+                const double x = (double)rabs * ze.wi;
+                z[r] = (rr & 1) ? -x : x;
+                if (!(rabs < ze.ki)) slowbits |= 1u << r;
+            }
+            if (4u * lane >= wn) slowbits = 0;
         }
         for (;;) {
+            // first slow word at or after sp
             uint32_t mine = 0xffffffffu;
 #pragma unroll
             for (int r = 3; r >= 0; --r) {
-                uint32_t p = 4u * lane + r;
+                const uint32_t p = 4u * lane + r;
                 if (((slowbits >> r) & 1u) && p >= sp) mine = p;
             }
             uint32_t t = __reduce_min_sync(SA_FULL, mine);
-            if (t > wn) t = wn;
+            t = t > wn ? wn : t;
             uint32_t nf = t - sp;
             if (nf > (uint32_t)(count - k)) nf = (uint32_t)(count - k);
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
-                uint32_t p = 4u * lane + r;
-                if (p >= sp && p < sp + nf) emit(k + (int)(p - sp), z[r]);
+                const uint32_t off = 4u * lane + r - sp;  // wraps when p < sp
+                if (off < nf) emit(k + (int)off, z[r]);
             }
             k += (int)nf;
             sp += nf;
@@ -285,12 +313,28 @@ __device__ __forceinline__ void normals(WStream& s, int lane, int count, Emit&& 
                 s.wpos = s.wb + sp;
                 break;
             }
-            // slow word at sp: resolve uniformly
-            uint64_t r0 = s.win[sp];
+            // slow word at sp (numpy's wedge / tail paths), resolved uniformly
+            const uint64_t r0 = s.win[sp];
             s.wpos = s.wb + sp + 1;
-            uint64_t old_wb = s.wb;
+            const int idx = (int)(r0 & 0xff);
+            const uint64_t old_wb = s.wb;
+            bool ok;
             double v;
-            if (zig_slow(s, lane, r0, v)) {
+            if (idx != 0) {  // wedge: one uniform, then the density test
+                const uint64_t rr = r0 >> 8;
+                const uint64_t rabs = (rr >> 1) & 0x000fffffffffffffULL;
+                double x = (double)rabs * zig[idx].wi;
+                if (rr & 1) x = -x;
+                if (s.wpos >= s.wb + s.wn) refill(s, lane);
+                const double u = u53(s.win[s.wpos - s.wb]);
+                s.wpos += 1;
+                const double fi0 = __ldg(&g_fi[idx - 1]), fi1 = __ldg(&g_fi[idx]);
+                ok = ((fi0 - fi1) * u + fi1) < exp(-0.5 * x * x);
+                v = x;
+            } else {
+                ok = zig_slow(s, lane, r0, v);  // tail: out of line, ~3e-4 of words
+            }
+            if (ok) {
                 if (lane == 0) emit(k, v);
                 k += 1;
             }
@@ -306,14 +350,19 @@ template <class Emit>
 __device__ __forceinline__ void doubles(WStream& s, int lane, int count, Emit&& emit) {
     int k = 0;
     while (k < count) {
-        if (s.wpos >= s.wb + s.wn) refill(s, lane);
-        uint32_t sp = (uint32_t)(s.wpos - s.wb);
-        uint32_t avail = s.wn - sp;
-        uint32_t take = avail < (uint32_t)(count - k) ? avail : (uint32_t)(count - k);
+        if (s.wpos >= s.wb + s.wn) refill_inline(s, lane);
+        const uint32_t sp = (uint32_t)(s.wpos - s.wb);
+        const uint32_t avail = s.wn - sp;
+        const uint32_t take = avail < (uint32_t)(count - k) ? avail : (uint32_t)(count - k);
+        if (4u * lane < s.wn) {
+            const ulonglong2* w2 = reinterpret_cast<const ulonglong2*>(s.win) + 2 * lane;
+            ulonglong2 a = w2[0], b = w2[1];
+            const uint64_t wv[4] = {a.x, a.y, b.x, b.y};
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            uint32_t p = 4u * lane + r;
-            if (p >= sp && p < sp + take) emit(k + (int)(p - sp), u53(s.win[p]));
+            for (int r = 0; r < 4; ++r) {
+                const uint32_t off = 4u * lane + r - sp;
+                if (off < take) emit(k + (int)off, u53(wv[r]));
+            }
         }
         k += (int)take;
         s.wpos += take;
