@@ -194,6 +194,7 @@ def run_b200(args, rank, world, local_rank):
 
     from bench_inputs import CONFIG_SHAPES, device_walks, host_input, pipeline
     from paper_2601_03159_b200 import _engine, _native
+    from paper_2601_03159_b200.sharding import shard_range
 
     cfg = args.config
     torch.cuda.set_device(local_rank)
@@ -204,7 +205,7 @@ def run_b200(args, rank, world, local_rank):
         N = args.n_series
     pipe = pipeline(cfg)
     L_out = pipe.projected_length(L)
-    r0, r1 = N * rank // world, N * (rank + 1) // world
+    r0, r1 = shard_range(N, rank, world)
     n = r1 - r0
     if cfg == 5:
         x = device_walks(n, L, 5, dev, row0=r0)
