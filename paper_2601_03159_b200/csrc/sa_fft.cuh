@@ -13,6 +13,12 @@
 //                  conjugate (IFFT(Z) = conj(FFT(conj Z))), 1/M scaling,
 //                  result read back as the real series in place.
 //
+// General lengths (pocketfft handles any L): the complex length N (= L/2
+// packed for even L, = L for odd L, whose real input is complexified) is
+// factored on the host into radix-8/4/2 passes followed by one generic pass
+// per remaining prime factor (each output of a generic pass is a direct
+// R-term sum with one twiddle lookup per term).
+//
 // Twiddles come from a per-length table tw[k] = exp(-2*pi*i*k/L), k < L,
 // computed on the host in long double (correctly rounded) and cached.
 // Parity with pocketfft is to tolerance (FFT rounding differs), so FMAs are
@@ -80,7 +86,7 @@ __device__ __forceinline__ void stockham_pass(const double2* __restrict__ src, d
     const int Q = M / R;
     const int tstep = L / (Ns * R);
     for (int j = lane; j < Q; j += 32) {
-        int k = j & (Ns - 1);
+        int k = j % Ns;
         double2 v[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) v[r] = src[j + r * Q];
@@ -102,40 +108,82 @@ __device__ __forceinline__ void stockham_pass(const double2* __restrict__ src, d
     __syncwarp();
 }
 
-// M-point complex FFT (M a power of two), data in a; b is scratch.
-// Returns the buffer holding the result.
-template <bool INV>
-__device__ double2* fft_pow2(double2* a, double2* b, int M, const double2* tw, int L, int lane) {
+// Host-built pass plan of an N-point complex FFT (N | L).
+#define SA_FFT_MAXPASS 24
+struct FftGeo {
+    int32_t N;         // complex transform length
+    int32_t packed;    // 1: even L, N = L/2 (real input viewed as complex)
+    int32_t npass;
+    int32_t pad;
+    int16_t radix[SA_FFT_MAXPASS];
+};
+
+// Generic radix-R Stockham pass (any R | N): each output is the direct sum
+// V[u] = sum_r src[j + rQ] * W_N^(r*k*N/(Ns R) + (r*u mod R)*N/R).
+__device__ __forceinline__ void generic_pass(const double2* __restrict__ src, double2* __restrict__ dst, int N, int Ns,
+                                             int R, const double2* __restrict__ tw, int L, int lane) {
+    const int Q = N / R;
+    const int ts = L / N;               // table stride for W_N
+    const int a = N / (Ns * R), b = N / R;
+    for (int idx = lane; idx < Q * R; idx += 32) {
+        const int j = idx % Q, u = idx / Q;
+        const int k = j % Ns;
+        double2 acc = make_double2(0.0, 0.0);
+        int e1 = 0, e2 = 0;             // r*k*a mod N, (r*u mod R)*b
+        for (int r = 0; r < R; ++r) {
+            int e = e1 + e2;
+            e = e >= N ? e - N : e;
+            const double2 w = __ldg(&tw[e * ts]);
+            acc = cadd(acc, cmul(src[j + r * Q], w));
+            e1 += k * a;
+            e1 %= N;
+            e2 += u * b;
+            e2 = e2 >= N ? e2 - N : e2;
+        }
+        dst[(j - k) * R + k + u * Ns] = acc;
+    }
+    __syncwarp();
+}
+
+// Forward N-point complex FFT per the plan; data in a, b is scratch.
+__device__ __forceinline__ double2* fft_any(double2* a, double2* b, const FftGeo& g, const double2* tw, int L,
+                                            int lane) {
     int Ns = 1;
     double2* src = a;
     double2* dst = b;
-    while (Ns < M) {
-        int rem = M / Ns;
-        if (rem >= 8 && rem != 16) {  // 16 = 4 x 4 keeps passes balanced
-            stockham_pass<8, INV>(src, dst, M, Ns, tw, L, lane);
-            Ns *= 8;
-        } else if (rem >= 4) {
-            stockham_pass<4, INV>(src, dst, M, Ns, tw, L, lane);
-            Ns *= 4;
-        } else {
-            stockham_pass<2, INV>(src, dst, M, Ns, tw, L, lane);
-            Ns *= 2;
-        }
+    const int ts = L / g.N;  // W_N = tw[.. * ts]; the radix passes take the table length L
+    for (int p = 0; p < g.npass; ++p) {
+        const int R = g.radix[p];
+        if (R == 8) stockham_pass<8, false>(src, dst, g.N, Ns, tw, L, lane);
+        else if (R == 4) stockham_pass<4, false>(src, dst, g.N, Ns, tw, L, lane);
+        else if (R == 2) stockham_pass<2, false>(src, dst, g.N, Ns, tw, L, lane);
+        else generic_pass(src, dst, g.N, Ns, R, tw, L, lane);
+        Ns *= R;
         double2* t = src;
         src = dst;
         dst = t;
     }
+    (void)ts;
     return src;
 }
 
-// rfft of x (length L = 2M, in buffer xa viewed as complex) into X[0..M]
-// (M + 1 complex).  xb is scratch of the same capacity.  Returns the buffer
-// holding X (one of xa / xb); the other is free afterwards.
-__device__ __forceinline__ double2* rfft_warp(double* xa, double* xb, int L, const double2* tw, int lane) {
-    const int M = L >> 1;
+// rfft of the real series x (length L, in buffer xa) -> X[0 .. L/2]
+// (complex, bins = L/2 + 1).  xb is scratch of the same capacity (>= 2L + 2
+// doubles for odd L).  Returns the buffer holding X; the other is free.
+__device__ __forceinline__ double2* rfft_any(double* xa, double* xb, int L, const FftGeo& g, const double2* tw,
+                                            int lane) {
     double2* za = reinterpret_cast<double2*>(xa);
     double2* zb = reinterpret_cast<double2*>(xb);
-    double2* Z = fft_pow2<false>(za, zb, M, tw, L, lane);
+    if (!g.packed) {  // odd L: complexify into xb, N = L transform, keep bins
+        for (int n = lane; n < L; n += 32) zb[n] = make_double2(xa[n], 0.0);
+        __syncwarp();
+        double2* Z = fft_any(zb, za, g, tw, L, lane);
+        if (lane == 0) Z[0].y = 0.0;
+        __syncwarp();
+        return Z;
+    }
+    const int M = L >> 1;
+    double2* Z = fft_any(za, zb, g, tw, L, lane);
     double2* X = (Z == za) ? zb : za;
     for (int k = lane; k <= M; k += 32) {
         double2 zk = Z[k == M ? 0 : k];
@@ -155,15 +203,33 @@ __device__ __forceinline__ double2* rfft_warp(double* xa, double* xb, int L, con
     return X;
 }
 
-// irfft of X[0..M] (in buffer X) to a real series of length L = 2M.
-// Returns the buffer holding the series (one of X / other).
-__device__ __forceinline__ double* irfft_warp(double2* X, double2* other, int L, const double2* tw, int lane) {
+// irfft of X[0 .. L/2] (buffer X) to a real series of length L; `other` is
+// free scratch.  Uses IFFT(Z) = conj(FFT(conj Z)).  Returns the buffer
+// holding the series.  irfft ignores the imaginary part of the DC bin (and
+// of the Nyquist bin for even L).
+__device__ __forceinline__ double* irfft_any(double2* X, double2* other, int L, const FftGeo& g, const double2* tw,
+                                            int lane) {
+    if (!g.packed) {  // odd L: Hermitian completion, full transform, real part
+        const int bins = L / 2 + 1;
+        for (int k = lane; k < bins; k += 32) {
+            double2 v = X[k];
+            if (k == 0) v.y = 0.0;
+            other[k] = make_double2(v.x, -v.y);
+            if (k > 0) other[L - k] = v;
+        }
+        __syncwarp();
+        double2* Z = fft_any(other, X, g, tw, L, lane);
+        double* out = reinterpret_cast<double*>(Z == X ? other : X);
+        const double s = 1.0 / (double)L;
+        for (int n = lane; n < L; n += 32) out[n] = Z[n].x * s;
+        __syncwarp();
+        return out;
+    }
     const int M = L >> 1;
-    // inverse split; store conj(Z) so the forward passes compute conj(IFFT)
     for (int k = lane; k < M; k += 32) {
         double2 xk = X[k];
         double2 xc = X[M - k];
-        if (k == 0) { xk.y = 0.0; xc.y = 0.0; }  // irfft ignores im of DC / Nyquist
+        if (k == 0) { xk.y = 0.0; xc.y = 0.0; }
         xc.y = -xc.y;
         double er = 0.5 * (xk.x + xc.x), ei = 0.5 * (xk.y + xc.y);
         double dr = 0.5 * (xk.x - xc.x), di = 0.5 * (xk.y - xc.y);
@@ -173,7 +239,7 @@ __device__ __forceinline__ double* irfft_warp(double2* X, double2* other, int L,
         other[k] = make_double2(er - o.y, -(ei + o.x));
     }
     __syncwarp();
-    double2* Z = fft_pow2<false>(other, X, M, tw, L, lane);
+    double2* Z = fft_any(other, X, g, tw, L, lane);
     const double s = 1.0 / (double)M;
     for (int k = lane; k < M; k += 32) {
         double2 z = Z[k];

@@ -230,6 +230,7 @@ __global__ void __launch_bounds__(512) chain_kernel(const __grid_constant__ Chai
 
 // ------------------------------------------------------------ spectral kernels
 struct FftParams {
+    FftGeo fft;
     const double* x;
     const double* re;
     const double* im;
@@ -251,7 +252,7 @@ __global__ void __launch_bounds__(32) rfft_kernel(const __grid_constant__ FftPar
         const double* src = p.x + row * p.L;
         for (int t = lane; t < p.L; t += 32) A[t] = src[t];
         __syncwarp();
-        double2* X = rfft_warp(A, B, p.L, p.tw, lane);
+        double2* X = rfft_any(A, B, p.L, p.fft, p.tw, lane);
         for (int k = lane; k < bins; k += 32) {
             p.reo[row * bins + k] = X[k].x;
             p.imo[row * bins + k] = X[k].y;
@@ -269,7 +270,7 @@ __global__ void __launch_bounds__(32) irfft_kernel(const __grid_constant__ FftPa
     for (int64_t row = blockIdx.x; row < p.n; row += gridDim.x) {
         for (int k = lane; k < bins; k += 32) X[k] = make_double2(p.re[row * bins + k], p.im[row * bins + k]);
         __syncwarp();
-        double* y = irfft_warp(X, O, p.L, p.tw, lane);
+        double* y = irfft_any(X, O, p.L, p.fft, p.tw, lane);
         for (int t = lane; t < p.L; t += 32) p.xo[row * p.L + t] = y[t];
         __syncwarp();
     }
@@ -429,7 +430,44 @@ int get_twiddles(int dev, int L, const double2** out) {
     return SA_OK;
 }
 
-bool fft_len_supported(int64_t L) { return L >= 2 && (L % 2) == 0 && ((L / 2) & (L / 2 - 1)) == 0; }
+// Pass plan of the complex transform used for a real length L: N = L/2
+// (packed) for even L, N = L for odd L; radix 8/4/2 passes first, then one
+// generic pass per remaining prime factor (ascending).
+bool make_fft_geo(int64_t L, FftGeo* g) {
+    std::memset(g, 0, sizeof(*g));
+    if (L < 1) return false;
+    g->packed = (L % 2 == 0) ? 1 : 0;
+    int64_t N = g->packed ? L / 2 : L;
+    g->N = (int32_t)N;
+    int64_t rem = N;
+    int np = 0;
+    int64_t p2 = 1;
+    while (rem % 2 == 0) { rem /= 2; p2 *= 2; }
+    int64_t left = p2;
+    while (left > 1) {
+        int r = (left >= 8 && left != 16) ? 8 : (left >= 4 ? 4 : 2);
+        if (np >= SA_FFT_MAXPASS) return false;
+        g->radix[np++] = (int16_t)r;
+        left /= r;
+    }
+    for (int64_t f = 3; rem > 1; f += 2) {
+        while (rem % f == 0) {
+            if (np >= SA_FFT_MAXPASS || f > 32767) return false;
+            g->radix[np++] = (int16_t)f;
+            rem /= f;
+        }
+        if (f * f > rem && rem > 1) {
+            if (np >= SA_FFT_MAXPASS || rem > 32767) return false;
+            g->radix[np++] = (int16_t)rem;
+            rem = 1;
+        }
+    }
+    g->npass = np;
+    return true;
+}
+
+// doubles per buffer a spectral stage needs at length L
+int64_t fft_lcap(int64_t L) { return (L % 2 == 0) ? L + 2 : 2 * L + 2; }
 
 bool is_spectral(int op) { return op == SA_OP_APP || op == SA_OP_FREQ_MASK || op == SA_OP_SINUSOID; }
 
@@ -489,12 +527,11 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
         if (s.op == SA_OP_CONVOLVE && (s.aux_off < 0 || s.aux_len < 1 || s.aux_off + s.aux_len > n_aux))
             return fail(SA_ERR_INVALID_ARG, "convolve taps out of range");
         if (is_spectral(s.op) && s.probability > 0.0) {
-            if (!fft_len_supported(L))
-                return fail(SA_ERR_UNSUPPORTED,
-                            "spectral stage at length " + std::to_string(L) +
-                                ": this build's FFT needs an even length with L/2 a power of two");
+            if (!make_fft_geo(L, &d.fft))
+                return fail(SA_ERR_UNSUPPORTED, "no FFT plan for length " + std::to_string(L));
             int rc = get_twiddles(dev, (int)L, &d.tw);
             if (rc) return rc;
+            spike_lcap = std::max<int64_t>(spike_lcap, fft_lcap(L));
         }
         if (s.probability == 1.0 && (s.op == SA_OP_CROP || s.op == SA_OP_RESIZE)) L = s.i[0];
         d.len_out = (int32_t)L;
@@ -570,7 +607,7 @@ int flags_status(uint32_t f) {
 }
 
 int fft_plan_smem(int dev, int64_t L, int* lcap, size_t* smem, int* grid, const void* kern, int64_t n) {
-    *lcap = (int)((L + 2 + 1) & ~1LL);
+    *lcap = (int)((fft_lcap(L) + 1) & ~1LL);
     *smem = (size_t)(*lcap) * 8 * 2 + 8 * SA_WIN + 64;
     DeviceState& ds = g_dev[dev];
     if (*smem > ds.smem_optin) return fail(SA_ERR_UNSUPPORTED, "series too long");
@@ -714,9 +751,8 @@ int sa_fft_forward(const double* d_in, int64_t n, int64_t len, double* d_re, dou
     int dev;
     int rc = ensure_device(&dev);
     if (rc) return rc;
-    if (!fft_len_supported(len))
-        return fail(SA_ERR_UNSUPPORTED, "this build's FFT needs an even length with L/2 a power of two");
     FftParams p{};
+    if (!make_fft_geo(len, &p.fft)) return fail(SA_ERR_UNSUPPORTED, "no FFT plan for this length");
     p.x = d_in; p.reo = d_re; p.imo = d_im; p.n = n; p.L = (int32_t)len;
     rc = get_twiddles(dev, (int)len, &p.tw);
     if (rc) return rc;
@@ -736,9 +772,8 @@ int sa_fft_inverse(const double* d_re, const double* d_im, int64_t n, int64_t le
     int dev;
     int rc = ensure_device(&dev);
     if (rc) return rc;
-    if (!fft_len_supported(len))
-        return fail(SA_ERR_UNSUPPORTED, "this build's FFT needs an even length with L/2 a power of two");
     FftParams p{};
+    if (!make_fft_geo(len, &p.fft)) return fail(SA_ERR_UNSUPPORTED, "no FFT plan for this length");
     p.re = d_re; p.im = d_im; p.xo = d_out; p.n = n; p.L = (int32_t)len;
     rc = get_twiddles(dev, (int)len, &p.tw);
     if (rc) return rc;

@@ -26,6 +26,7 @@ struct DevStage {
     double f[4];
     int64_t i[4];
     const double2* tw;  // exp(-2 pi i k / len_in), k < len_in (spectral ops)
+    FftGeo fft;         // transform plan for len_in (spectral ops)
 };
 
 struct ChainParams {
@@ -876,11 +877,11 @@ __device__ __forceinline__ void perturb_spectrum(const DevStage& st, WStream& s,
 // freqaugment.py:37-47 SpectralAugmenter._apply (time-domain entry)
 __device__ __forceinline__ bool op_spectral(const DevStage& st, WStream& s, double*& cur, double*& oth, int L, Warp& w) {
     if (spectral_noop(st)) return false;
-    double2* X = rfft_warp(cur, oth, L, st.tw, w.lane);
+    double2* X = rfft_any(cur, oth, L, st.fft, st.tw, w.lane);
     double* free_buf = (reinterpret_cast<double*>(X) == cur) ? oth : cur;
     perturb_spectrum(st, s, X, L, free_buf, w);
     double2* other = reinterpret_cast<double2*>(free_buf);
-    double* y = irfft_warp(X, other, L, st.tw, w.lane);
+    double* y = irfft_any(X, other, L, st.fft, st.tw, w.lane);
     if (y != cur) swapbuf(cur, oth);
     return true;
 }
