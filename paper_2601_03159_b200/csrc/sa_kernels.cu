@@ -115,8 +115,9 @@ __global__ void __launch_bounds__(512) chain_kernel(const __grid_constant__ Chai
     // Rows are dealt to warps; the trip count is uniform across the CTA so
     // the stage-boundary barriers below are reached by every warp.
     for (int64_t base = (int64_t)blockIdx.x * nw; base < p.rows_out; base += (int64_t)gridDim.x * nw) {
-        const int64_t row = base + wid;
-        const bool active = row < p.rows_out;
+        const int64_t slot = base + wid;
+        const bool active = slot < p.rows_out;
+        const int64_t row = (active && p.order) ? (int64_t)p.order[slot] : slot;
         const int64_t in_row = (active ? row : 0) / r;
         const double* src = p.in + in_row * (int64_t)p.len_in;
         uint64_t fire_lo = 0;  // fire bits of stages 0..63
@@ -226,6 +227,70 @@ __global__ void __launch_bounds__(512) chain_kernel(const __grid_constant__ Chai
         __syncwarp();
     }
     if (flags && lane == 0) atomicOr(p.flags, flags);
+}
+
+
+// ------------------------------------------------------------ fire-pattern scheduling
+// The stage barrier makes every stage cost the slowest firing warp of the
+// CTA.  Rows whose gates fire the same expensive stages are therefore
+// grouped: key = fire bits of the (up to 16) most expensive gated stages,
+// counting-sorted; the chain kernel takes rows in that order.  Output rows
+// are still written to their own positions, so results are unchanged.
+__device__ __forceinline__ uint32_t fire_key(const ChainParams& p, int64_t row) {
+    const int64_t in_row = row / p.repeat_r;
+    uint32_t key = 0;
+    for (int q = 0; q < p.key_bits; ++q) {
+        const DevStage& st = p.st[p.key_stage[q]];
+        const uint64_t series =
+            st.post_repeat ? (uint64_t)(p.offset * p.repeat_r + row) : (uint64_t)(p.offset + in_row);
+        uint64_t k0, k1, o0, o1, o2, o3;
+        derive_key(p.seed, (uint64_t)st.index, series, k0, k1);
+        philox(k0, k1, 1, o0, o1, o2, o3);
+        key = (key << 1) | (u53(o0) < st.prob ? 1u : 0u);
+    }
+    return key;
+}
+
+__global__ void __launch_bounds__(256) key_hist_kernel(const __grid_constant__ ChainParams p, uint32_t* keys,
+                                                       uint32_t* hist) {
+    for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < p.rows_out;
+         row += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = fire_key(p, row);
+        keys[row] = k;
+        atomicAdd(&hist[k], 1u);
+    }
+}
+
+// exclusive scan of nb <= 65536 counters, one CTA of 1024 threads
+__global__ void __launch_bounds__(1024) key_scan_kernel(uint32_t* hist, int nb) {
+    __shared__ uint32_t part[1024];
+    const int per = (nb + 1023) / 1024;
+    const int a = threadIdx.x * per, b = min(nb, a + per);
+    uint32_t s = 0;
+    for (int i = a; i < b; ++i) s += hist[i];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {
+        uint32_t v = threadIdx.x >= off ? part[threadIdx.x - off] : 0u;
+        __syncthreads();
+        part[threadIdx.x] += v;
+        __syncthreads();
+    }
+    uint32_t run = threadIdx.x ? part[threadIdx.x - 1] : 0u;
+    for (int i = a; i < b; ++i) {
+        const uint32_t c = hist[i];
+        hist[i] = run;
+        run += c;
+    }
+}
+
+__global__ void __launch_bounds__(256) key_scatter_kernel(int64_t rows, const uint32_t* keys, uint32_t* offs,
+                                                          int32_t* order) {
+    for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < rows;
+         row += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t pos = atomicAdd(&offs[keys[row]], 1u);
+        order[pos] = (int32_t)row;
+    }
 }
 
 // ------------------------------------------------------------ spectral kernels
@@ -360,6 +425,12 @@ struct DeviceState {
 };
 std::map<int, DeviceState> g_dev;
 
+int current_dev_cached() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+}
+
 int current_device(int* dev) {
     SA_CUDA(cudaGetDevice(dev));
     return SA_OK;
@@ -484,6 +555,21 @@ int env_int(const char* k, int d) {
     return v && *v ? atoi(v) : d;
 }
 
+// Relative per-series cost of an operator at L ~ 1e3 (tools/op_timing.py),
+// used only to choose which gates form the scheduling key.
+double op_cost(int op) {
+    switch (op) {
+        case SA_OP_APP: return 10.0;
+        case SA_OP_FREQ_MASK: case SA_OP_SINUSOID: return 4.5;
+        case SA_OP_JITTER: case SA_OP_NOISE_GAUSSIAN: case SA_OP_NOISE_SPIKE: return 3.0;
+        case SA_OP_SPEED_WARP: case SA_OP_DRIFT: case SA_OP_TIME_WARP: return 2.4;
+        case SA_OP_CONVOLVE: case SA_OP_RESIZE: return 1.5;
+        case SA_OP_NOISE_UNIFORM: case SA_OP_WINDOW_WARP: case SA_OP_DROPOUT: return 1.0;
+        case SA_OP_QUANTIZE: case SA_OP_POOL: return 0.5;
+        default: return 0.1;
+    }
+}
+
 // Lower the ABI stage table into kernel parameters and a launch shape.
 int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, int32_t n_aux, uint64_t seed,
               int64_t offset, int64_t n, int64_t len_in, int64_t len_out, Plan* plan) {
@@ -575,7 +661,21 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
     warps = std::max(1, std::min(warps, std::min(16, fit)));
     plan->warps = warps;
     plan->smem = (size_t)per_warp * warps + 256 * sizeof(ZigEntry);
-    p.sync_every = ns > 1 ? env_int("SA_SYNC_EVERY", 3) : 0;
+    p.sync_every = ns > 1 ? env_int("SA_SYNC_EVERY", 4) : 0;
+    // scheduling key: gated (0 < p < 1) stages, most expensive first
+    {
+        std::vector<std::pair<double, int>> cand;
+        for (int j = 0; j < ns; ++j)
+            if (stages[j].probability > 0.0 && stages[j].probability < 1.0 && stages[j].op != SA_OP_REPEAT)
+                cand.push_back({-op_cost(stages[j].op), j});
+        std::stable_sort(cand.begin(), cand.end());
+        int kb = (int)std::min<size_t>(16, cand.size());
+        // enough rows per bucket for the key to matter
+        while (kb > 0 && (p.rows_out >> kb) < 8 * (int64_t)warps) --kb;
+        if (env_int("SA_SCHEDULE", 1) == 0 || p.rows_out > INT32_MAX) kb = 0;
+        p.key_bits = kb;
+        for (int q = 0; q < kb; ++q) p.key_stage[q] = (int8_t)cand[q].second;
+    }
     int per_sm = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chain_kernel, 32 * warps, plan->smem);
     if (e != cudaSuccess) return cuda_fail(e, "occupancy");
@@ -586,6 +686,42 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
     return SA_OK;
 }
 
+// Schedule (fire-pattern counting sort) and launch the chain kernel for the
+// rows described by plan->p (in/out/flags/offset/rows_out already set).
+int launch_chain(Plan* plan, cudaStream_t stream) {
+    ChainParams& p = plan->p;
+    if (p.rows_out == 0) return SA_OK;
+    DeviceState& ds = g_dev[current_dev_cached()];
+    uint32_t* keys = nullptr;
+    uint32_t* hist = nullptr;
+    int32_t* order = nullptr;
+    p.order = nullptr;
+    while (p.key_bits > 0 && (p.rows_out >> p.key_bits) < 8 * (int64_t)plan->warps) --p.key_bits;
+    if (p.key_bits > 0) {
+        const int nb = 1 << p.key_bits;
+        SA_CUDA(cudaMallocAsync(&keys, sizeof(uint32_t) * (size_t)p.rows_out, stream));
+        SA_CUDA(cudaMallocAsync(&hist, sizeof(uint32_t) * (size_t)nb, stream));
+        SA_CUDA(cudaMallocAsync(&order, sizeof(int32_t) * (size_t)p.rows_out, stream));
+        SA_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (size_t)nb, stream));
+        const int g = (int)std::min<int64_t>((int64_t)ds.sms * 8, (p.rows_out + 255) / 256);
+        key_hist_kernel<<<g, 256, 0, stream>>>(p, keys, hist);
+        key_scan_kernel<<<1, 1024, 0, stream>>>(hist, nb);
+        key_scatter_kernel<<<g, 256, 0, stream>>>(p.rows_out, keys, hist, order);
+        SA_CUDA(cudaGetLastError());
+        __atomic_add_fetch(&g_launches, 3, __ATOMIC_RELAXED);
+        p.order = order;
+    }
+    chain_kernel<<<plan->grid, 32 * plan->warps, plan->smem, stream>>>(p);
+    SA_CUDA(cudaGetLastError());
+    __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
+    if (keys) {
+        SA_CUDA(cudaFreeAsync(keys, stream));
+        SA_CUDA(cudaFreeAsync(hist, stream));
+        SA_CUDA(cudaFreeAsync(order, stream));
+    }
+    return SA_OK;
+}
+
 int launch_plan(Plan* plan, const double* d_in, double* d_out, uint32_t* d_flags, cudaStream_t stream) {
     ChainParams& p = plan->p;
     p.in = d_in;
@@ -593,11 +729,7 @@ int launch_plan(Plan* plan, const double* d_in, double* d_out, uint32_t* d_flags
     p.flags = d_flags;
     p.bulk_in = ((p.len_in & 1) == 0 && (reinterpret_cast<uintptr_t>(d_in) & 15u) == 0) ? 1 : 0;
     SA_CUDA(cudaMemsetAsync(d_flags, 0, sizeof(uint32_t), stream));
-    if (p.rows_out == 0) return SA_OK;
-    chain_kernel<<<plan->grid, 32 * plan->warps, plan->smem, stream>>>(p);
-    SA_CUDA(cudaGetLastError());
-    __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
-    return SA_OK;
+    return launch_chain(plan, stream);
 }
 
 int flags_status(uint32_t f) {
@@ -733,10 +865,9 @@ int sa_pipeline_run_host(const sa_stage* stages, int32_t n_stages, const double*
         pl.p.out = ds.dout[c & 1];
         pl.p.flags = ds.dflags + (c & 1);
         pl.p.bulk_in = ((len_in & 1) == 0) ? 1 : 0;
-        if (pl.p.rows_out) {
-            chain_kernel<<<pl.grid, 32 * pl.warps, pl.smem, st>>>(pl.p);
-            SA_CUDA(cudaGetLastError());
-            __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
+        {
+            int rc2 = launch_chain(&pl, st);
+            if (rc2) return rc2;
         }
         SA_CUDA(cudaMemcpyAsync(h_out + r0 * r * len_out, ds.dout[c & 1], (size_t)(rows * row_out_b),
                                 cudaMemcpyDeviceToHost, st));

@@ -13,7 +13,8 @@ x = device_walks(n, L, 5, torch.device("cuda"))
 out = torch.empty((n, pipe.projected_length(L)), dtype=torch.float64, device="cuda")
 flags = torch.zeros(1, dtype=torch.int32, device="cuda")
 ref = None
-for warps, sync in [(1, 0), (2, 1), (4, 1), (8, 1), (0, 1), (0, 2), (0, 3), (0, 5), (0, 0)]:
+for warps, sync, sched in [(0, 3, 1), (0, 3, 0), (0, 1, 1), (0, 2, 1), (0, 4, 1), (0, 6, 1), (0, 20, 1)]:
+    os.environ['SA_SCHEDULE'] = str(sched)
     os.environ["SA_CTA_WARPS"] = str(warps)
     os.environ["SA_SYNC_EVERY"] = str(sync)
     for _ in range(2):
@@ -28,4 +29,4 @@ for warps, sync in [(1, 0), (2, 1), (4, 1), (8, 1), (0, 1), (0, 2), (0, 3), (0, 
     if ref is None:
         ref = out.clone()
     same = torch.equal(ref, out)
-    print(f"cfg{cfg} warps={warps or 'fit':>3} sync_every={sync}  {ms:8.3f} ms  {n * out.shape[1] / ms / 1e6:7.2f} Gpts/s  same={same}", flush=True)
+    print(f"cfg{cfg} warps={warps or 'fit':>3} sync_every={sync} sched={sched}  {ms:8.3f} ms  {n * out.shape[1] / ms / 1e6:7.2f} Gpts/s  same={same}", flush=True)
