@@ -77,31 +77,48 @@ __device__ __forceinline__ void dft8(double2* v) {
     }
 }
 
-// One Stockham pass of radix R over M points: src -> dst.
-// tw: exp(-2 pi i q / L), L = 2M; W_{Ns R}^{rk} = tw[r k (L / (Ns R))].
+// One Stockham pass of radix R (2, 4, 8) over M points: src -> dst, for
+// Ns = 2^lns (the power-of-two passes run first, so Ns is a power of two).
+// tw: exp(-2 pi i q / L); W_{Ns R}^{rk} = tw[r k tstep], tstep = L / (Ns R).
+// Twiddles: W^k, W^2k, W^4k are loaded, the odd powers multiplied out.
 template <int R, bool INV>
 __device__ __forceinline__ void stockham_pass(const double2* __restrict__ src, double2* __restrict__ dst,
-                                              int M, int Ns, const double2* __restrict__ tw, int L,
+                                              int M, int lns, const double2* __restrict__ tw, int tstep,
                                               int lane) {
     const int Q = M / R;
-    const int tstep = L / (Ns * R);
+    const int Ns = 1 << lns;
+#pragma unroll 2
     for (int j = lane; j < Q; j += 32) {
-        int k = j % Ns;
+        const int k = j & (Ns - 1);
         double2 v[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) v[r] = src[j + r * Q];
         if (Ns > 1) {
-#pragma unroll
-            for (int r = 1; r < R; ++r) {
-                double2 w = __ldg(&tw[r * k * tstep]);
-                if (INV) w.y = -w.y;
-                v[r] = cmul(v[r], w);
+            double2 w1 = __ldg(&tw[k * tstep]);
+            if (INV) w1.y = -w1.y;
+            if (R == 2) {
+                v[1] = cmul(v[1], w1);
+            } else {
+                double2 w2 = __ldg(&tw[2 * k * tstep]);
+                if (INV) w2.y = -w2.y;
+                const double2 w3 = cmul(w1, w2);
+                v[1] = cmul(v[1], w1);
+                v[2] = cmul(v[2], w2);
+                v[3] = cmul(v[3], w3);
+                if (R == 8) {
+                    double2 w4 = __ldg(&tw[4 * k * tstep]);
+                    if (INV) w4.y = -w4.y;
+                    v[4] = cmul(v[4], w4);
+                    v[5] = cmul(v[5], cmul(w1, w4));
+                    v[6] = cmul(v[6], cmul(w2, w4));
+                    v[7] = cmul(v[7], cmul(w3, w4));
+                }
             }
         }
         if (R == 2) dft2<INV>(v);
         if (R == 4) dft4<INV>(v);
         if (R == 8) dft8<INV>(v);
-        int base = (j - k) * R + k;
+        const int base = ((j >> lns) << (lns + (R == 8 ? 3 : (R == 4 ? 2 : 1)))) + k;
 #pragma unroll
         for (int r = 0; r < R; ++r) dst[base + r * Ns] = v[r];
     }
@@ -152,12 +169,18 @@ __device__ __forceinline__ double2* fft_any(double2* a, double2* b, const FftGeo
     double2* src = a;
     double2* dst = b;
     const int ts = L / g.N;  // W_N = tw[.. * ts]; the radix passes take the table length L
+    int lns = 0;
     for (int p = 0; p < g.npass; ++p) {
         const int R = g.radix[p];
-        if (R == 8) stockham_pass<8, false>(src, dst, g.N, Ns, tw, L, lane);
-        else if (R == 4) stockham_pass<4, false>(src, dst, g.N, Ns, tw, L, lane);
-        else if (R == 2) stockham_pass<2, false>(src, dst, g.N, Ns, tw, L, lane);
-        else generic_pass(src, dst, g.N, Ns, R, tw, L, lane);
+        if (R == 8 || R == 4 || R == 2) {
+            const int tstep = L >> (lns + (R == 8 ? 3 : (R == 4 ? 2 : 1)));  // L / (Ns R)
+            if (R == 8) stockham_pass<8, false>(src, dst, g.N, lns, tw, tstep, lane);
+            else if (R == 4) stockham_pass<4, false>(src, dst, g.N, lns, tw, tstep, lane);
+            else stockham_pass<2, false>(src, dst, g.N, lns, tw, tstep, lane);
+            lns += (R == 8 ? 3 : (R == 4 ? 2 : 1));
+        } else {
+            generic_pass(src, dst, g.N, Ns, R, tw, L, lane);
+        }
         Ns *= R;
         double2* t = src;
         src = dst;
