@@ -826,15 +826,25 @@ __device__ __forceinline__ void perturb_spectrum(const DevStage& st, WStream& s,
         normals(s, w.lane, bins, w.zig, [&](int k, double z) { amp[k] = 0.0 + sa * z; });
         normals(s, w.lane, bins, w.zig, [&](int k, double z) { ph[k] = 0.0 + sp * z; });
         __syncwarp();
+        // r' = max(|X| + amp, 0) at angle atan2(im, re) + ph (freqaugment.py:
+        // 117-122), evaluated as a rotation of X by ph scaled by r'/|X|: the
+        // same quantity without atan2 and full-range sin/cos (differs from
+        // the reference's formula in rounding only; spectral results are
+        // compared to tolerance).  |X| == 0 keeps the reference's form.
         for (int b = 1 + w.lane; b < hi; b += 32) {
-            double2 v = X[b];
-            double r = hypot(v.x, v.y);
-            double th = atan2(v.y, v.x) + ph[b];
-            r = r + amp[b];
-            if (!(r >= 0.0)) r = (r != r) ? r : 0.0;
+            const double2 v = X[b];
+            const double r = hypot(v.x, v.y);
+            double rn = r + amp[b];
+            rn = (rn >= 0.0) ? rn : ((rn != rn) ? rn : 0.0);
             double sn, cs;
-            sincos(th, &sn, &cs);
-            X[b] = make_double2(r * cs, r * sn);
+            if (r > 0.0) {
+                sincos(ph[b], &sn, &cs);
+                const double f = rn / r;
+                X[b] = make_double2(f * (v.x * cs - v.y * sn), f * (v.x * sn + v.y * cs));
+            } else {
+                sincos(atan2(v.y, v.x) + ph[b], &sn, &cs);
+                X[b] = make_double2(rn * cs, rn * sn);
+            }
         }
         __syncwarp();
         if (w.lane == 0) {
