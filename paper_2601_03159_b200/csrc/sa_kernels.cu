@@ -163,6 +163,7 @@ __global__ void __launch_bounds__(512) chain_kernel(const __grid_constant__ Chai
         }
         }
         // 3. the chain (stage-major across the CTA when sync_every > 0)
+        bool bad = false;  // per-lane: some stage output was non-finite
         double* cur = A;
         double* oth = B;
         int L = p.len_in;
@@ -184,36 +185,35 @@ __global__ void __launch_bounds__(512) chain_kernel(const __grid_constant__ Chai
             bool arith = false;
             switch (st.op) {
                 case SA_OP_JITTER:
-                case SA_OP_NOISE_GAUSSIAN: arith = op_gauss(st, s, cur, oth, L, w); break;
-                case SA_OP_SCALE: arith = op_scale(st, s, cur, oth, L, w); break;
+                case SA_OP_NOISE_GAUSSIAN: arith = op_gauss(st, s, cur, oth, L, w, bad); break;
+                case SA_OP_SCALE: arith = op_scale(st, s, cur, oth, L, w, bad); break;
                 case SA_OP_ROTATE: arith = op_rotate(cur, L, w); break;
                 case SA_OP_PERMUTE: arith = op_permute(st, s, cur, oth, L, w); break;
                 case SA_OP_CROP: arith = op_crop(st, s, cur, oth, L, w); break;
                 case SA_OP_REVERSE: arith = op_reverse(cur, oth, L, w); break;
-                case SA_OP_RESIZE: arith = op_resize(st, cur, oth, L, w); break;
-                case SA_OP_QUANTIZE: arith = op_quantize(st, cur, L, w); break;
-                case SA_OP_DRIFT: arith = op_drift(st, s, cur, oth, L, w); break;
-                case SA_OP_NOISE_UNIFORM: arith = op_uniform(st, s, cur, L, w); break;
-                case SA_OP_NOISE_SPIKE: arith = op_spike(st, s, cur, oth, L, w); break;
-                case SA_OP_NOISE_SLOPE: arith = op_slope(st, s, cur, L, w); break;
+                case SA_OP_RESIZE: arith = op_resize(st, cur, oth, L, w, bad); break;
+                case SA_OP_QUANTIZE: arith = op_quantize(st, cur, L, w, bad); break;
+                case SA_OP_DRIFT: arith = op_drift(st, s, cur, oth, L, w, bad); break;
+                case SA_OP_NOISE_UNIFORM: arith = op_uniform(st, s, cur, L, w, bad); break;
+                case SA_OP_NOISE_SPIKE: arith = op_spike(st, s, cur, oth, L, w, bad); break;
+                case SA_OP_NOISE_SLOPE: arith = op_slope(st, s, cur, L, w, bad); break;
                 case SA_OP_APP:
                 case SA_OP_FREQ_MASK:
                 case SA_OP_SINUSOID: arith = op_spectral(st, s, cur, oth, L, w); break;
-                case SA_OP_TIME_WARP: arith = op_time_warp(st, s, cur, oth, L, w, flags); break;
-                case SA_OP_WINDOW_WARP: arith = op_window_warp(st, s, cur, oth, L, w, flags); break;
+                case SA_OP_TIME_WARP: arith = op_time_warp(st, s, cur, oth, L, w, flags, bad); break;
+                case SA_OP_WINDOW_WARP: arith = op_window_warp(st, s, cur, oth, L, w, flags, bad); break;
                 case SA_OP_DROPOUT: arith = op_dropout(st, s, cur, L, w); break;
-                case SA_OP_POOL: arith = op_pool(st, cur, L, w); break;
-                case SA_OP_CONVOLVE: arith = op_convolve(st, p.aux, cur, oth, L, w); break;
-                case SA_OP_SPEED_WARP: arith = op_speed_warp(st, s, cur, oth, L, w); break;
+                case SA_OP_POOL: arith = op_pool(st, cur, L, w, bad); break;
+                case SA_OP_CONVOLVE: arith = op_convolve(st, p.aux, cur, oth, L, w, bad); break;
+                case SA_OP_SPEED_WARP: arith = op_speed_warp(st, s, cur, oth, L, w, bad); break;
                 default: break;
             }
-            if (arith) {
-                bool bad = false;
+            if (arith) {  // ops that do not fold the check into their writes
 #pragma unroll 4
                 for (int t = lane; t < L; t += 32) bad |= nonfinite(cur[t]);
-                if (__any_sync(SA_FULL, bad)) flags |= SA_FLAG_NONFINITE;
             }
         }
+        if (__any_sync(SA_FULL, bad)) flags |= SA_FLAG_NONFINITE;
         // 5. write the row
         if (!active) continue;
         double* dst = p.out + row * (int64_t)p.len_out;

@@ -314,21 +314,29 @@ __device__ __forceinline__ void swapbuf(double*& a, double*& b) {
 
 // basic.py:41-44 Jitter, basic.py:356-359 InjectNoise(gaussian):
 // y = x + (0.0 + sigma * z)
-__device__ __forceinline__ bool op_gauss(const DevStage& st, WStream& s, double*& cur, double*& oth, int& L, Warp& w) {
+__device__ __forceinline__ bool op_gauss(const DevStage& st, WStream& s, double*& cur, double*& oth, int& L, Warp& w, bool& bad) {
     const double sigma = st.f[0];
     if (sigma == 0.0) return false;
     double* x = cur;
-    normals(s, w.lane, L, w.zig, [&](int k, double z) { x[k] = x[k] + (0.0 + sigma * z); });
+    normals(s, w.lane, L, w.zig, [&](int k, double z) {
+        const double v = x[k] + (0.0 + sigma * z);
+        x[k] = v;
+        bad |= nonfinite(v);
+    });
     __syncwarp();
-    return true;
+    return false;
 }
 
 // basic.py:58-60 Scale: s = 1.0 + sigma_factor * z; y = x * s
-__device__ __forceinline__ bool op_scale(const DevStage& st, WStream& s, double*& cur, double*& oth, int& L, Warp& w) {
+__device__ __forceinline__ bool op_scale(const DevStage& st, WStream& s, double*& cur, double*& oth, int& L, Warp& w, bool& bad) {
     double f = 1.0 + st.f[0] * std_normal(s, w.lane);
-    for (int t = w.lane; t < L; t += 32) cur[t] = cur[t] * f;
+    for (int t = w.lane; t < L; t += 32) {
+        const double v = cur[t] * f;
+        cur[t] = v;
+        bad |= nonfinite(v);
+    }
     __syncwarp();
-    return true;
+    return false;
 }
 
 // basic.py:70-71 Rotate: -x
@@ -388,24 +396,32 @@ __device__ __forceinline__ bool op_reverse(double*& cur, double*& oth, int L, Wa
 }
 
 // basic.py:174-177 Resize: interp(linspace(0, L-1, T), arange(L), x)
-__device__ __forceinline__ bool op_resize(const DevStage& st, double*& cur, double*& oth, int& L, Warp& w) {
+__device__ __forceinline__ bool op_resize(const DevStage& st, double*& cur, double*& oth, int& L, Warp& w, bool& bad) {
     const int T = (int)st.i[0];
     if (T == L) return false;
     const Linspace ls(0.0, (double)L - 1.0, T);
     if (ls.fast()) {
 #pragma unroll 4
-        for (int t = w.lane; t < T; t += 32) oth[t] = interp_grid_fast(ls.at_fast(t), cur, L);
+        for (int t = w.lane; t < T; t += 32) {
+            const double v = interp_grid_fast(ls.at_fast(t), cur, L);
+            oth[t] = v;
+            bad |= nonfinite(v);
+        }
     } else {
-        for (int t = w.lane; t < T; t += 32) oth[t] = interp_grid(ls.at(t), cur, L);
+        for (int t = w.lane; t < T; t += 32) {
+            const double v = interp_grid(ls.at(t), cur, L);
+            oth[t] = v;
+            bad |= nonfinite(v);
+        }
     }
     __syncwarp();
     swapbuf(cur, oth);
     L = T;
-    return true;
+    return false;
 }
 
 // basic.py:196-207 Quantize / snap_to_levels
-__device__ __forceinline__ bool op_quantize(const DevStage& st, double*& cur, int L, Warp& w) {
+__device__ __forceinline__ bool op_quantize(const DevStage& st, double*& cur, int L, Warp& w, bool& bad) {
     double lo = cur[0], hi = cur[0];
     for (int t = w.lane; t < L; t += 32) {
         double v = cur[t];
@@ -421,16 +437,18 @@ __device__ __forceinline__ bool op_quantize(const DevStage& st, double*& cur, in
         double idx = ceil((cur[t] - lo) / step - 0.5);
         idx = (idx < 0.0) ? 0.0 : idx;  // np.clip keeps -0.0 (x < 0 is false)
         idx = (idx > top) ? top : idx;
-        cur[t] = lo + idx * step;
+        const double v = lo + idx * step;
+        cur[t] = v;
+        bad |= nonfinite(v);
     }
     __syncwarp();
-    return true;
+    return false;
 }
 
 // basic.py:227-241 Drift: anchors ~ N(0,1)^n at linspace(0, L-1, n),
 // curve = interp(arange(L), positions, anchors) - curve[0], scaled so its peak
 // magnitude is max_drift.
-__device__ __forceinline__ bool op_drift(const DevStage& st, WStream& s, double*& cur, double*& oth, int L, Warp& w) {
+__device__ __forceinline__ bool op_drift(const DevStage& st, WStream& s, double*& cur, double*& oth, int L, Warp& w, bool& bad) {
     const double md = st.f[0];
     if (md == 0.0) return false;
     const int np_ = (int)st.i[0];
@@ -460,20 +478,28 @@ __device__ __forceinline__ bool op_drift(const DevStage& st, WStream& s, double*
     peak = warp_max(peak);
     if (peak == 0.0) return false;
 #pragma unroll 4
-    for (int t = w.lane; t < L; t += 32) cur[t] = cur[t] + (curve[t] / peak) * md;
+    for (int t = w.lane; t < L; t += 32) {
+        const double v = cur[t] + (curve[t] / peak) * md;
+        cur[t] = v;
+        bad |= nonfinite(v);
+    }
     __syncwarp();
-    return true;
+    return false;
 }
 
 // basic.py:352-355 InjectNoise(uniform): x + uniform(-hw, hw)
-__device__ __forceinline__ bool op_uniform(const DevStage& st, WStream& s, double*& cur, int L, Warp& w) {
+__device__ __forceinline__ bool op_uniform(const DevStage& st, WStream& s, double*& cur, int L, Warp& w, bool& bad) {
     const double hw = st.f[0];
     if (hw == 0.0) return false;
     const double lo = -hw, range = hw - lo;
     double* x = cur;
-    doubles(s, w.lane, L, [&](int k, double u) { x[k] = x[k] + (lo + range * u); });
+    doubles(s, w.lane, L, [&](int k, double u) {
+        const double v = x[k] + (lo + range * u);
+        x[k] = v;
+        bad |= nonfinite(v);
+    });
     __syncwarp();
-    return true;
+    return false;
 }
 
 // Generator.choice(L, k, replace=False) into idx[0..k) (int32 scratch).
@@ -533,7 +559,7 @@ __device__ __noinline__ void choice_noreplace(WStream& s, int lane, int pop, int
 }
 
 // basic.py:360-370 InjectNoise(spike)
-__device__ __forceinline__ bool op_spike(const DevStage& st, WStream& s, double*& cur, double*& oth, int L, Warp& w) {
+__device__ __forceinline__ bool op_spike(const DevStage& st, WStream& s, double*& cur, double*& oth, int L, Warp& w, bool& bad) {
     const int cnt = (int)st.i[0];
     const double mag = st.f[0];
     if (cnt == 0 || mag == 0.0) return false;
@@ -557,15 +583,17 @@ __device__ __forceinline__ bool op_spike(const DevStage& st, WStream& s, double*
         double sign = (double)((int64_t)bounded(s, w.lane, 1u) * 2 - 1);
         if (w.lane == 0) {
             int p = idx[q];
-            cur[p] = cur[p] + (sign * mag) * scale;
+            const double v = cur[p] + (sign * mag) * scale;
+            cur[p] = v;
+            bad |= nonfinite(v);
         }
     }
     __syncwarp();
-    return true;
+    return false;
 }
 
 // basic.py:371-375 InjectNoise(slope_trend)
-__device__ __forceinline__ bool op_slope(const DevStage& st, WStream& s, double*& cur, int L, Warp& w) {
+__device__ __forceinline__ bool op_slope(const DevStage& st, WStream& s, double*& cur, int L, Warp& w, bool& bad) {
     const double mo = st.f[0];
     if (mo == 0.0) return false;
     const double sign = next_double(s, w.lane) < 0.5 ? 1.0 : -1.0;
@@ -573,12 +601,20 @@ __device__ __forceinline__ bool op_slope(const DevStage& st, WStream& s, double*
     const Linspace ls(0.0, stop, L);
     if (ls.fast()) {
 #pragma unroll 4
-        for (int t = w.lane; t < L; t += 32) cur[t] = cur[t] + ls.at_fast(t);
+        for (int t = w.lane; t < L; t += 32) {
+            const double v = cur[t] + ls.at_fast(t);
+            cur[t] = v;
+            bad |= nonfinite(v);
+        }
     } else {
-        for (int t = w.lane; t < L; t += 32) cur[t] = cur[t] + ls.at(t);
+        for (int t = w.lane; t < L; t += 32) {
+            const double v = cur[t] + ls.at(t);
+            cur[t] = v;
+            bad |= nonfinite(v);
+        }
     }
     __syncwarp();
-    return true;
+    return false;
 }
 
 // warp.py:25-47 warp_positions: builds knots (small[0..n)) and warped
@@ -637,7 +673,7 @@ __device__ __noinline__ bool warp_knots(int len, int nk, double intensity, WStre
 
 // warp.py:73-76 TimeWarp
 __device__ __forceinline__ bool op_time_warp(const DevStage& st, WStream& s, double*& cur, double*& oth, int L, Warp& w,
-                             uint32_t& flags) {
+                             uint32_t& flags, bool& bad) {
     if (st.f[0] == 0.0) return false;
     const int nk = (int)st.i[0];
     WStream t = s;
@@ -652,16 +688,19 @@ __device__ __forceinline__ bool op_time_warp(const DevStage& st, WStream& s, dou
     const double* sl = w.small + 2 * nk;
     const double inv = (double)(nk - 1) / ((double)L - 1.0);
 #pragma unroll 4
-    for (int t = w.lane; t < L; t += 32)
-        oth[t] = interp_grid_fast(interp_slopes((double)t, knots, warped, sl, nk, (int)((double)t * inv)), cur, L);
+    for (int t = w.lane; t < L; t += 32) {
+        const double v = interp_grid_fast(interp_slopes((double)t, knots, warped, sl, nk, (int)((double)t * inv)), cur, L);
+        oth[t] = v;
+        bad |= nonfinite(v);
+    }
     __syncwarp();
     swapbuf(cur, oth);
-    return true;
+    return false;
 }
 
 // warp.py:108-118 WindowWarp
 __device__ __forceinline__ bool op_window_warp(const DevStage& st, WStream& s, double*& cur, double*& oth, int L, Warp& w,
-                               uint32_t& flags) {
+                               uint32_t& flags, bool& bad) {
     if (st.f[0] == 0.0) return false;
     const int wsz = (int)st.i[0];
     const int nk = (int)st.i[1];
@@ -681,13 +720,15 @@ __device__ __forceinline__ bool op_window_warp(const DevStage& st, WStream& s, d
 #pragma unroll 4
     for (int t = w.lane; t < L; t += 32) {
         int u = t - start;
-        oth[t] = (u >= 0 && u < wsz)
-                     ? interp_grid_fast(interp_slopes((double)u, knots, warped, sl, nk, (int)((double)u * inv)), win, wsz)
-                     : cur[t];
+        const double v = (u >= 0 && u < wsz)
+                             ? interp_grid_fast(interp_slopes((double)u, knots, warped, sl, nk, (int)((double)u * inv)), win, wsz)
+                             : cur[t];
+        oth[t] = v;
+        bad |= nonfinite(v);
     }
     __syncwarp();
     swapbuf(cur, oth);
-    return true;
+    return false;
 }
 
 // BASELINE M2 Dropout
@@ -703,7 +744,7 @@ __device__ __forceinline__ bool op_dropout(const DevStage& st, WStream& s, doubl
 }
 
 // BASELINE M3 Pool
-__device__ __forceinline__ bool op_pool(const DevStage& st, double*& cur, int L, Warp& w) {
+__device__ __forceinline__ bool op_pool(const DevStage& st, double*& cur, int L, Warp& w, bool& bad) {
     const int P = (int)st.i[0];
     if (P == 1) return false;
     const int red = (int)st.i[1];
@@ -723,13 +764,14 @@ __device__ __forceinline__ bool op_pool(const DevStage& st, double*& cur, int L,
             for (int u = b0 + 1; u < b1; ++u) v = (cur[u] < v) ? cur[u] : v;
         }
         for (int u = b0; u < b1; ++u) cur[u] = v;
+        bad |= nonfinite(v);
     }
     __syncwarp();
-    return red == 0;
+    return false;
 }
 
 // BASELINE M4 Convolve (taps in params.aux)
-__device__ __forceinline__ bool op_convolve(const DevStage& st, const double* aux, double*& cur, double*& oth, int L, Warp& w) {
+__device__ __forceinline__ bool op_convolve(const DevStage& st, const double* aux, double*& cur, double*& oth, int L, Warp& w, bool& bad) {
     const double* taps = aux + st.aux_off;
     const int S = st.aux_len, h = S / 2;
     for (int t = w.lane; t < L; t += 32) {
@@ -740,14 +782,15 @@ __device__ __forceinline__ bool op_convolve(const DevStage& st, const double* au
             acc = acc + taps[k] * cur[u];
         }
         oth[t] = acc;
+        bad |= nonfinite(acc);
     }
     __syncwarp();
     swapbuf(cur, oth);
-    return true;
+    return false;
 }
 
 // BASELINE M5 SpeedWarp
-__device__ __forceinline__ bool op_speed_warp(const DevStage& st, WStream& s, double*& cur, double*& oth, int L, Warp& w) {
+__device__ __forceinline__ bool op_speed_warp(const DevStage& st, WStream& s, double*& cur, double*& oth, int L, Warp& w, bool& bad) {
     const int K = (int)st.i[0];
     const double R = st.f[0];
     if (K == 0 || R == 1.0) return false;
@@ -774,9 +817,17 @@ __device__ __forceinline__ bool op_speed_warp(const DevStage& st, WStream& s, do
     int* sbt = reinterpret_cast<int*>(w.iscr);  // segment starts sb[m], m <= K
     for (int m = w.lane; m <= K; m += 32) sbt[m] = (int)(((int64_t)m * L + K) / segs);
     __syncwarp();
+    int sbr[16];  // segment starts in registers (K < 16); smem table otherwise
+#pragma unroll
+    for (int q = 0; q < 16; ++q) sbr[q] = q <= K ? sbt[q] : 0x7fffffff;
     auto tau_raw = [&](int t) {
         int m = 0;  // floor(t * segs / L) == #{q in 1..K : sb[q] <= t}
-        for (int q = 1; q <= K; ++q) m += (t >= sbt[q]) ? 1 : 0;
+        if (K < 16) {
+#pragma unroll
+            for (int q = 1; q < 16; ++q) m += (t >= sbr[q]) ? 1 : 0;
+        } else {
+            for (int q = 1; q <= K; ++q) m += (t >= sbt[q]) ? 1 : 0;
+        }
         return base[m] + speeds[m] * (double)(t - sbt[m]);
     };
     const double f = ((double)L - 1.0) / tau_raw(L - 1);
@@ -801,10 +852,11 @@ __device__ __forceinline__ bool op_speed_warp(const DevStage& st, WStream& s, do
         y = (tau >= (double)(L - 1)) ? cur[L - 1] : y;
         y = (tau <= 0.0) ? cur[0] : y;
         oth[t] = y;
+        bad |= nonfinite(y);
     }
     __syncwarp();
     swapbuf(cur, oth);
-    return true;
+    return false;
 }
 
 __device__ __forceinline__ bool spectral_noop(const DevStage& st) {

@@ -329,7 +329,13 @@ __device__ __forceinline__ void normals(WStream& s, int lane, int count, const Z
                 const double u = u53(s.win[s.wpos - s.wb]);
                 s.wpos += 1;
                 const double fi0 = __ldg(&g_fi[idx - 1]), fi1 = __ldg(&g_fi[idx]);
-                ok = ((fi0 - fi1) * u + fi1) < exp(-0.5 * x * x);
+                const double lhs = (fi0 - fi1) * u + fi1;
+                const double e2 = -0.5 * x * x;  // |x| < 3.66 on the wedge: e2 > -6.7
+                // float pre-test: __expf is within ~1e-6 relative of exp(e2); only
+                // near-ties fall back to the double exp the reference compares with
+                const double ef = (double)__expf((float)e2);
+                const double d = lhs - ef;
+                ok = (fabs(d) > 1e-5 * ef) ? (d < 0.0) : (lhs < exp(e2));
                 v = x;
             } else {
                 ok = zig_slow(s, lane, r0, v);  // tail: out of line, ~3e-4 of words

@@ -25,11 +25,15 @@ for name, aug in ops:
     for _ in range(2):
         _engine.launch_device(pipe.stages, x, out, flags, 1, lowered=low)
     torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    for _ in range(3):
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    ev[0].record()
+    for i in range(3):
         _engine.launch_device(pipe.stages, x, out, flags, 1, lowered=low)
-    b.record(); torch.cuda.synchronize()
-    ms = a.elapsed_time(b) / 3
+        ev[i + 1].record()
+    torch.cuda.synchronize()
+    per = [ev[i].elapsed_time(ev[i + 1]) for i in range(3)]
+    ms = sum(per) / 3
+    if max(per) > 1.5 * min(per):
+        print("   uneven launches:", ["%.3f" % v for v in per], flush=True)
     gbs = 8 * n * (L + Lo) / (ms / 1e3) / 1e9
     print(f"{name:18s} {ms:8.3f} ms  {ms * 1e3 / n * 148:8.2f} us/series/SM  {gbs:7.1f} GB/s", flush=True)
