@@ -670,8 +670,10 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
                 cand.push_back({-op_cost(stages[j].op), j});
         std::stable_sort(cand.begin(), cand.end());
         int kb = (int)std::min<size_t>(16, cand.size());
-        // enough rows per bucket for the key to matter
-        while (kb > 0 && (p.rows_out >> kb) < 8 * (int64_t)warps) --kb;
+        // sorted keys put similar fire patterns next to each other even when
+        // buckets are sparse; only keep the histogram proportionate
+        while (kb > 0 && ((int64_t)1 << kb) > 4 * p.rows_out) --kb;
+        if (p.rows_out < 4 * (int64_t)warps) kb = 0;
         if (env_int("SA_SCHEDULE", 1) == 0 || p.rows_out > INT32_MAX) kb = 0;
         p.key_bits = kb;
         for (int q = 0; q < kb; ++q) p.key_stage[q] = (int8_t)cand[q].second;
@@ -696,7 +698,7 @@ int launch_chain(Plan* plan, cudaStream_t stream) {
     uint32_t* hist = nullptr;
     int32_t* order = nullptr;
     p.order = nullptr;
-    while (p.key_bits > 0 && (p.rows_out >> p.key_bits) < 8 * (int64_t)plan->warps) --p.key_bits;
+    while (p.key_bits > 0 && ((int64_t)1 << p.key_bits) > 4 * p.rows_out) --p.key_bits;
     if (p.key_bits > 0) {
         const int nb = 1 << p.key_bits;
         SA_CUDA(cudaMallocAsync(&keys, sizeof(uint32_t) * (size_t)p.rows_out, stream));
