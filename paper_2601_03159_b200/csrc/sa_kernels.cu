@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(512) chain_kernel(const __grid_constant__ Chai
         double* oth = B;
         int L = p.len_in;
         for (int j = 0; j < p.ns; ++j) {
-            if (p.sync_every && (j % p.sync_every) == 0) __syncthreads();
+            if ((p.sync_mask >> j) & 1ull) __syncthreads();
             if (!active || !((fire_lo >> j) & 1ull)) continue;
             const DevStage& st = p.st[j];
             const uint64_t* c = scache + 6 * j;
@@ -417,9 +417,10 @@ struct DeviceState {
     size_t smem_optin = 0;
     std::map<int, double2*> twiddles;  // by length
     // host-path workspaces (two streams)
-    cudaStream_t hs[2] = {nullptr, nullptr};
-    double* din[2] = {nullptr, nullptr};
-    double* dout[2] = {nullptr, nullptr};
+    static constexpr int NS = 3;  // host-path pipeline depth (H2D / kernel / D2H in flight)
+    cudaStream_t hs[NS] = {nullptr, nullptr, nullptr};
+    double* din[NS] = {nullptr, nullptr, nullptr};
+    double* dout[NS] = {nullptr, nullptr, nullptr};
     uint32_t* dflags = nullptr;
     size_t in_cap = 0, out_cap = 0;
 };
@@ -662,6 +663,27 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
     plan->warps = warps;
     plan->smem = (size_t)per_warp * warps + 256 * sizeof(ZigEntry);
     p.sync_every = ns > 1 ? env_int("SA_SYNC_EVERY", 4) : 0;
+    // barrier placement (bit j: barrier before stage j).  Policy 0: every
+    // `sync_every` stages; policy 1: before every stage whose operator is
+    // expensive (op_cost >= threshold) and every `sync_every` cheap stages.
+    p.sync_mask = 0;
+    if (p.sync_every) {
+        const int policy = env_int("SA_SYNC_POLICY", 0);
+        const double thr = env_int("SA_SYNC_COST_X10", 20) / 10.0;
+        int since = 0;
+        for (int j = 0; j < ns; ++j) {
+            bool b;
+            if (policy == 1) {
+                const bool heavy = op_cost(stages[j].op) >= thr;
+                b = heavy || since >= p.sync_every;
+                since = heavy ? 0 : since + 1;
+                if (b && !heavy) since = 0;
+            } else {
+                b = (j % p.sync_every) == 0;
+            }
+            if (b) p.sync_mask |= 1ull << j;
+        }
+    }
     // scheduling key: gated (0 < p < 1) stages, most expensive first
     {
         std::vector<std::pair<double, int>> cand;
@@ -830,54 +852,61 @@ int sa_pipeline_run_host(const sa_stage* stages, int32_t n_stages, const double*
     const int64_t r = plan.p.repeat_r;
     std::lock_guard<std::mutex> lk(g_mu);
     DeviceState& ds = g_dev[dev];
-    // chunk of ~64 MB of input rows, two streams
+    // Chunks of ~128 MB of rows, round-robin over NS streams: stream s runs
+    // chunks s, s + NS, ... (H2D -> fused kernel -> D2H), so the two copy
+    // engines and the SMs work on different chunks at the same time.
+    constexpr int NS = DeviceState::NS;
     const int64_t row_in_b = 8 * len_in, row_out_b = 8 * len_out * r;
-    int64_t chunk = std::max<int64_t>(1, (64ll << 20) / std::max<int64_t>(row_in_b, row_out_b));
-    chunk = std::min<int64_t>(chunk, std::max<int64_t>(n, 1));
+    int64_t chunk = std::max<int64_t>(1, (128ll << 20) / std::max<int64_t>(row_in_b, row_out_b));
+    chunk = std::min<int64_t>(chunk, std::max<int64_t>((n + NS - 1) / NS, 1));
     size_t need_in = (size_t)(chunk * row_in_b), need_out = (size_t)(chunk * row_out_b);
     if (!ds.hs[0]) {
-        SA_CUDA(cudaStreamCreateWithFlags(&ds.hs[0], cudaStreamNonBlocking));
-        SA_CUDA(cudaStreamCreateWithFlags(&ds.hs[1], cudaStreamNonBlocking));
-        SA_CUDA(cudaMalloc(&ds.dflags, 2 * sizeof(uint32_t)));
+        for (int k = 0; k < NS; ++k) SA_CUDA(cudaStreamCreateWithFlags(&ds.hs[k], cudaStreamNonBlocking));
+        SA_CUDA(cudaMalloc(&ds.dflags, NS * sizeof(uint32_t)));
     }
     if (need_in > ds.in_cap || need_out > ds.out_cap) {
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < NS; ++k) {
+            SA_CUDA(cudaStreamSynchronize(ds.hs[k]));
             if (ds.din[k]) cudaFree(ds.din[k]);
             if (ds.dout[k]) cudaFree(ds.dout[k]);
-            SA_CUDA(cudaMalloc(&ds.din[k], std::max(need_in, ds.in_cap)));
-            SA_CUDA(cudaMalloc(&ds.dout[k], std::max(need_out, ds.out_cap)));
+            ds.din[k] = ds.dout[k] = nullptr;
         }
         ds.in_cap = std::max(need_in, ds.in_cap);
         ds.out_cap = std::max(need_out, ds.out_cap);
+        for (int k = 0; k < NS; ++k) {
+            SA_CUDA(cudaMalloc(&ds.din[k], ds.in_cap));
+            SA_CUDA(cudaMalloc(&ds.dout[k], ds.out_cap));
+        }
     }
-    uint32_t hflags[2] = {0, 0};
-    SA_CUDA(cudaMemsetAsync(ds.dflags, 0, 2 * sizeof(uint32_t), ds.hs[0]));
-    SA_CUDA(cudaStreamSynchronize(ds.hs[0]));
+    uint32_t hflags[NS] = {0, 0, 0};
+    SA_CUDA(cudaMemset(ds.dflags, 0, NS * sizeof(uint32_t)));
     int c = 0;
     for (int64_t r0 = 0; r0 < n; r0 += chunk, ++c) {
         const int64_t rows = std::min(chunk, n - r0);
-        cudaStream_t st = ds.hs[c & 1];
-        SA_CUDA(cudaMemcpyAsync(ds.din[c & 1], h_in + r0 * len_in, (size_t)(rows * row_in_b),
+        const int k = c % NS;
+        cudaStream_t st = ds.hs[k];
+        SA_CUDA(cudaMemcpyAsync(ds.din[k], h_in + r0 * len_in, (size_t)(rows * row_in_b),
                                 cudaMemcpyHostToDevice, st));
         Plan pl = plan;
         pl.p.offset = series_offset + r0;
         pl.p.rows_out = rows * r;
         pl.grid = (int)std::max<int64_t>(1, std::min<int64_t>(plan.grid, (pl.p.rows_out + plan.warps - 1) / plan.warps));
-        pl.p.in = ds.din[c & 1];
-        pl.p.out = ds.dout[c & 1];
-        pl.p.flags = ds.dflags + (c & 1);
+        pl.p.in = ds.din[k];
+        pl.p.out = ds.dout[k];
+        pl.p.flags = ds.dflags + k;
         pl.p.bulk_in = ((len_in & 1) == 0) ? 1 : 0;
         {
             int rc2 = launch_chain(&pl, st);
             if (rc2) return rc2;
         }
-        SA_CUDA(cudaMemcpyAsync(h_out + r0 * r * len_out, ds.dout[c & 1], (size_t)(rows * row_out_b),
+        SA_CUDA(cudaMemcpyAsync(h_out + r0 * r * len_out, ds.dout[k], (size_t)(rows * row_out_b),
                                 cudaMemcpyDeviceToHost, st));
     }
-    SA_CUDA(cudaMemcpyAsync(hflags, ds.dflags, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, ds.hs[c & 1]));
-    SA_CUDA(cudaStreamSynchronize(ds.hs[0]));
-    SA_CUDA(cudaStreamSynchronize(ds.hs[1]));
-    return flags_status(hflags[0] | hflags[1]);
+    for (int k = 0; k < NS; ++k) SA_CUDA(cudaStreamSynchronize(ds.hs[k]));
+    SA_CUDA(cudaMemcpy(hflags, ds.dflags, NS * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    uint32_t f = 0;
+    for (int k = 0; k < NS; ++k) f |= hflags[k];
+    return flags_status(f);
 }
 
 int sa_fft_forward(const double* d_in, int64_t n, int64_t len, double* d_re, double* d_im, void* stream) {

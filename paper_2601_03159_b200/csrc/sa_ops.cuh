@@ -33,7 +33,8 @@ struct ChainParams {
     int32_t ns, repeat_r;
     int32_t len_in, len_out;
     int32_t lcap, small_words, iscr_words, bulk_in;
-    int32_t sync_every, key_bits;  // CTA barrier cadence; fire-pattern key width
+    int32_t sync_every, key_bits;  // sync_every != 0: barriers on; fire-pattern key width
+    uint64_t sync_mask;            // bit j: CTA barrier before stage j
     const int32_t* order;          // row schedule (nullptr: identity)
     int8_t key_stage[16];          // stages whose gates form the key, most expensive first
     uint64_t seed;

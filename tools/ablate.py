@@ -24,7 +24,10 @@ base = t(full)
 print(f"full config5: {base:.3f} ms for {n} series")
 rows = []
 for j, s in enumerate(full.stages):
-    p = Pipeline(stages=full.stages[:j] + full.stages[j + 1:], master_seed=full.master_seed)
+    import dataclasses
+    st = list(full.stages)
+    st[j] = dataclasses.replace(st[j], probability=0.0)  # same indices / streams / barrier grouping
+    p = Pipeline(stages=tuple(st), master_seed=full.master_seed)
     d = base - t(p)
     rows.append((d, j, s.kind, repr(s)[:60]))
 for d, j, k, r in sorted(rows, reverse=True):
