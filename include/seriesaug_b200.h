@@ -153,6 +153,12 @@ int sa_fft_forward(const double* d_in, int64_t n, int64_t len,
 int sa_fft_inverse(const double* d_re, const double* d_im, int64_t n, int64_t len,
                    double* d_out, void* stream);
 
+/* Orthonormal DCT-II / DCT-III along each row (reference freqtransform.py:
+ * 91-98: scipy.fft.dct / idct, type 2, norm="ortho"), any length.
+ * Asynchronous on `stream`; d_in / d_out are (n, len) float64. */
+int sa_dct_forward(const double* d_in, int64_t n, int64_t len, double* d_out, void* stream);
+int sa_dct_inverse(const double* d_in, int64_t n, int64_t len, double* d_out, void* stream);
+
 /* SpectralAugmenter.augment_spectrum (reference freqaugment.py:49-76): one
  * spectral stage applied directly to a half spectrum. Synchronous. */
 int sa_augment_spectrum(const sa_stage* stage, uint64_t master_seed, int64_t series_offset,

@@ -33,6 +33,7 @@ def lib():
         L.sao_augment_spectrum.argtypes = [vp, u64, i64, vp, vp, i64, i64, vp, vp]
         L.sao_fft_forward.argtypes = [vp, i64, i64, vp, vp]
         L.sao_fft_inverse.argtypes = [vp, vp, i64, i64, vp]
+        L.sao_dct.argtypes = [vp, i64, i64, vp, i32]
         L.sao_derive_key.argtypes = [u64, u64, u64, vp]
         L.sao_raw.argtypes = [u64, u64, u64, i64, vp]
         L.sao_normals.argtypes = [u64, u64, u64, i64, ctypes.c_double, ctypes.c_double, vp]
@@ -161,3 +162,10 @@ def pairwise_sum(a):
 def std(a):
     a = np.ascontiguousarray(a, dtype=np.float64)
     return lib().sao_std(_p(a), a.size)
+
+
+def dct(values: np.ndarray, inverse: bool = False) -> np.ndarray:
+    values = np.ascontiguousarray(values, dtype=np.float64)
+    out = np.empty_like(values)
+    lib().sao_dct(_p(values), values.shape[0], values.shape[1], _p(out), int(inverse))
+    return out

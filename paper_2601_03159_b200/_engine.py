@@ -139,3 +139,17 @@ def augment_spectrum_host(stage, seed: int, re: np.ndarray, im: np.ndarray, L: i
         ore.data_ptr(), oim.data_ptr(), st,
     ))
     return ore.cpu().numpy(), oim.cpu().numpy()
+
+
+def dct_host(values: np.ndarray, inverse: bool) -> np.ndarray:
+    """Orthonormal DCT-II (inverse: DCT-III) of each row on the device."""
+    import torch
+
+    dev = _native.current_device()
+    x = torch.from_numpy(np.ascontiguousarray(values, dtype=np.float64)).to(f"cuda:{dev}")
+    n, L = x.shape
+    out = torch.empty_like(x)
+    st = torch.cuda.current_stream().cuda_stream
+    fn = _native.lib().sa_dct_inverse if inverse else _native.lib().sa_dct_forward
+    _native.check(fn(x.data_ptr(), n, L, out.data_ptr(), st))
+    return out.cpu().numpy()

@@ -296,6 +296,8 @@ __global__ void __launch_bounds__(256) key_scatter_kernel(int64_t rows, const ui
 // ------------------------------------------------------------ spectral kernels
 struct FftParams {
     FftGeo fft;
+    const double2* dtw;  // DCT twiddles exp(-i pi k / 2N)
+    int32_t inverse, pad;
     const double* x;
     const double* re;
     const double* im;
@@ -336,6 +338,23 @@ __global__ void __launch_bounds__(32) irfft_kernel(const __grid_constant__ FftPa
         for (int k = lane; k < bins; k += 32) X[k] = make_double2(p.re[row * bins + k], p.im[row * bins + k]);
         __syncwarp();
         double* y = irfft_any(X, O, p.L, p.fft, p.tw, lane);
+        for (int t = lane; t < p.L; t += 32) p.xo[row * p.L + t] = y[t];
+        __syncwarp();
+    }
+}
+
+// dct_forward / dct_inverse (reference freqtransform.py:91-98), one warp per row
+__global__ void __launch_bounds__(32) dct_kernel(const __grid_constant__ FftParams p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x;
+    double* A = reinterpret_cast<double*>(smem);
+    double* B = A + p.lcap;
+    for (int64_t row = blockIdx.x; row < p.n; row += gridDim.x) {
+        const double* src = p.x + row * p.L;
+        for (int t = lane; t < p.L; t += 32) A[t] = src[t];
+        __syncwarp();
+        double* y = p.inverse ? dct3_any(A, B, p.L, p.fft, p.tw, p.dtw, lane)
+                              : dct2_any(A, B, p.L, p.fft, p.tw, p.dtw, lane);
         for (int t = lane; t < p.L; t += 32) p.xo[row * p.L + t] = y[t];
         __syncwarp();
     }
@@ -464,6 +483,7 @@ int init_device(int dev) {
     SA_CUDA(cudaFuncSetAttribute(rfft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(irfft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(spectrum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(dct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaSetDevice(prev));
     ds.ready = true;
     return SA_OK;
@@ -536,6 +556,42 @@ bool make_fft_geo(int64_t L, FftGeo* g) {
     }
     g->npass = np;
     return true;
+}
+
+// Plan of a plain N-point complex transform (DCT path).
+bool make_fft_geo_complex(int64_t N, FftGeo* g) {
+    if (N < 1) return false;
+    // reuse the factorisation with an odd-length "real" geometry: N stays N
+    if (!make_fft_geo(N % 2 ? N : 2 * N, g)) return false;
+    if (N % 2 == 0) {  // make_fft_geo(2N) planned an N-point transform, packed
+        g->packed = 0;
+    }
+    g->N = (int32_t)N;
+    return true;
+}
+
+std::map<std::pair<int, int>, double2*> g_dct_tw;  // (device, N) -> exp(-i pi k / 2N)
+
+int get_dct_twiddles(int dev, int N, const double2** out) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto key = std::make_pair(dev, N);
+    auto it = g_dct_tw.find(key);
+    if (it != g_dct_tw.end()) {
+        *out = it->second;
+        return SA_OK;
+    }
+    std::vector<double2> h((size_t)N);
+    const long double pi = 3.141592653589793238462643383279502884L;
+    for (int k = 0; k < N; ++k) {
+        long double a = -pi * (long double)k / (2.0L * (long double)N);
+        h[(size_t)k] = make_double2((double)cosl(a), (double)sinl(a));
+    }
+    double2* d = nullptr;
+    SA_CUDA(cudaMalloc(&d, sizeof(double2) * (size_t)N));
+    SA_CUDA(cudaMemcpy(d, h.data(), sizeof(double2) * (size_t)N, cudaMemcpyHostToDevice));
+    g_dct_tw[key] = d;
+    *out = d;
+    return SA_OK;
 }
 
 // doubles per buffer a spectral stage needs at length L
@@ -949,6 +1005,37 @@ int sa_fft_inverse(const double* d_re, const double* d_im, int64_t n, int64_t le
     SA_CUDA(cudaGetLastError());
     __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
     return SA_OK;
+}
+
+static int dct_launch(const double* d_in, int64_t n, int64_t len, double* d_out, void* stream, int inverse) {
+    int dev;
+    int rc = ensure_device(&dev);
+    if (rc) return rc;
+    FftParams p{};
+    if (len < 1 || !make_fft_geo_complex(len, &p.fft)) return fail(SA_ERR_UNSUPPORTED, "no DCT plan for this length");
+    p.x = d_in; p.xo = d_out; p.n = n; p.L = (int32_t)len; p.inverse = inverse;
+    rc = get_twiddles(dev, (int)len, &p.tw);
+    if (rc) return rc;
+    rc = get_dct_twiddles(dev, (int)len, &p.dtw);
+    if (rc) return rc;
+    size_t smem;
+    int lcap, grid;
+    rc = fft_plan_smem(dev, 2 * len, &lcap, &smem, &grid, (const void*)dct_kernel, n);  // 2N + 2 doubles
+    if (rc) return rc;
+    p.lcap = lcap;
+    if (n == 0) return SA_OK;
+    dct_kernel<<<grid, 32, smem, (cudaStream_t)stream>>>(p);
+    SA_CUDA(cudaGetLastError());
+    __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
+    return SA_OK;
+}
+
+int sa_dct_forward(const double* d_in, int64_t n, int64_t len, double* d_out, void* stream) {
+    return dct_launch(d_in, n, len, d_out, stream, 0);
+}
+
+int sa_dct_inverse(const double* d_in, int64_t n, int64_t len, double* d_out, void* stream) {
+    return dct_launch(d_in, n, len, d_out, stream, 1);
 }
 
 int sa_augment_spectrum(const sa_stage* stage, uint64_t master_seed, int64_t series_offset, const double* d_re,

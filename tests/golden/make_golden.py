@@ -170,6 +170,13 @@ def main() -> None:
         arrays["ifft_" + key] = ref.fft_inverse(sb).values
         cases.append({"name": "fft_" + key, "kind": "fft", "input": I[key],
                       "re": "fftre_" + key, "im": "fftim_" + key, "inverse": "ifft_" + key})
+    # --- DCT (next-1: freqtransform.py:91-98)
+    for key in ("w1", "w2", "w7", "w15", "w64", "w100", "w1024"):
+        db = ref.dct_forward(ref.Batch(arrays[I[key]]))
+        arrays["dct_" + key] = db.coeffs
+        arrays["idct_" + key] = ref.dct_inverse(db).values
+        cases.append({"name": "dct_" + key, "kind": "dct", "input": I[key], "coeffs": "dct_" + key,
+                      "inverse": "idct_" + key})
     # --- augment_spectrum (F2)
     for name, rec in (("spec_app", st("amplitude_phase_perturb", sigma_amp=0.5, sigma_phase=0.2)),
                       ("spec_fmask", st("frequency_mask", 0.5, width=7))):

@@ -226,3 +226,39 @@ def test_fft_roundtrip_any_length(L):
     tol = spectral_tol(re)
     assert np.abs(sb.re - re).max() <= tol and np.abs(sb.im - im).max() <= tol
     assert np.abs(fft_inverse(sb).values - x).max() <= spectral_tol(x)
+
+
+# ------------------------------------------------------------- transforms
+def test_golden_dct_cases(golden):
+    from paper_2601_03159_b200 import DctBatch, dct_forward, dct_inverse
+
+    meta, arrays = golden
+    for case in meta["cases"]:
+        if case["kind"] != "dct":
+            continue
+        x = arrays[case["input"]]
+        db = dct_forward(Batch(x))
+        assert np.abs(db.coeffs - arrays[case["coeffs"]]).max() <= spectral_tol(x), case["name"]
+        back = dct_inverse(DctBatch(arrays[case["coeffs"]])).values
+        assert np.abs(back - arrays[case["inverse"]]).max() <= spectral_tol(x), case["name"]
+
+
+@pytest.mark.parametrize("L", [1, 2, 3, 64, 97, 1000, 1024, 2900])
+def test_transform_roundtrips_acceptance_bound(L):
+    """Acceptance criterion 1 (test_acceptance.py:81-97): round trips <= 1e-8."""
+    from paper_2601_03159_b200 import roundtrip_check
+
+    b = Batch(np.random.default_rng(L).normal(0, 1, (30, L)))
+    assert roundtrip_check(b, "dct") <= 1e-8
+    assert roundtrip_check(b, "fft") <= 1e-8
+    from paper_2601_03159_b200 import dct_forward
+
+    assert np.abs(dct_forward(b).coeffs - O.dct(b.values)).max() <= 1e-10 * max(1.0, np.abs(b.values).max() * L)
+
+
+def test_exact_small_ffts():
+    """Known answers of the reference's transform tests (test_freqtransform.py:53-61)."""
+    sb = fft_forward(Batch(np.array([[1.0, 1.0, 1.0, 1.0]])))
+    assert np.array_equal(sb.re[0], [4.0, 0.0, 0.0]) and np.array_equal(sb.im[0], [0.0, 0.0, 0.0])
+    sb = fft_forward(Batch(np.array([[1.0, -1.0, 1.0, -1.0]])))
+    assert np.array_equal(sb.re[0], [0.0, 0.0, 4.0]) and np.array_equal(sb.im[0], [0.0, 0.0, 0.0])

@@ -110,3 +110,15 @@ def test_standard_equals_per_sample_and_sharding(golden):
     parts = [O.run_pipeline(pipe, x[a:b], series_offset=a) for a, b in ((0, 1), (1, 3))]
     assert np.array_equal(np.concatenate(parts), full)
     assert np.array_equal(O.run_pipeline(pipe, x, threads=3), full)
+
+
+def test_dct_cases(golden):
+    """Orthonormal DCT-II / III vs scipy via the reference (freqtransform.py:91-98)."""
+    meta, arrays = golden
+    cases = [c for c in meta["cases"] if c["kind"] == "dct"]
+    assert len(cases) >= 7
+    for case in cases:
+        x = arrays[case["input"]]
+        assert np.abs(O.dct(x) - arrays[case["coeffs"]]).max() <= spectral_tol(x), case["name"]
+        back = O.dct(arrays[case["coeffs"]], inverse=True)
+        assert np.abs(back - arrays[case["inverse"]]).max() <= spectral_tol(x), case["name"]
