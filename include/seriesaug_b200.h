@@ -159,6 +159,19 @@ int sa_fft_inverse(const double* d_re, const double* d_im, int64_t n, int64_t le
 int sa_dct_forward(const double* d_in, int64_t n, int64_t len, double* d_out, void* stream);
 int sa_dct_inverse(const double* d_in, int64_t n, int64_t len, double* d_out, void* stream);
 
+/* ---- DTW quality scoring (reference dtw.py:40-106) ----------------------
+ * Row-wise DTW distance of n_pairs (a, b) series pairs, |a_i - b_j| local
+ * cost, steps (1,1), (1,0), (0,1); bitwise the reference's accumulated cost.
+ * Replaces the per-pair loop of mean_similarity (dtw.py:97-106). Async. */
+int sa_dtw_batch(const double* d_a, const double* d_b, int64_t n_pairs, int64_t len_a, int64_t len_b,
+                 double* d_dist, void* stream);
+/* One pair with its optimal path, ties broken like dtw.py:64-82 (diagonal,
+ * then advancing a, then advancing b).  d_acc: len_a * len_b workspace;
+ * d_path: 2 * (len_a + len_b) int32 receiving (i, j) pairs from (0, 0).
+ * Replaces dtw_distance (dtw.py:40-85). Async. */
+int sa_dtw_path(const double* d_a, int64_t len_a, const double* d_b, int64_t len_b, double* d_acc,
+                int32_t* d_path, int32_t* d_path_len, double* d_dist, void* stream);
+
 /* SpectralAugmenter.augment_spectrum (reference freqaugment.py:49-76): one
  * spectral stage applied directly to a half spectrum. Synchronous. */
 int sa_augment_spectrum(const sa_stage* stage, uint64_t master_seed, int64_t series_offset,

@@ -34,6 +34,8 @@ def lib():
         L.sao_fft_forward.argtypes = [vp, i64, i64, vp, vp]
         L.sao_fft_inverse.argtypes = [vp, vp, i64, i64, vp]
         L.sao_dct.argtypes = [vp, i64, i64, vp, i32]
+        L.sao_dtw.argtypes = [vp, i64, vp, i64, vp, vp]
+        L.sao_dtw.restype = ctypes.c_double
         L.sao_derive_key.argtypes = [u64, u64, u64, vp]
         L.sao_raw.argtypes = [u64, u64, u64, i64, vp]
         L.sao_normals.argtypes = [u64, u64, u64, i64, ctypes.c_double, ctypes.c_double, vp]
@@ -169,3 +171,14 @@ def dct(values: np.ndarray, inverse: bool = False) -> np.ndarray:
     out = np.empty_like(values)
     lib().sao_dct(_p(values), values.shape[0], values.shape[1], _p(out), int(inverse))
     return out
+
+
+def dtw(a, b):
+    """(distance, path) of dtw.py:40-85."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    path = np.empty(2 * (a.size + b.size), dtype=np.int32)
+    plen = np.zeros(1, dtype=np.int32)
+    d = lib().sao_dtw(_p(a), a.size, _p(b), b.size, _p(path), _p(plen))
+    k = int(plen[0])
+    return d, [tuple(int(v) for v in path[2 * q:2 * q + 2]) for q in range(k)]

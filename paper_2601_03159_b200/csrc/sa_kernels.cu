@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "../../include/seriesaug_b200.h"
+#include "sa_dtw.cuh"
 #include "sa_ops.cuh"
 
 namespace sa {
@@ -360,6 +361,42 @@ __global__ void __launch_bounds__(32) dct_kernel(const __grid_constant__ FftPara
     }
 }
 
+// DTW (reference dtw.py:40-106) -----------------------
+struct DtwParams {
+    const double* a;
+    const double* b;
+    double* dist;
+    double* acc;      // path mode: n x m workspace
+    int32_t* path;    // path mode: 2 * (n + m) ints
+    int32_t* path_len;
+    int64_t pairs;
+    int32_t n, m;
+};
+
+// one warp per pair: distance only
+__global__ void __launch_bounds__(32) dtw_batch_kernel(const __grid_constant__ DtwParams p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* prow = reinterpret_cast<double*>(smem);
+    for (int64_t q = blockIdx.x; q < p.pairs; q += gridDim.x) {
+        const double d = dtw_warp(p.a + q * p.n, p.n, p.b + q * p.m, p.m, prow, nullptr, threadIdx.x);
+        if (threadIdx.x == 0) p.dist[q] = d;
+        __syncwarp();
+    }
+}
+
+// one pair with the full matrix and the reference's backtracked path
+__global__ void __launch_bounds__(32) dtw_path_kernel(const __grid_constant__ DtwParams p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* prow = reinterpret_cast<double*>(smem);
+    const double d = dtw_warp(p.a, p.n, p.b, p.m, prow, p.acc, threadIdx.x);
+    __syncwarp();
+    __threadfence_block();
+    if (threadIdx.x == 0) {
+        p.dist[0] = d;
+        p.path_len[0] = dtw_backtrack(p.acc, p.n, p.m, p.path);
+    }
+}
+
 struct SpecParams {
     DevStage st;
     uint64_t seed;
@@ -484,6 +521,8 @@ int init_device(int dev) {
     SA_CUDA(cudaFuncSetAttribute(irfft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(spectrum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(dct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(dtw_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(dtw_path_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaSetDevice(prev));
     ds.ready = true;
     return SA_OK;
@@ -1036,6 +1075,45 @@ int sa_dct_forward(const double* d_in, int64_t n, int64_t len, double* d_out, vo
 
 int sa_dct_inverse(const double* d_in, int64_t n, int64_t len, double* d_out, void* stream) {
     return dct_launch(d_in, n, len, d_out, stream, 1);
+}
+
+int sa_dtw_batch(const double* d_a, const double* d_b, int64_t n_pairs, int64_t len_a, int64_t len_b,
+                 double* d_dist, void* stream) {
+    int dev;
+    int rc = ensure_device(&dev);
+    if (rc) return rc;
+    if (len_a < 1 || len_b < 1) return fail(SA_ERR_INVALID_ARG, "DTW needs non-empty series");
+    DeviceState& ds = g_dev[dev];
+    const size_t smem = sizeof(double) * (size_t)len_b;
+    if (smem > ds.smem_optin) return fail(SA_ERR_UNSUPPORTED, "second series too long for DTW row buffer");
+    DtwParams p{};
+    p.a = d_a; p.b = d_b; p.dist = d_dist; p.pairs = n_pairs; p.n = (int32_t)len_a; p.m = (int32_t)len_b;
+    if (n_pairs == 0) return SA_OK;
+    int per_sm = 0;
+    SA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dtw_batch_kernel, 32, smem));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ds.sms * std::max(per_sm, 1), n_pairs));
+    dtw_batch_kernel<<<grid, 32, smem, (cudaStream_t)stream>>>(p);
+    SA_CUDA(cudaGetLastError());
+    __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
+    return SA_OK;
+}
+
+int sa_dtw_path(const double* d_a, int64_t len_a, const double* d_b, int64_t len_b, double* d_acc, int32_t* d_path,
+                int32_t* d_path_len, double* d_dist, void* stream) {
+    int dev;
+    int rc = ensure_device(&dev);
+    if (rc) return rc;
+    if (len_a < 1 || len_b < 1) return fail(SA_ERR_INVALID_ARG, "DTW needs non-empty series");
+    DeviceState& ds = g_dev[dev];
+    const size_t smem = sizeof(double) * (size_t)len_b;
+    if (smem > ds.smem_optin) return fail(SA_ERR_UNSUPPORTED, "second series too long for DTW row buffer");
+    DtwParams p{};
+    p.a = d_a; p.b = d_b; p.dist = d_dist; p.acc = d_acc; p.path = d_path; p.path_len = d_path_len;
+    p.pairs = 1; p.n = (int32_t)len_a; p.m = (int32_t)len_b;
+    dtw_path_kernel<<<1, 32, smem, (cudaStream_t)stream>>>(p);
+    SA_CUDA(cudaGetLastError());
+    __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
+    return SA_OK;
 }
 
 int sa_augment_spectrum(const sa_stage* stage, uint64_t master_seed, int64_t series_offset, const double* d_re,

@@ -177,6 +177,36 @@ def main() -> None:
         arrays["idct_" + key] = ref.dct_inverse(db).values
         cases.append({"name": "dct_" + key, "kind": "dct", "input": I[key], "coeffs": "dct_" + key,
                       "inverse": "idct_" + key})
+    # --- DTW (next-2: dtw.py:40-106)
+    drng = np.random.default_rng(77)
+    for q, (n1, n2) in enumerate([(1, 1), (1, 5), (6, 1), (3, 4), (17, 23), (64, 64), (100, 37), (33, 129)]):
+        a1 = np.round(drng.normal(0, 2, n1), 1) if q < 4 else drng.normal(0, 1, n1).cumsum()
+        b1 = np.round(drng.normal(0, 2, n2), 1) if q < 4 else drng.normal(0, 1, n2).cumsum()
+        r = ref.dtw_distance(a1, b1)
+        arrays[f"dtw_a{q}"], arrays[f"dtw_b{q}"] = a1, b1
+        cases.append({"name": f"dtw_{q}", "kind": "dtw", "a": f"dtw_a{q}", "b": f"dtw_b{q}",
+                      "distance": r.distance, "path": [list(p) for p in r.path], "similarity": r.similarity})
+    # criterion 10 (test_acceptance.py:334-369): scores recorded as 0.998/0.964/0.901/0.722
+    crng = ref.derive_stream(ref.SeedContext(2026))
+    n_c, len_c = 24, 128
+    tt = np.arange(len_c)
+    rows = []
+    for _ in range(n_c):
+        center = len_c / 2 + crng.normal(0.0, 1.5)
+        width = len_c / 8 * (1.0 + 0.15 * crng.normal())
+        amp = 2.0 + 0.3 * crng.normal()
+        rows.append(amp * np.exp(-0.5 * ((tt - center) / width) ** 2) + 0.05 * crng.normal(0.0, 1.0, len_c))
+    base = np.array(rows)
+    arrays["crit10_base"] = base
+    crit = {}
+    for name, rec in (("window_warp", st("time_warp_window", window_size=16, n_knots=4, intensity=0.5)),
+                      ("reverse", st("reverse")), ("drift", st("drift", max_drift=0.6, n_points=6)),
+                      ("app", st("amplitude_phase_perturb", sigma_amp=5.0, sigma_phase=2.0))):
+        aug = ref.stage_from_dict(rec)
+        out = aug.augment_batch(ref.Batch(base), 99)
+        arrays["crit10_" + name] = out.values
+        crit[name] = {"stage": rec, "score": ref.mean_similarity(ref.Batch(base), out)}
+    cases.append({"name": "criterion10", "kind": "similarity", "base": "crit10_base", "augmented": crit})
     # --- augment_spectrum (F2)
     for name, rec in (("spec_app", st("amplitude_phase_perturb", sigma_amp=0.5, sigma_phase=0.2)),
                       ("spec_fmask", st("frequency_mask", 0.5, width=7))):

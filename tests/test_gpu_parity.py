@@ -262,3 +262,44 @@ def test_exact_small_ffts():
     assert np.array_equal(sb.re[0], [4.0, 0.0, 0.0]) and np.array_equal(sb.im[0], [0.0, 0.0, 0.0])
     sb = fft_forward(Batch(np.array([[1.0, -1.0, 1.0, -1.0]])))
     assert np.array_equal(sb.re[0], [0.0, 0.0, 4.0]) and np.array_equal(sb.im[0], [0.0, 0.0, 0.0])
+
+
+# ------------------------------------------------------------- DTW
+def test_golden_dtw_cases(golden):
+    from paper_2601_03159_b200 import dtw_distance
+
+    meta, arrays = golden
+    for case in meta["cases"]:
+        if case["kind"] != "dtw":
+            continue
+        r = dtw_distance(arrays[case["a"]], arrays[case["b"]])
+        assert r.distance == case["distance"], case["name"]
+        assert [list(p) for p in r.path] == case["path"], case["name"]
+        assert r.similarity == case["similarity"]
+
+
+def test_dtw_batch_bitwise_vs_oracle():
+    from paper_2601_03159_b200 import dtw_distances
+
+    rng = np.random.default_rng(5)
+    for n1, n2 in [(1, 1), (31, 33), (64, 64), (100, 257), (1024, 1024)]:
+        a = rng.normal(0, 1, (8, n1)).cumsum(1)
+        b = rng.normal(0, 1, (8, n2)).cumsum(1)
+        d = dtw_distances(Batch(a), Batch(b))
+        want = np.array([O.dtw(a[i], b[i])[0] for i in range(8)])
+        assert np.array_equal(d, want), (n1, n2)
+
+
+def test_similarity_ordering_criterion10(golden):
+    from paper_2601_03159_b200 import mean_similarity
+
+    meta, arrays = golden
+    case = next(c for c in meta["cases"] if c["kind"] == "similarity")
+    base = Batch(arrays[case["base"]])
+    scores = {}
+    for name, info in case["augmented"].items():
+        out = stage_from_dict(info["stage"]).augment_batch(base, 99)
+        scores[name] = mean_similarity(base, out)
+        assert abs(scores[name] - info["score"]) < 1e-9, name
+    assert scores["window_warp"] > scores["reverse"] > scores["app"]
+    assert scores["window_warp"] > scores["drift"] > scores["app"]

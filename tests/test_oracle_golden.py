@@ -122,3 +122,28 @@ def test_dct_cases(golden):
         assert np.abs(O.dct(x) - arrays[case["coeffs"]]).max() <= spectral_tol(x), case["name"]
         back = O.dct(arrays[case["coeffs"]], inverse=True)
         assert np.abs(back - arrays[case["inverse"]]).max() <= spectral_tol(x), case["name"]
+
+
+def test_dtw_cases(golden):
+    """dtw.py:40-85: distance bitwise, path exactly (tie order included)."""
+    meta, arrays = golden
+    cases = [c for c in meta["cases"] if c["kind"] == "dtw"]
+    assert len(cases) >= 8
+    for case in cases:
+        d, path = O.dtw(arrays[case["a"]], arrays[case["b"]])
+        assert d == case["distance"], case["name"]
+        assert [list(p) for p in path] == case["path"], case["name"]
+
+
+def test_similarity_ordering_criterion10(golden):
+    """Acceptance criterion 10 (test_acceptance.py:334-369) through the
+    oracle: recorded scores 0.998 / 0.964 / 0.901 / 0.722 (test_output.txt:29)."""
+    meta, arrays = golden
+    case = next(c for c in meta["cases"] if c["kind"] == "similarity")
+    base = arrays[case["base"]]
+    for name, rec in case["augmented"].items():
+        pipe = Pipeline.parse({"master_seed": 99, "stages": [rec["stage"]]})
+        out = O.run_pipeline(pipe, base)
+        sims = [1.0 / (1.0 + O.dtw(base[i], out[i])[0] / base.shape[1]) for i in range(base.shape[0])]
+        score = sum(sims) / len(sims)
+        assert abs(score - case["augmented"][name]["score"]) < 1e-9, name
