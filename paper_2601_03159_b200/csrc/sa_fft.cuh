@@ -81,10 +81,19 @@ __device__ __forceinline__ void dft8(double2* v) {
 // Ns = 2^lns (the power-of-two passes run first, so Ns is a power of two).
 // tw: exp(-2 pi i q / L); W_{Ns R}^{rk} = tw[r k tstep], tstep = L / (Ns R).
 // Twiddles: W^k, W^2k, W^4k are loaded, the odd powers multiplied out.
+// Swizzled intermediate: the first pass writes dst[R j + r] (stride R across
+// lanes -> an R-way shared-memory bank conflict).  That buffer (read only by
+// the second pass) is stored at i ^ ((i >> log2 R) & (R - 1)), which spreads
+// each 8-lane phase over distinct banks for both the writes and the reads.
+struct Swz {
+    int sh, mask;  // mask == 0: identity
+    __device__ __forceinline__ int operator()(int i) const { return i ^ ((i >> sh) & mask); }
+};
+
 template <int R, bool INV>
 __device__ __forceinline__ void stockham_pass(const double2* __restrict__ src, double2* __restrict__ dst,
                                               int M, int lns, const double2* __restrict__ tw, int tstep,
-                                              int lane) {
+                                              int lane, Swz sin = {0, 0}, Swz sout = {0, 0}) {
     const int Q = M / R;
     const int Ns = 1 << lns;
 #pragma unroll 2
@@ -92,7 +101,7 @@ __device__ __forceinline__ void stockham_pass(const double2* __restrict__ src, d
         const int k = j & (Ns - 1);
         double2 v[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[r] = src[j + r * Q];
+        for (int r = 0; r < R; ++r) v[r] = src[sin(j + r * Q)];
         if (Ns > 1) {
             double2 w1 = __ldg(&tw[k * tstep]);
             if (INV) w1.y = -w1.y;
@@ -120,7 +129,7 @@ __device__ __forceinline__ void stockham_pass(const double2* __restrict__ src, d
         if (R == 8) dft8<INV>(v);
         const int base = ((j >> lns) << (lns + (R == 8 ? 3 : (R == 4 ? 2 : 1)))) + k;
 #pragma unroll
-        for (int r = 0; r < R; ++r) dst[base + r * Ns] = v[r];
+        for (int r = 0; r < R; ++r) dst[sout(base + r * Ns)] = v[r];
     }
     __syncwarp();
 }
@@ -170,14 +179,20 @@ __device__ __forceinline__ double2* fft_any(double2* a, double2* b, const FftGeo
     double2* dst = b;
     const int ts = L / g.N;  // W_N = tw[.. * ts]; the radix passes take the table length L
     int lns = 0;
+    Swz carry = {0, 0};  // swizzle of the buffer the next pass reads
     for (int p = 0; p < g.npass; ++p) {
         const int R = g.radix[p];
         if (R == 8 || R == 4 || R == 2) {
-            const int tstep = L >> (lns + (R == 8 ? 3 : (R == 4 ? 2 : 1)));  // L / (Ns R)
-            if (R == 8) stockham_pass<8, false>(src, dst, g.N, lns, tw, tstep, lane);
-            else if (R == 4) stockham_pass<4, false>(src, dst, g.N, lns, tw, tstep, lane);
-            else stockham_pass<2, false>(src, dst, g.N, lns, tw, tstep, lane);
-            lns += (R == 8 ? 3 : (R == 4 ? 2 : 1));
+            const int lr = (R == 8 ? 3 : (R == 4 ? 2 : 1));
+            const int tstep = L >> (lns + lr);  // L / (Ns R)
+            // swizzle pass 0's output when pass 1 is a power-of-two pass too
+            const bool swz = (p == 0 && R > 2 && g.npass > 1 && (g.radix[1] & (g.radix[1] - 1)) == 0);
+            const Swz out = swz ? Swz{lr, R - 1} : Swz{0, 0};
+            if (R == 8) stockham_pass<8, false>(src, dst, g.N, lns, tw, tstep, lane, carry, out);
+            else if (R == 4) stockham_pass<4, false>(src, dst, g.N, lns, tw, tstep, lane, carry, out);
+            else stockham_pass<2, false>(src, dst, g.N, lns, tw, tstep, lane, carry, out);
+            carry = out;
+            lns += lr;
         } else {
             generic_pass(src, dst, g.N, Ns, R, tw, L, lane);
         }
