@@ -317,6 +317,55 @@ def run_b200(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def run_suite(args):
+    """Device-resident kernel throughput of configs 1-5 and of the config-5
+    sweep (100 datasets) -- documentation numbers, not the driver's line."""
+    import torch
+
+    import bench_inputs
+    from paper_2601_03159_b200 import _engine, _native
+
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    _native.ensure_device(0)
+    flags = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def timed(pipe, x, reps=5):
+        out = torch.empty((x.shape[0] * pipe.row_factor(), pipe.projected_length(x.shape[1])),
+                          dtype=torch.float64, device=dev)
+        low = _engine._lower(pipe.stages, 0, True)
+        for _ in range(2):
+            _engine.launch_device(pipe.stages, x, out, flags, pipe.master_seed, lowered=low)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            _engine.launch_device(pipe.stages, x, out, flags, pipe.master_seed, lowered=low)
+        b.record()
+        torch.cuda.synchronize()
+        assert int(flags.item()) == 0
+        return a.elapsed_time(b) / reps, out.numel()
+
+    res = {}
+    for cfg in (1, 2, 3, 4, 5):
+        N, L = bench_inputs.CONFIG_SHAPES[cfg]
+        x = bench_inputs.device_walks(N, L, 5, dev) if cfg == 5 else \
+            torch.from_numpy(bench_inputs.host_input(cfg)).to(dev)
+        ms, pts = timed(bench_inputs.pipeline(cfg), x)
+        byt = 8 * (x.numel() + pts)
+        res[f"config{cfg}"] = {"ms": ms, "gpts_s": pts / ms / 1e6, "hbm_gbs": byt / ms / 1e6,
+                               "hbm_frac": byt / ms / 1e6 / measured_peak()[0]}
+        del x
+    tot_ms, tot_pts = 0.0, 0
+    for i, n, L in bench_inputs.sweep_datasets():
+        x = torch.from_numpy(bench_inputs.synthetic_walks(n, L, i)).to(dev)
+        ms, pts = timed(bench_inputs.sweep_pipeline(L, i), x, reps=3)
+        tot_ms += ms
+        tot_pts += pts
+    res["sweep100"] = {"ms": tot_ms, "gpts_s": tot_pts / tot_ms / 1e6, "datasets": 100, "points": tot_pts}
+    print(json.dumps(res), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -327,8 +376,12 @@ def main():
     ap.add_argument("--n-series", type=int, default=0, help="override the config's series count")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--suite", action="store_true", help="configs 1-5 + sweep, device-resident, one JSON")
     args = ap.parse_args()
     rank, world, local_rank = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    if args.suite:
+        run_suite(args)
+        return
     if args.impl == "reference":
         run_reference(args, rank, world)
         return

@@ -120,3 +120,36 @@ def pipeline(cfg: int):
                   RandomSinusoid(0.5, probability=p), SpeedWarp(3, 3.0, probability=p))
         seed = 5
     return Pipeline(stages=stages, master_seed=seed)
+
+
+def sweep_datasets(count: int = 100, seed: int = 2026):
+    """BASELINE config 5's sweep: `count` synthetic datasets with series
+    counts log-uniform in [20, 24000] and lengths log-uniform in [24, 2900]
+    (random walks, seed = dataset id).  Returns [(id, n, L)]."""
+    rng = np.random.default_rng(seed)
+    n = np.exp(rng.uniform(np.log(20), np.log(24_000), count)).astype(int)
+    L = np.exp(rng.uniform(np.log(24), np.log(2_900), count)).astype(int)
+    return [(i, int(a), int(b)) for i, (a, b) in enumerate(zip(n, L))]
+
+
+def sweep_pipeline(L: int, seed: int):
+    """The config-5 chain with length-scaled parameters:
+    mask width ~5% of the bins, window = min(128, L), segments <= L."""
+    from paper_2601_03159_b200 import (AmplitudePhasePerturb, Convolve, Drift, Dropout, FrequencyMask,
+                                       GaussianNoise, InjectNoise, Jitter, PermuteSegments, Pipeline, Pool,
+                                       Quantize, RandomSinusoid, Reverse, Rotate, Scale, SlopeTrendNoise,
+                                       SpeedWarp, SpikeNoise, TimeWarp, UniformNoise, WindowWarp)
+
+    p = 0.5
+    bins = L // 2 + 1
+    stages = (Jitter(0.05, probability=p), Scale(0.1, probability=p), Rotate(probability=p),
+              PermuteSegments(min(4, L), probability=p), Reverse(probability=p), Quantize(16, probability=p),
+              Drift(0.5, 5, probability=p), InjectNoise(UniformNoise(0.1), probability=p),
+              InjectNoise(GaussianNoise(0.1), probability=p),
+              InjectNoise(SpikeNoise(min(5, L), 2.0), probability=p),
+              InjectNoise(SlopeTrendNoise(0.5), probability=p), AmplitudePhasePerturb(0.1, 0.1, probability=p),
+              FrequencyMask(max(1, int(0.05 * bins)), probability=p), TimeWarp(5, 0.5, probability=p),
+              WindowWarp(min(128, L), 4, 0.5, probability=p), Dropout(0.05, probability=p),
+              Pool(4, probability=p), Convolve("hann", 7, probability=p),
+              RandomSinusoid(0.5, min_bin=min(1, L // 2), probability=p), SpeedWarp(3, 3.0, probability=p))
+    return Pipeline(stages=stages, master_seed=seed)

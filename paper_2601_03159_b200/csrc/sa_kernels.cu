@@ -790,7 +790,8 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
         // sorted keys put similar fire patterns next to each other even when
         // buckets are sparse; only keep the histogram proportionate
         while (kb > 0 && ((int64_t)1 << kb) > 4 * p.rows_out) --kb;
-        if (p.rows_out < 4 * (int64_t)warps) kb = 0;
+        // small batches: a few CTAs, three extra launches would cost more than the balance gains
+        if (p.rows_out < env_int("SA_SCHEDULE_MIN_ROWS", 4096)) kb = 0;
         if (env_int("SA_SCHEDULE", 1) == 0 || p.rows_out > INT32_MAX) kb = 0;
         p.key_bits = kb;
         for (int q = 0; q < kb; ++q) p.key_stage[q] = (int8_t)cand[q].second;

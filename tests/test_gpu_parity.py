@@ -303,3 +303,35 @@ def test_similarity_ordering_criterion10(golden):
         assert abs(scores[name] - info["score"]) < 1e-9, name
     assert scores["window_warp"] > scores["reverse"] > scores["app"]
     assert scores["window_warp"] > scores["drift"] > scores["app"]
+
+
+# ------------------------------------------------------------- BASELINE config-5 sweep
+def test_config5_sweep_vs_oracle():
+    """BASELINE config 5's sweep (N log-uniform in [20, 24000], L in [24, 2900],
+    arbitrary lengths incl. odd / prime), parity on the first 64 series of
+    every dataset.  The chain holds FFT stages, so the bound is the spectral
+    tolerance.  A row may deviate only through APP's ill-conditioning: an
+    (almost) exactly zero bin at APP's input has a rounding-determined phase
+    that APP turns into magnitude ~sigma_amp; such rows are
+    checked to have that cause."""
+    import dataclasses
+
+    import bench_inputs
+
+    total, excused = 0, 0
+    for i, n, L in bench_inputs.sweep_datasets():
+        pipe = bench_inputs.sweep_pipeline(L, seed=i)
+        x = bench_inputs.synthetic_walks(min(n, 64), L, seed=i)
+        want = O.run_pipeline(pipe, x)
+        got = gpu_run(pipe, x)
+        tol = 1e-9 * max(1.0, float(np.abs(want).max()))
+        total += x.shape[0]
+        for r in np.flatnonzero(np.abs(got - want).max(axis=1) > tol):
+            j_app = next(j for j, s in enumerate(pipe.stages) if s.kind == "amplitude_phase_perturb")
+            pre = O.run_pipeline(Pipeline(stages=pipe.stages[:j_app], master_seed=pipe.master_seed),
+                                 x[r:r + 1], series_offset=int(r))
+            re, im = O.fft_forward(pre)
+            mag = np.hypot(re, im)[0, 1:-1]
+            assert mag.min() < 1e-10 * np.median(mag), (i, n, L, int(r))
+            excused += 1
+    assert excused <= max(2, total // 1000), (excused, total)
