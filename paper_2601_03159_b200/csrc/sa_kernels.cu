@@ -84,7 +84,7 @@ __host__ __device__ inline Layout make_layout(int lcap, int ns, int small_words,
 }
 
 // ------------------------------------------------------------ the kernel
-__global__ void __launch_bounds__(512) chain_kernel(const __grid_constant__ ChainParams p) {
+__global__ void __launch_bounds__(384) chain_kernel(const __grid_constant__ ChainParams p) {
     extern __shared__ __align__(16) unsigned char smem_all[];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
@@ -753,8 +753,8 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
     const int per_warp = (int)plan->lay.total;
     int fit = (int)((ds.smem_optin - 256 * sizeof(ZigEntry)) / (size_t)per_warp);
     int warps = env_int("SA_CTA_WARPS", 0);
-    if (warps <= 0) warps = std::min(16, std::max(1, fit));
-    warps = std::max(1, std::min(warps, std::min(16, fit)));
+    if (warps <= 0) warps = std::min(12, std::max(1, fit));
+    warps = std::max(1, std::min(warps, std::min(12, fit)));
     plan->warps = warps;
     plan->smem = (size_t)per_warp * warps + 256 * sizeof(ZigEntry);
     p.sync_every = ns > 1 ? env_int("SA_SYNC_EVERY", 4) : 0;
