@@ -38,7 +38,8 @@ def _ptr(a: np.ndarray) -> int:
 
 
 def run_host(stages, values: np.ndarray, seed: int, first_index: int = 0, series_offset: int = 0,
-             len_out: int | None = None, check_finite: bool = True, repeat_rows: bool = True) -> np.ndarray:
+             len_out: int | None = None, check_finite: bool = True, repeat_rows: bool = True,
+             out: np.ndarray | None = None) -> np.ndarray:
     """Run `stages` over a host (n, L) float64 batch; returns a new array."""
     values = np.ascontiguousarray(values, dtype=np.float64)
     n, L = values.shape
@@ -46,7 +47,10 @@ def run_host(stages, values: np.ndarray, seed: int, first_index: int = 0, series
     arr, aux = _lower(stages, first_index, repeat_rows)
     rows = n * _row_factor(stages, repeat_rows)
     L_out = L if len_out is None else int(len_out)
-    out = np.empty((rows, L_out), dtype=np.float64)
+    if out is None:
+        out = np.empty((rows, L_out), dtype=np.float64)
+    elif out.shape != (rows, L_out) or out.dtype != np.float64 or not out.flags.c_contiguous:
+        raise ValueError(f"out must be a C-contiguous float64 array of shape {(rows, L_out)}")
     rc = _native.lib().sa_pipeline_run_host(
         arr, len(stages), aux.ctypes.data_as(ctypes.c_void_p), aux.size, int(seed),
         int(series_offset), _ptr(values), n, L, _ptr(out), L_out,

@@ -335,3 +335,16 @@ def test_config5_sweep_vs_oracle():
             assert mag.min() < 1e-10 * np.median(mag), (i, n, L, int(r))
             excused += 1
     assert excused <= max(2, total // 1000), (excused, total)
+
+
+def test_pinned_host_batches_roundtrip():
+    from paper_2601_03159_b200 import pinned_copy, pinned_empty
+
+    x = walks(300, 256, 12)
+    pipe = Pipeline(stages=(Jitter(0.1), TimeWarp(4, 0.5, probability=0.5)), master_seed=8)
+    want = pipe.run(Batch(x)).values
+    xp = pinned_copy(x)
+    out = pinned_empty((300, 256))
+    got = pipe.run(Batch(xp), out=out).values
+    assert got is out or np.shares_memory(got, out)
+    assert np.array_equal(got, want)
