@@ -145,28 +145,43 @@ struct FftGeo {
 };
 
 // Generic radix-R Stockham pass (any R | N): each output is the direct sum
-// V[u] = sum_r src[j + rQ] * W_N^(r*k*N/(Ns R) + (r*u mod R)*N/R).
+// V[u] = sum_r src[j + rQ] * W_N^(r*k*N/(Ns R) + (r*u mod R)*N/R).  The
+// exponents advance by steps < N, so a conditional subtraction keeps them
+// reduced (no integer division in the inner loop); two outputs of the same
+// input column are accumulated together (shared loads, two FMA chains).
 __device__ __forceinline__ void generic_pass(const double2* __restrict__ src, double2* __restrict__ dst, int N, int Ns,
                                              int R, const double2* __restrict__ tw, int L, int lane) {
     const int Q = N / R;
     const int ts = L / N;               // table stride for W_N
     const int a = N / (Ns * R), b = N / R;
-    for (int idx = lane; idx < Q * R; idx += 32) {
-        const int j = idx % Q, u = idx / Q;
+    const int half = (R + 1) / 2;       // outputs u and u + half share the column j
+    for (int idx = lane; idx < Q * half; idx += 32) {
+        const int j = idx % Q, u0 = idx / Q, u1 = u0 + half;
+        const bool two = u1 < R;
         const int k = j % Ns;
-        double2 acc = make_double2(0.0, 0.0);
-        int e1 = 0, e2 = 0;             // r*k*a mod N, (r*u mod R)*b
+        const int ka = k * a;            // < N
+        const int s0 = u0 * b, s1 = two ? u1 * b : 0;  // < N
+        double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
+        int e1 = 0, e20 = 0, e21 = 0;    // r*k*a mod N, (r*u mod R)*b
         for (int r = 0; r < R; ++r) {
-            int e = e1 + e2;
+            const double2 v = src[j + r * Q];
+            int e = e1 + e20;
             e = e >= N ? e - N : e;
-            const double2 w = __ldg(&tw[e * ts]);
-            acc = cadd(acc, cmul(src[j + r * Q], w));
-            e1 += k * a;
-            e1 %= N;
-            e2 += u * b;
-            e2 = e2 >= N ? e2 - N : e2;
+            acc0 = cadd(acc0, cmul(v, __ldg(&tw[e * ts])));
+            if (two) {
+                int f = e1 + e21;
+                f = f >= N ? f - N : f;
+                acc1 = cadd(acc1, cmul(v, __ldg(&tw[f * ts])));
+            }
+            e1 += ka;
+            e1 = e1 >= N ? e1 - N : e1;
+            e20 += s0;
+            e20 = e20 >= N ? e20 - N : e20;
+            e21 += s1;
+            e21 = e21 >= N ? e21 - N : e21;
         }
-        dst[(j - k) * R + k + u * Ns] = acc;
+        dst[(j - k) * R + k + u0 * Ns] = acc0;
+        if (two) dst[(j - k) * R + k + u1 * Ns] = acc1;
     }
     __syncwarp();
 }

@@ -517,6 +517,16 @@ int init_device(int dev) {
     SA_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     ds.smem_optin = (size_t)optin;
     SA_CUDA(cudaFuncSetAttribute(chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    // The scheduling buffers come from the stream-ordered allocator; keep the
+    // pool's memory mapped between calls (the default release threshold of 0
+    // unmaps it at every synchronisation and the next cudaMallocAsync pays a
+    // remap -- seen as 20-60 ms host stalls inside sa_pipeline_launch).
+    {
+        cudaMemPool_t pool;
+        SA_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+        uint64_t keep = UINT64_MAX;
+        SA_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    }
     SA_CUDA(cudaFuncSetAttribute(rfft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(irfft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(spectrum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
@@ -797,8 +807,20 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
         for (int q = 0; q < kb; ++q) p.key_stage[q] = (int8_t)cand[q].second;
     }
     int per_sm = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chain_kernel, 32 * warps, plan->smem);
-    if (e != cudaSuccess) return cuda_fail(e, "occupancy");
+    {
+        static std::mutex occ_mu;
+        static std::map<std::pair<int, size_t>, int> occ_cache;  // (warps, smem) -> CTAs per SM
+        std::lock_guard<std::mutex> lk(occ_mu);
+        auto key = std::make_pair(warps, plan->smem);
+        auto it = occ_cache.find(key);
+        if (it != occ_cache.end()) {
+            per_sm = it->second;
+        } else {
+            cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chain_kernel, 32 * warps, plan->smem);
+            if (e != cudaSuccess) return cuda_fail(e, "occupancy");
+            occ_cache[key] = per_sm;
+        }
+    }
     per_sm = std::max(per_sm, 1);
     int64_t ctas_needed = (p.rows_out + warps - 1) / warps;
     int64_t want = (int64_t)ds.sms * per_sm;
