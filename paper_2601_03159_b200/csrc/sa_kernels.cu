@@ -480,9 +480,16 @@ struct DeviceState {
     uint32_t* dflags = nullptr;
     size_t in_cap = 0, out_cap = 0;
 };
-std::map<int, DeviceState> g_dev;
+// Per-device state in a fixed array: lookups never reallocate, so readers
+// need no lock; initialisation and the caches inside are guarded by g_mu,
+// the host-buffer pipeline (streams + staging buffers) by its own mutex.
+constexpr int kMaxDevices = 64;
+DeviceState g_dev_state[kMaxDevices];
+std::mutex g_host_mu[kMaxDevices];
 
-int current_dev_cached() {
+DeviceState& dev_state(int dev) { return g_dev_state[dev < 0 ? 0 : (dev >= kMaxDevices ? kMaxDevices - 1 : dev)]; }
+
+int current_device_id() {
     int d = 0;
     cudaGetDevice(&d);
     return d;
@@ -495,7 +502,7 @@ int current_device(int* dev) {
 
 int init_device(int dev) {
     std::lock_guard<std::mutex> lk(g_mu);
-    DeviceState& ds = g_dev[dev];
+    DeviceState& ds = dev_state(dev);
     if (ds.ready) return SA_OK;
     int prev;
     SA_CUDA(cudaGetDevice(&prev));
@@ -551,7 +558,7 @@ int ensure_device(int* dev_out) {
 // exp(-2 pi i k / L), k < L, correctly rounded via long double.
 int get_twiddles(int dev, int L, const double2** out) {
     std::lock_guard<std::mutex> lk(g_mu);
-    DeviceState& ds = g_dev[dev];
+    DeviceState& ds = dev_state(dev);
     auto it = ds.twiddles.find(L);
     if (it != ds.twiddles.end()) {
         *out = it->second;
@@ -752,7 +759,7 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
     p.small_words = small;
     p.iscr_words = iscr;
     plan->lay = make_layout(p.lcap, ns, small, iscr);
-    DeviceState& ds = g_dev[dev];
+    DeviceState& ds = dev_state(dev);
     if (plan->lay.total + 256 * sizeof(ZigEntry) > ds.smem_optin)
         return fail(SA_ERR_UNSUPPORTED, "series too long for one warp's shared memory (" +
                                             std::to_string(plan->lay.total) + " B)");
@@ -833,7 +840,7 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
 int launch_chain(Plan* plan, cudaStream_t stream) {
     ChainParams& p = plan->p;
     if (p.rows_out == 0) return SA_OK;
-    DeviceState& ds = g_dev[current_dev_cached()];
+    DeviceState& ds = dev_state(current_device_id());
     uint32_t* keys = nullptr;
     uint32_t* hist = nullptr;
     int32_t* order = nullptr;
@@ -883,7 +890,7 @@ int flags_status(uint32_t f) {
 int fft_plan_smem(int dev, int64_t L, int* lcap, size_t* smem, int* grid, const void* kern, int64_t n) {
     *lcap = (int)((fft_lcap(L) + 1) & ~1LL);
     *smem = (size_t)(*lcap) * 8 * 2 + 8 * SA_WIN + 64;
-    DeviceState& ds = g_dev[dev];
+    DeviceState& ds = dev_state(dev);
     if (*smem > ds.smem_optin) return fail(SA_ERR_UNSUPPORTED, "series too long");
     int per_sm = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32, *smem);
@@ -907,7 +914,8 @@ int sa_init(int32_t device) {
     int count = 0;
     cudaError_t e = cudaGetDeviceCount(&count);
     if (e != cudaSuccess || count == 0) return fail(SA_ERR_NO_DEVICE, "no CUDA device available");
-    if (device < 0 || device >= count) return fail(SA_ERR_INVALID_ARG, "device index out of range");
+    if (device < 0 || device >= count || device >= kMaxDevices)
+        return fail(SA_ERR_INVALID_ARG, "device index out of range");
     SA_CUDA(cudaSetDevice(device));
     return init_device(device);
 }
@@ -968,8 +976,8 @@ int sa_pipeline_run_host(const sa_stage* stages, int32_t n_stages, const double*
     rc = make_plan(dev, stages, n_stages, aux, n_aux, master_seed, series_offset, n, len_in, len_out, &plan);
     if (rc) return rc;
     const int64_t r = plan.p.repeat_r;
-    std::lock_guard<std::mutex> lk(g_mu);
-    DeviceState& ds = g_dev[dev];
+    std::lock_guard<std::mutex> lk(g_host_mu[dev < 0 ? 0 : (dev >= kMaxDevices ? kMaxDevices - 1 : dev)]);
+    DeviceState& ds = dev_state(dev);
     // Chunks of ~128 MB of rows, round-robin over NS streams: stream s runs
     // chunks s, s + NS, ... (H2D -> fused kernel -> D2H), so the two copy
     // engines and the SMs work on different chunks at the same time.
@@ -1106,7 +1114,7 @@ int sa_dtw_batch(const double* d_a, const double* d_b, int64_t n_pairs, int64_t 
     int rc = ensure_device(&dev);
     if (rc) return rc;
     if (len_a < 1 || len_b < 1) return fail(SA_ERR_INVALID_ARG, "DTW needs non-empty series");
-    DeviceState& ds = g_dev[dev];
+    DeviceState& ds = dev_state(dev);
     const size_t smem = sizeof(double) * (size_t)len_b;
     if (smem > ds.smem_optin) return fail(SA_ERR_UNSUPPORTED, "second series too long for DTW row buffer");
     DtwParams p{};
@@ -1127,7 +1135,7 @@ int sa_dtw_path(const double* d_a, int64_t len_a, const double* d_b, int64_t len
     int rc = ensure_device(&dev);
     if (rc) return rc;
     if (len_a < 1 || len_b < 1) return fail(SA_ERR_INVALID_ARG, "DTW needs non-empty series");
-    DeviceState& ds = g_dev[dev];
+    DeviceState& ds = dev_state(dev);
     const size_t smem = sizeof(double) * (size_t)len_b;
     if (smem > ds.smem_optin) return fail(SA_ERR_UNSUPPORTED, "second series too long for DTW row buffer");
     DtwParams p{};

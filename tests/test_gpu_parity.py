@@ -348,3 +348,27 @@ def test_pinned_host_batches_roundtrip():
     got = pipe.run(Batch(xp), out=out).values
     assert got is out or np.shares_memory(got, out)
     assert np.array_equal(got, want)
+
+
+def test_concurrent_callers_match_sequential():
+    """The reference API is safe from several threads on distinct batches
+    (SPEC.md:90); the C ABI entry points are reentrant."""
+    import threading
+
+    pipe = Pipeline(stages=(Jitter(0.1, probability=0.5), FrequencyMask(4, probability=0.5),
+                            TimeWarp(4, 0.5, probability=0.5)), master_seed=21)
+    xs = [walks(500, 128 + 64 * k, k) for k in range(6)]
+    want = [pipe.run(Batch(x)).values for x in xs]
+    got = [None] * len(xs)
+
+    def work(k):
+        got[k] = pipe.run(Batch(xs[k])).values if k % 2 else \
+            pipe.run_device(torch.from_numpy(xs[k]).cuda()).cpu().numpy()
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(len(xs))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for k in range(len(xs)):
+        assert np.array_equal(got[k], want[k]), k
