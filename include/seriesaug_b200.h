@@ -172,6 +172,19 @@ int sa_dtw_batch(const double* d_a, const double* d_b, int64_t n_pairs, int64_t 
 int sa_dtw_path(const double* d_a, int64_t len_a, const double* d_b, int64_t len_b, double* d_acc,
                 int32_t* d_path, int32_t* d_path_len, double* d_dist, void* stream);
 
+/* ---- text codec (dataset files, reference datafiles.py) ----------------
+ * repr(float(v)) of each value into a 32-byte slot of d_out (length in
+ * d_len), bit-exact with CPython's shortest round-trip repr. Async. */
+int sa_repr_values(const double* d_values, int64_t n, char* d_out, int32_t* d_len, void* stream);
+/* float(field) for the UTF-8 fields d_text[d_offsets[i] .. d_offsets[i+1]),
+ * bit-exact with CPython's float(str) (Unicode digits and spaces, '_'
+ * separators, inf/nan, correct rounding); d_ok[i] = 0 where float() would
+ * raise ValueError. d_scratch: a buffer as large as the text, used only for
+ * non-ASCII fields (may be NULL for ASCII text; non-ASCII fields then fail).
+ * Async. */
+int sa_parse_values(const char* d_text, const int64_t* d_offsets, int64_t n, double* d_out, int32_t* d_ok,
+                    char* d_scratch, void* stream);
+
 /* SpectralAugmenter.augment_spectrum (reference freqaugment.py:49-76): one
  * spectral stage applied directly to a half spectrum. Synchronous. */
 int sa_augment_spectrum(const sa_stage* stage, uint64_t master_seed, int64_t series_offset,

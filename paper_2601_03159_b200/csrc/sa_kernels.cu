@@ -26,6 +26,7 @@
 
 #include "../../include/seriesaug_b200.h"
 #include "sa_dtw.cuh"
+#include "sa_text.cuh"
 #include "sa_ops.cuh"
 
 namespace sa {
@@ -394,6 +395,27 @@ __global__ void __launch_bounds__(32) dtw_path_kernel(const __grid_constant__ Dt
     if (threadIdx.x == 0) {
         p.dist[0] = d;
         p.path_len[0] = dtw_backtrack(p.acc, p.n, p.m, p.path);
+    }
+}
+
+// ------------------------------------------------------------ text codec (dataset IO)
+__global__ void __launch_bounds__(256) repr_values_kernel(const double* __restrict__ v, int64_t n, char* out,
+                                                          int32_t* len) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        char buf[32];
+        const int k = repr_format(v[i], buf);
+        for (int t = 0; t < k; ++t) out[i * 32 + t] = buf[t];
+        len[i] = k;
+    }
+}
+
+__global__ void __launch_bounds__(256) parse_values_kernel(const char* __restrict__ text, const int64_t* __restrict__ off,
+                                                           int64_t n, double* out, int32_t* ok, char* scratch) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double v = 0.0;
+        const bool good = parse_field(text, off[i], off[i + 1], scratch, &v);
+        out[i] = v;
+        ok[i] = good ? 1 : 0;
     }
 }
 
@@ -1142,6 +1164,31 @@ int sa_dtw_path(const double* d_a, int64_t len_a, const double* d_b, int64_t len
     p.a = d_a; p.b = d_b; p.dist = d_dist; p.acc = d_acc; p.path = d_path; p.path_len = d_path_len;
     p.pairs = 1; p.n = (int32_t)len_a; p.m = (int32_t)len_b;
     dtw_path_kernel<<<1, 32, smem, (cudaStream_t)stream>>>(p);
+    SA_CUDA(cudaGetLastError());
+    __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
+    return SA_OK;
+}
+
+int sa_repr_values(const double* d_values, int64_t n, char* d_out, int32_t* d_len, void* stream) {
+    int dev;
+    int rc = ensure_device(&dev);
+    if (rc) return rc;
+    if (n == 0) return SA_OK;
+    const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)dev_state(dev).sms * 16);
+    repr_values_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(d_values, n, d_out, d_len);
+    SA_CUDA(cudaGetLastError());
+    __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
+    return SA_OK;
+}
+
+int sa_parse_values(const char* d_text, const int64_t* d_offsets, int64_t n, double* d_out, int32_t* d_ok,
+                    char* d_scratch, void* stream) {
+    int dev;
+    int rc = ensure_device(&dev);
+    if (rc) return rc;
+    if (n == 0) return SA_OK;
+    const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)dev_state(dev).sms * 16);
+    parse_values_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(d_text, d_offsets, n, d_out, d_ok, d_scratch);
     SA_CUDA(cudaGetLastError());
     __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
     return SA_OK;
