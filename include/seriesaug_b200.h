@@ -185,6 +185,73 @@ int sa_repr_values(const double* d_values, int64_t n, char* d_out, int32_t* d_le
 int sa_parse_values(const char* d_text, const int64_t* d_offsets, int64_t n, double* d_out, int32_t* d_ok,
                     char* d_scratch, void* stream);
 
+/* ---- dataset files (reference datafiles.py:70-143) --------------------
+ * parse_dataset on device-resident UTF-8 text:
+ *   sa_dataset_open   line split (str.splitlines), strip, format detection
+ *                     ('@' on the first non-blank line), TS header/label
+ *                     split (rsplit ':'), field counts and the reference's
+ *                     structural errors in line order.  Synchronizes.  On
+ *                     info->status == SA_DS_OK the batch is n_series x length.
+ *   sa_dataset_values float() of every field into d_values (row-major
+ *                     n_series x length); may report SA_DS_NOT_A_NUMBER or
+ *                     SA_DS_NONFINITE.  Synchronizes.
+ *   sa_dataset_labels / sa_dataset_headers  the TS labels (stripped) / header
+ *                     lines, each followed by '\n', label_bytes / header_bytes
+ *                     in total.  Async.
+ *   sa_dataset_close  frees the handle's tables (stream ordered).
+ * Errors report the first failing line (1-based, as the reference) and for
+ * SA_DS_NOT_A_NUMBER the field's byte range [err_begin, err_end) in the text;
+ * for SA_DS_BAD_UTF8 err_begin is the first invalid byte. */
+#define SA_FORMAT_AUTO (-1)
+#define SA_FORMAT_CSV 0
+#define SA_FORMAT_TS 1
+#define SA_DS_OK 0
+#define SA_DS_EMPTY 1             /* "dataset file is empty" */
+#define SA_DS_HEADER_AFTER_DATA 2 /* "line N: header after first data row" */
+#define SA_DS_MISSING_LABEL 3     /* "line N: missing ':label' separator" */
+#define SA_DS_NOT_A_NUMBER 4      /* "line N: not a number: '...'" */
+#define SA_DS_RAGGED 5            /* "line N: F fields, but line M has W" */
+#define SA_DS_NO_DATA 6           /* "dataset file has headers but no data rows" */
+#define SA_DS_NONFINITE 7         /* Batch: "batch contains non-finite values" */
+#define SA_DS_BAD_UTF8 8          /* the file is not UTF-8 (UnicodeDecodeError) */
+
+typedef struct sa_dataset sa_dataset;
+typedef struct sa_dataset_info {
+    int32_t format; /* SA_FORMAT_CSV / SA_FORMAT_TS, detected or forced */
+    int32_t status; /* SA_DS_* */
+    int64_t n_lines;
+    int64_t n_series;
+    int64_t length;
+    int64_t header_bytes;
+    int64_t label_bytes;
+    int64_t err_line;
+    int64_t err_ref_line;
+    int64_t err_fields;
+    int64_t err_ref_fields;
+    int64_t err_begin;
+    int64_t err_end;
+} sa_dataset_info;
+
+int sa_dataset_open(const char* d_text, int64_t n_bytes, int32_t format, int32_t validate_utf8, sa_dataset** out,
+                    sa_dataset_info* info, void* stream);
+int sa_dataset_values(sa_dataset* ds, double* d_values, sa_dataset_info* info);
+int sa_dataset_labels(sa_dataset* ds, char* d_out);
+int sa_dataset_headers(sa_dataset* ds, char* d_out);
+int sa_dataset_close(sa_dataset* ds);
+
+/* format_dataset rows (datafiles.py:127-138): row r of the n x len batch is
+ * ",".join(repr(v)) [+ ":" + label r] + "\n".  Labels (TS only, may be NULL
+ * for empty labels) are bytes d_labels[d_label_off[r] .. d_label_off[r+1]).
+ * sa_dataset_format_size writes each row's absolute offset (base = bytes
+ * before the first row, e.g. the header lines) into d_row_off[n] and the
+ * file size into *total (synchronizes); sa_dataset_format_write writes the
+ * rows into d_out (async). */
+int sa_dataset_format_size(const double* d_values, int64_t n, int64_t len, int32_t format,
+                           const int64_t* d_label_off, int64_t base, int64_t* d_row_off, int64_t* total,
+                           void* stream);
+int sa_dataset_format_write(const double* d_values, int64_t n, int64_t len, int32_t format, const char* d_labels,
+                            const int64_t* d_label_off, const int64_t* d_row_off, char* d_out, void* stream);
+
 /* SpectralAugmenter.augment_spectrum (reference freqaugment.py:49-76): one
  * spectral stage applied directly to a half spectrum. Synchronous. */
 int sa_augment_spectrum(const sa_stage* stage, uint64_t master_seed, int64_t series_offset,

@@ -48,6 +48,28 @@ SA_OP_MAX = 24
 
 SA_MAX_STAGES = 64
 
+# dataset files (include/seriesaug_b200.h, reference datafiles.py)
+SA_FORMAT_AUTO = -1
+SA_FORMAT_CSV = 0
+SA_FORMAT_TS = 1
+SA_DS_OK = 0
+SA_DS_EMPTY = 1
+SA_DS_HEADER_AFTER_DATA = 2
+SA_DS_MISSING_LABEL = 3
+SA_DS_NOT_A_NUMBER = 4
+SA_DS_RAGGED = 5
+SA_DS_NO_DATA = 6
+SA_DS_NONFINITE = 7
+SA_DS_BAD_UTF8 = 8
+
+
+class SaDatasetInfo(ctypes.Structure):
+    _fields_ = [("format", ctypes.c_int32), ("status", ctypes.c_int32), ("n_lines", ctypes.c_int64),
+                ("n_series", ctypes.c_int64), ("length", ctypes.c_int64), ("header_bytes", ctypes.c_int64),
+                ("label_bytes", ctypes.c_int64), ("err_line", ctypes.c_int64), ("err_ref_line", ctypes.c_int64),
+                ("err_fields", ctypes.c_int64), ("err_ref_fields", ctypes.c_int64), ("err_begin", ctypes.c_int64),
+                ("err_end", ctypes.c_int64)]
+
 
 class SaStage(ctypes.Structure):
     """struct sa_stage: one lowered {kind, probability, params} record."""

@@ -27,6 +27,7 @@
 #include "../../include/seriesaug_b200.h"
 #include "sa_dtw.cuh"
 #include "sa_text.cuh"
+#include "sa_dataset.cuh"
 #include "sa_ops.cuh"
 
 namespace sa {
@@ -1237,3 +1238,5 @@ int sa_host_free(void* ptr) {
 }
 
 }  // extern "C"
+
+#include "sa_dataset_host.inc"

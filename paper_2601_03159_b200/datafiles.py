@@ -1,0 +1,327 @@
+"""Dataset files in the reference's two layouts, parsed and formatted on the
+GPU (reference: datafiles.py).
+
+CSV-rows: one series per line, comma-separated decimals, every line the same
+field count.  TS-style: '@'-prefixed header lines (kept verbatim), then one
+series per line with a class label after the last ':'.  The format is
+detected from the first non-blank line ('@' means TS) and can be forced.
+Numbers are written as ``repr(float(v))`` (shortest round trip) and read with
+``float()`` semantics -- both bit-exact on the device (csrc/sa_text.cuh).
+
+The text itself is split, stripped, classified, checked and converted by the
+kernels of csrc/sa_dataset.cuh through the C ABI (sa_dataset_*); the host
+only moves bytes and turns the kernels' status into the reference's
+exception messages.  ``parse_dataset_device`` / ``format_dataset_device``
+keep the batch in HBM for device-resident flows (``augment_file``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, replace
+from typing import Optional
+
+import numpy as np
+
+from . import _abi, _native
+from .core import Batch
+from .errors import InvalidInputError
+
+FORMATS = ("csv", "ts")
+_FMT_CODE = {"csv": _abi.SA_FORMAT_CSV, "ts": _abi.SA_FORMAT_TS}
+
+
+@dataclass(frozen=True)
+class DatasetFile:
+    """A parsed dataset (reference datafiles.py:24-56)."""
+
+    batch: Batch
+    format: str                            # "csv" | "ts"
+    header_lines: tuple[str, ...] = ()     # ts only, kept verbatim
+    labels: Optional[tuple[str, ...]] = None  # ts only, one per series
+
+    def __post_init__(self) -> None:
+        if self.format not in FORMATS:
+            raise InvalidInputError(f"format must be one of {FORMATS}, got {self.format!r}")
+        if self.labels is not None and len(self.labels) != self.batch.n:
+            raise InvalidInputError(f"{len(self.labels)} labels for {self.batch.n} series")
+        if self.format == "csv" and (self.header_lines or self.labels is not None):
+            raise InvalidInputError("csv datasets carry no header lines or labels")
+
+    def with_batch(self, batch: Batch) -> "DatasetFile":
+        """Carry format and labels over to an augmented batch; a batch grown
+        to a whole multiple of N (repeat) replicates each label consecutively
+        (datafiles.py:43-56)."""
+        labels = self.labels
+        if labels is not None and batch.n != self.batch.n:
+            if batch.n % self.batch.n != 0:
+                raise InvalidInputError(f"cannot carry {len(labels)} labels onto {batch.n} series")
+            r = batch.n // self.batch.n
+            labels = tuple(lab for lab in labels for _ in range(r))
+        return replace(self, batch=batch, labels=labels)
+
+
+@dataclass(frozen=True)
+class DeviceDataset:
+    """A parsed dataset whose (n, L) float64 batch stays on the GPU."""
+
+    values: object                         # torch.Tensor, cuda, float64
+    format: str
+    header_lines: tuple[str, ...] = ()
+    labels: Optional[tuple[str, ...]] = None
+
+
+def _vp(x) -> ctypes.c_void_p:
+    return ctypes.c_void_p(int(x))
+
+
+def _cur_stream(torch, dev):
+    return _vp(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def _to_device_bytes(data, dev):
+    """Host bytes -> (cuda uint8 tensor, nbytes); page-locked staging so the
+    copy runs at PCIe speed."""
+    import torch
+
+    from .memory import pinned_empty
+
+    mv = memoryview(data).cast("B")
+    n = mv.nbytes
+    host = pinned_empty((max(n, 1),), np.uint8)
+    if n:
+        host[:n] = np.frombuffer(mv, dtype=np.uint8)
+    d = torch.empty(max(n, 1), dtype=torch.uint8, device=f"cuda:{dev}")
+    d.copy_(torch.from_numpy(host), non_blocking=True)
+    torch.cuda.current_stream(dev).synchronize()
+    return d, n
+
+
+def _split_joined(buf: bytes, count: int) -> tuple[str, ...]:
+    """'\\n'-terminated items -> tuple of str."""
+    if count == 0:
+        return ()
+    items = buf.decode("utf-8", "surrogatepass").split("\n")
+    return tuple(items[:count])
+
+
+def _raise_status(info, host_bytes) -> None:
+    st = info.status
+    k = info.err_line
+    if st == _abi.SA_DS_EMPTY:
+        raise InvalidInputError("dataset file is empty")
+    if st == _abi.SA_DS_HEADER_AFTER_DATA:
+        raise InvalidInputError(f"line {k}: header after first data row")
+    if st == _abi.SA_DS_MISSING_LABEL:
+        raise InvalidInputError(f"line {k}: missing ':label' separator")
+    if st == _abi.SA_DS_NOT_A_NUMBER:
+        field = bytes(host_bytes[info.err_begin:info.err_end]).decode("utf-8", "surrogatepass")
+        raise InvalidInputError(f"line {k}: not a number: {field.strip()!r}")
+    if st == _abi.SA_DS_RAGGED:
+        raise InvalidInputError(
+            f"line {k}: {info.err_fields} fields, but line {info.err_ref_line} has {info.err_ref_fields}")
+    if st == _abi.SA_DS_NO_DATA:
+        raise InvalidInputError("dataset file has headers but no data rows")
+    if st == _abi.SA_DS_NONFINITE:
+        raise InvalidInputError("batch contains non-finite values (NaN or Inf)")
+    if st == _abi.SA_DS_BAD_UTF8:
+        bytes(host_bytes).decode("utf-8")  # raises the decoder's own UnicodeDecodeError
+    raise RuntimeError(f"dataset parse: unexpected status {st}")
+
+
+def _parse_device(d_text, nbytes: int, host_bytes, fmt, validate: bool) -> DeviceDataset:
+    import torch
+
+    if fmt is not None and fmt not in FORMATS:
+        code = _abi.SA_FORMAT_AUTO
+    else:
+        code = _abi.SA_FORMAT_AUTO if fmt is None else _FMT_CODE[fmt]
+    dev = d_text.device.index
+    L = _native.lib()
+    stream = _cur_stream(torch, dev)
+    info = _abi.SaDatasetInfo()
+    handle = ctypes.c_void_p()
+    _native.check(L.sa_dataset_open(_vp(d_text.data_ptr()), nbytes, code, 1 if validate else 0,
+                                    ctypes.byref(handle), ctypes.byref(info), stream), "sa_dataset_open")
+    try:
+        if fmt is not None and fmt not in FORMATS:
+            if info.status in (_abi.SA_DS_EMPTY, _abi.SA_DS_BAD_UTF8):  # checked before the format (:71-79)
+                _raise_status(info, host_bytes)
+            raise InvalidInputError(f"format must be one of {FORMATS}, got {fmt!r}")
+        values = None
+        if info.status == _abi.SA_DS_OK:
+            values = torch.empty((info.n_series, info.length), dtype=torch.float64, device=d_text.device)
+            _native.check(L.sa_dataset_values(handle, _vp(values.data_ptr()), ctypes.byref(info)),
+                          "sa_dataset_values")
+        if info.status != _abi.SA_DS_OK:
+            _raise_status(info, host_bytes)
+        fmt_name = FORMATS[info.format]
+        hb, lb = info.header_bytes, info.label_bytes
+        d_hdr = torch.empty(max(hb, 1), dtype=torch.uint8, device=d_text.device)
+        d_lab = torch.empty(max(lb, 1), dtype=torch.uint8, device=d_text.device)
+        _native.check(L.sa_dataset_headers(handle, _vp(d_hdr.data_ptr())), "sa_dataset_headers")
+        _native.check(L.sa_dataset_labels(handle, _vp(d_lab.data_ptr())), "sa_dataset_labels")
+        headers = ()
+        if hb:
+            headers = tuple(d_hdr[:hb].cpu().numpy().tobytes().decode("utf-8", "surrogatepass").split("\n")[:-1])
+        labels = None
+        if fmt_name == "ts":
+            labels = _split_joined(d_lab[:lb].cpu().numpy().tobytes(), info.n_series)
+        return DeviceDataset(values=values, format=fmt_name, header_lines=headers, labels=labels)
+    finally:
+        L.sa_dataset_close(handle)
+
+
+def parse_dataset_device(data, fmt: Optional[str] = None, *, validate_utf8: bool = True) -> DeviceDataset:
+    """Parse UTF-8 dataset bytes on the current GPU; the batch stays there."""
+    dev = _native.current_device()
+    d_text, n = _to_device_bytes(data, dev)
+    return _parse_device(d_text, n, memoryview(data).cast("B"), fmt, validate_utf8)
+
+
+def parse_dataset(text: str, fmt: Optional[str] = None) -> DatasetFile:
+    """Reference datafiles.py:70-116 -- same result, same first error."""
+    data = text.encode("utf-8", "surrogatepass")
+    dd = parse_dataset_device(data, fmt, validate_utf8=False)
+    return _to_host(dd)
+
+
+def _to_host(dd: DeviceDataset) -> DatasetFile:
+    values = dd.values.cpu().numpy()
+    return DatasetFile(batch=Batch._from_device_checked(values), format=dd.format,
+                       header_lines=dd.header_lines, labels=dd.labels)
+
+
+def read_dataset(path, fmt: Optional[str] = None) -> DatasetFile:
+    """Reference datafiles.py:119-124: errors are prefixed with the path."""
+    from .memory import pinned_empty
+
+    with open(path, "rb") as fh:
+        size = fh.seek(0, 2)
+        fh.seek(0)
+        host = pinned_empty((max(size, 1),), np.uint8)
+        got = fh.readinto(memoryview(host)[:size]) if size else 0
+    data = memoryview(host)[:got]
+    try:
+        dd = parse_dataset_device(data, fmt)
+    except InvalidInputError as exc:
+        raise InvalidInputError(f"{path}: {exc}") from None
+    return _to_host(dd)
+
+
+# ------------------------------------------------------------------ format
+def _label_blob(labels, n: int):
+    """(label bytes without separators, int64 offsets[n+1]) or (None, None)."""
+    if labels is None:
+        return None, None
+    joined = "\n".join(labels)
+    blob = joined.encode("utf-8", "surrogatepass")
+    arr = np.frombuffer(blob, dtype=np.uint8)
+    nl = np.flatnonzero(arr == 10)
+    if len(nl) == n - 1:
+        ends = np.append(nl, len(arr)).astype(np.int64)
+        starts = np.concatenate([[0], nl + 1]).astype(np.int64)
+        lens = ends - starts
+        data = arr[arr != 10] if len(nl) else arr
+    else:  # labels that themselves hold '\n'
+        enc = [lab.encode("utf-8", "surrogatepass") for lab in labels]
+        lens = np.array([len(e) for e in enc], dtype=np.int64)
+        data = np.frombuffer(b"".join(enc), dtype=np.uint8)
+    off = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(lens, out=off[1:])
+    return data, off
+
+
+def format_dataset_device(values, fmt: str = "csv", header_lines=(), labels=None) -> bytes:
+    """The file bytes of format_dataset for an (n, L) CUDA float64 tensor."""
+    import torch
+
+    if fmt not in FORMATS:
+        raise InvalidInputError(f"format must be one of {FORMATS}, got {fmt!r}")
+    dev = values.device.index
+    values = values.contiguous()
+    n, length = int(values.shape[0]), int(values.shape[1])
+    L = _native.lib()
+    stream = _cur_stream(torch, dev)
+    head = "".join(h + "\n" for h in header_lines).encode("utf-8", "surrogatepass") if fmt == "ts" else b""
+    d_lab = d_off = None
+    if fmt == "ts" and labels is not None:
+        data, off = _label_blob(labels, n)
+        d_lab = torch.from_numpy(np.ascontiguousarray(data) if len(data) else np.zeros(1, np.uint8)).to(values.device)
+        d_off = torch.from_numpy(off).to(values.device)
+    row_off = torch.empty(n, dtype=torch.int64, device=values.device)
+    total = ctypes.c_int64()
+    _native.check(L.sa_dataset_format_size(_vp(values.data_ptr()), n, length, _FMT_CODE[fmt],
+                                           _vp(d_off.data_ptr()) if d_off is not None else None, len(head),
+                                           _vp(row_off.data_ptr()), ctypes.byref(total), stream),
+                  "sa_dataset_format_size")
+    out = torch.empty(total.value, dtype=torch.uint8, device=values.device)
+    if head:
+        out[:len(head)].copy_(torch.frombuffer(bytearray(head), dtype=torch.uint8))
+    _native.check(L.sa_dataset_format_write(_vp(values.data_ptr()), n, length, _FMT_CODE[fmt],
+                                            _vp(d_lab.data_ptr()) if d_lab is not None else None,
+                                            _vp(d_off.data_ptr()) if d_off is not None else None,
+                                            _vp(row_off.data_ptr()), _vp(out.data_ptr()), stream),
+                  "sa_dataset_format_write")
+    from .memory import pinned_empty
+
+    host = pinned_empty((total.value,), np.uint8)
+    torch.from_numpy(host).copy_(out, non_blocking=True)
+    torch.cuda.current_stream(dev).synchronize()
+    return host.tobytes()
+
+
+def format_dataset(ds: DatasetFile) -> str:
+    """Reference datafiles.py:127-138."""
+    import torch
+
+    dev = _native.current_device()
+    values = torch.from_numpy(np.ascontiguousarray(ds.batch.values)).to(f"cuda:{dev}")
+    labels = ds.labels
+    return format_dataset_device(values, ds.format, ds.header_lines, labels).decode("utf-8", "surrogatepass")
+
+
+def write_dataset(path, ds: DatasetFile) -> None:
+    """Reference datafiles.py:141-143."""
+    import torch
+
+    dev = _native.current_device()
+    values = torch.from_numpy(np.ascontiguousarray(ds.batch.values)).to(f"cuda:{dev}")
+    _write_bytes(path, format_dataset_device(values, ds.format, ds.header_lines, ds.labels), ds)
+
+
+def _write_bytes(path, data: bytes, ds_like) -> None:
+    try:  # the reference's text-mode write fails on unencodable labels/headers
+        for s in tuple(ds_like.header_lines) + tuple(ds_like.labels or ()):
+            s.encode("utf-8")
+    except UnicodeEncodeError:
+        with open(path, "w", encoding="utf-8") as fh:
+            fh.write(data.decode("utf-8", "surrogatepass"))
+        return
+    with open(path, "wb") as fh:
+        fh.write(data)
+
+
+def augment_file(src, dst, pipeline, fmt: Optional[str] = None) -> DeviceDataset:
+    """The reference's `seriesaug augment` data path (cli.py:48-54) with the
+    batch resident in HBM: read -> parse -> pipeline -> format -> write, one
+    H2D of the input text and one D2H of the output text."""
+    from .memory import pinned_empty
+
+    with open(src, "rb") as fh:
+        size = fh.seek(0, 2)
+        fh.seek(0)
+        host = pinned_empty((max(size, 1),), np.uint8)
+        got = fh.readinto(memoryview(host)[:size]) if size else 0
+    try:
+        dd = parse_dataset_device(memoryview(host)[:got], fmt)
+    except InvalidInputError as exc:
+        raise InvalidInputError(f"{src}: {exc}") from None
+    out = pipeline.run_device(dd.values)
+    labels = dd.labels
+    if labels is not None and out.shape[0] != dd.values.shape[0]:
+        r = out.shape[0] // dd.values.shape[0]
+        labels = tuple(lab for lab in labels for _ in range(r))
+    res = DeviceDataset(values=out, format=dd.format, header_lines=dd.header_lines, labels=labels)
+    _write_bytes(dst, format_dataset_device(out, dd.format, dd.header_lines, labels), res)
+    return res

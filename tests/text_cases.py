@@ -119,3 +119,83 @@ def py_float(s: str):
         return float(s), True
     except ValueError:
         return 0.0, False
+
+
+# ------------------------------------------------------------------ datasets
+_BREAKS = ["\n"] * 8 + ["\r\n", "\r", "\x0b", "\x0c", "\x1c", "\x1d", "\x1e", "\x85", "\u2028", "\u2029"]
+_PADS = ["", "", "", " ", "\t", "  ", "\xa0", "\u3000", "\u2003"]
+_LABELS = ["a", "b", "class 1", "", "  spaced  ", "\u03bb", "\u65e5\u672c", "x,y", "7"]
+
+
+def _field_text(rng, v: float) -> str:
+    r = rng.random()
+    if r < 0.6:
+        s = repr(float(v))
+    elif r < 0.75:
+        s = "%.17g" % v
+    elif r < 0.85:
+        s = "%.6e" % v
+    elif r < 0.9:
+        s = "%.3f" % v
+    elif r < 0.95 and abs(v) >= 1000 and float(int(v)) == v:
+        s = f"{int(v):_}"
+    else:
+        s = repr(float(v)).upper()
+    if rng.random() < 0.05:
+        s = _PADS[int(rng.integers(0, len(_PADS)))] + s + _PADS[int(rng.integers(0, len(_PADS)))]
+    return s
+
+
+def random_dataset(seed: int, n: int, L: int, ts: bool):
+    """(text, values, labels, headers): a valid dataset with mixed number
+    spellings, padding, blank lines and every str.splitlines() break;
+    values are float() of the spelled fields."""
+    rng = np.random.default_rng(seed)
+    pool = interesting_doubles(2000, seed)
+    pool = pool[np.abs(pool) < 1e300]  # '%.3f' of huge values stays finite
+    values = pool[rng.integers(0, len(pool), (n, L))]
+    spelled = [[_field_text(rng, v) for v in row] for row in values]
+    values = np.array([[float(f) for f in row] for row in spelled], dtype=np.float64).reshape(n, L)
+    headers = [f"@problemName set{seed}", "@timeStamps false", "@data"] if ts else []
+    labels = [_LABELS[int(rng.integers(0, len(_LABELS)))] for _ in range(n)] if ts else None
+    lines = list(headers)
+    for r in range(n):
+        body = ",".join(spelled[r])
+        if ts:
+            body += ":" + labels[r]
+        lines.append(body)
+        if rng.random() < 0.05:
+            lines.append(_PADS[int(rng.integers(0, len(_PADS)))])
+    text = ""
+    for ln in lines:
+        text += ln + _BREAKS[int(rng.integers(0, len(_BREAKS)))]
+    if rng.random() < 0.3:
+        text = text.rstrip("\n")
+    return text, values, labels, headers
+
+
+def corrupt_dataset(text: str, seed: int) -> str:
+    """One random corruption (bad number, ragged row, late header, missing
+    label separator, non-finite value) at a random line."""
+    rng = np.random.default_rng(seed)
+    lines = text.split("\n")
+    k = int(rng.integers(0, len(lines)))
+    kind = int(rng.integers(0, 6))
+    ln = lines[k]
+    if kind == 0 and "," in ln:
+        parts = ln.split(",")
+        j = int(rng.integers(0, len(parts)))
+        parts[j] = ["zz", "", "1..2", "1e", "--1", "0x1p3", "1_", "١x"][int(rng.integers(0, 8))]
+        ln = ",".join(parts)
+    elif kind == 1 and "," in ln:
+        ln = ln.replace(",", "", 1)
+    elif kind == 2:
+        ln = ln + ",1.5"
+    elif kind == 3:
+        ln = "@late header"
+    elif kind == 4:
+        ln = ln.replace(":", ";")
+    else:
+        ln = ln.replace(",", ",inf,", 1) if rng.random() < 0.5 else ln.replace(",", ",1e999,", 1)
+    lines[k] = ln
+    return "\n".join(lines)
