@@ -366,6 +366,169 @@ def run_suite(args):
     print(json.dumps(res), flush=True)
 
 
+DS_SHAPE = (100_000, 1024)
+DS_WORKLOAD = ("datafiles: TS dataset of 100,000 x 1,024 random walks (repr floats, 3 header lines, "
+               "labels): parse_dataset + format_dataset, text resident in HBM")
+
+
+def ds_text(n, L):
+    """The synthetic dataset: random walks formatted by the device codec and
+    checked against the oracle's formatting on a sample of rows."""
+    import torch
+
+    from bench_inputs import device_walks
+    from paper_2601_03159_b200 import format_dataset_device
+    from oracle import datafiles_oracle as O
+
+    x = device_walks(n, L, 7, torch.device("cuda", 0))
+    headers = ("@problemName walks", "@timeStamps false", "@data")
+    labels = tuple(f"c{r % 5}" for r in range(n))
+    data = format_dataset_device(x, "ts", headers, labels)
+    head = "".join(h + "\n" for h in headers)
+    sample = O.format_rows(x[:50].cpu().numpy(), "ts", headers, labels[:50])
+    if not data.startswith(sample.encode()) or not data.startswith(head.encode()):
+        raise RuntimeError("device formatting differs from the oracle")
+    return x, data, headers, labels
+
+
+def ds_cpu_baseline(data: bytes, n: int, target_rows: int = 3000):
+    """The reference algorithm (oracle/datafiles_oracle.py: Python's float /
+    repr, as the reference) on the first rows of the same file, one core."""
+    from oracle import datafiles_oracle as O
+
+    text = data.decode()
+    cut = 0
+    for _ in range(3 + target_rows):
+        cut = text.index("\n", cut) + 1
+    part = text[:cut]
+    t0 = time.perf_counter()
+    fmt, headers, labels, values = O.parse(part)
+    t1 = time.perf_counter()
+    O.format_rows(values, fmt, headers, labels)
+    t2 = time.perf_counter()
+    nbytes = len(part.encode())
+    return {"value": 2 * nbytes / (t2 - t0), "unit": "B/s", "cores": 1, "kind": "port",
+            "sample": f"first {target_rows} of {n} rows ({nbytes} bytes) parsed + formatted "
+                      f"({t1 - t0:.2f} s + {t2 - t1:.2f} s)",
+            "parse_bps": nbytes / (t1 - t0), "format_bps": nbytes / (t2 - t1)}
+
+
+def run_datafiles_reference(args, rank):
+    """The reference algorithm on the host (oracle port), bounded sample."""
+    if rank != 0:
+        return
+    from oracle import datafiles_oracle as O
+
+    n, L = DS_SHAPE
+    rng = np.random.default_rng(7)
+    rows = 2000
+    x = np.cumsum(rng.normal(0, 1, (rows, L)), axis=1)
+    headers = ("@problemName walks", "@timeStamps false", "@data")
+    labels = tuple(f"c{r % 5}" for r in range(rows))
+    text = O.format_rows(x, "ts", headers, labels)
+    for _ in range(args.warmup):
+        O.format_rows(O.parse(text)[3], "ts", headers, labels)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        fmt, h, lab, v = O.parse(text)
+        O.format_rows(v, fmt, h, lab)
+    dt = (time.perf_counter() - t0) / args.steps
+    nb = len(text.encode())
+    val = 2 * nb / dt
+    print(json.dumps({
+        "impl": "reference", "metric": "dataset text bytes/s (parse + format)", "value": val, "unit": "B/s",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+        "higher_is_better": True, "scaling": "replicas", "vs_baseline": None, "dtype": "f64+u8",
+        "data": "synthetic (seeded random walks)",
+        "config": {"workload": DS_WORKLOAD, "sample_series": rows, "len": L, "text_bytes": nb},
+        "cpu_baseline": {"value": val, "unit": "B/s", "cores": 1, "kind": "port",
+                         "sample": f"{rows} of {n} rows per step"},
+        "e2e": {"value": val, "unit": "B/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}), flush=True)
+
+
+def run_datafiles(args, rank, world, local_rank):
+    """One step = parse the resident TS text into the batch + format the
+    batch back into text (the two ends of `seriesaug augment`)."""
+    import torch
+
+    from paper_2601_03159_b200 import _native, format_dataset_device, parse_dataset_device
+    from paper_2601_03159_b200.datafiles import _parse_device, format_dataset_to_device
+
+    if rank != 0:
+        return
+    torch.cuda.set_device(0)
+    _native.ensure_device(0)
+    n, L = DS_SHAPE
+    if args.n_series:
+        n = args.n_series
+    x, data, headers, labels = ds_text(n, L)
+    nbytes = len(data)
+    d_text = torch.frombuffer(bytearray(data), dtype=torch.uint8).cuda()
+    hv = memoryview(data)
+
+    def step(pev=None, fev=None):
+        dd = _parse_device(d_text, nbytes, hv, None, True, events=pev)
+        out = format_dataset_to_device(dd.values, dd.format, dd.header_lines, dd.labels, events=fev)
+        return dd, out
+
+    for _ in range(args.warmup):
+        dd, out = step()
+    torch.cuda.synchronize()
+    if not torch.equal(out, d_text) or not torch.equal(dd.values, x):
+        raise RuntimeError("parse/format round trip differs")
+    launches0 = _native.launch_count()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)]
+    pev, fev = [], []
+    torch.cuda.synchronize()
+    with Clocks(local_rank) as clk:
+        for k in range(args.steps):
+            ev[2 * k].record()
+            step(pev, fev)
+            ev[2 * k + 1].record()
+        torch.cuda.synchronize()
+    launches = _native.launch_count() - launches0
+    ms = sum(ev[2 * k].elapsed_time(ev[2 * k + 1]) for k in range(args.steps)) / args.steps
+    p_ms = sum(a.elapsed_time(b) for a, b in pev) / len(pev)
+    f_ms = sum(a.elapsed_time(b) for a, b in fev) / len(fev)
+    # e2e through the public calls with host buffers: file bytes -> batch in
+    # host memory; host batch -> file bytes
+    host_vals = x.cpu().numpy()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v = parse_dataset_device(hv).values.cpu()
+        b = format_dataset_device(torch.from_numpy(host_vals).cuda(), "ts", headers, labels)
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    if b != data or not torch.equal(v, x.cpu()):
+        raise RuntimeError("e2e round trip differs")
+    peak, peak_src = measured_peak()
+    vals_b = 8 * n * L
+    # dominant kernels: rows_parse (text in, values out) and row_write
+    # (values in, text out); each moves text + values bytes once
+    ach_p = (nbytes + vals_b) / (p_ms / 1e3) / 1e9
+    ach_f = (nbytes + vals_b) / (f_ms / 1e3) / 1e9
+    dom = "rows_parse_kernel" if p_ms >= f_ms else "row_write_kernel"
+    ach = ach_p if p_ms >= f_ms else ach_f
+    line = {
+        "metric": "dataset text bytes/s (parse + format)", "value": 2 * nbytes / (ms / 1e3), "unit": "B/s",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "replicas", "vs_baseline": None, "dtype": "f64+u8",
+        "data": "synthetic (seeded random walks, device-formatted; oracle-checked sample)",
+        "config": {"workload": DS_WORKLOAD, "n_series": n, "len": L, "text_bytes": nbytes,
+                   "rows_parse_ms": p_ms, "row_write_ms": f_ms, "rows_parse_gbs": ach_p, "row_write_gbs": ach_f,
+                   "l2": "text and batch larger than L2 (no flush needed)"},
+        "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                     "traffic": None, "peak_source": peak_src, "kernel": dom,
+                     "algorithmic_bytes_per_launch": nbytes + vals_b},
+        "e2e": {"value": 2 * nbytes / e2e_s, "unit": "B/s", "h2d_bytes_per_step": nbytes + vals_b,
+                "d2h_bytes_per_step": nbytes + vals_b},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu:
+        line["cpu_baseline"] = ds_cpu_baseline(data, n)
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -377,8 +540,16 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--suite", action="store_true", help="configs 1-5 + sweep, device-resident, one JSON")
+    ap.add_argument("--workload", default="pipeline", choices=["pipeline", "datafiles"],
+                    help="datafiles: the dataset parse/format codec (SURVEY.md §8(f) next-3)")
     args = ap.parse_args()
     rank, world, local_rank = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    if args.workload == "datafiles":
+        if args.impl == "reference":
+            run_datafiles_reference(args, rank)
+        else:
+            run_datafiles(args, rank, world, local_rank)
+        return
     if args.suite:
         run_suite(args)
         return

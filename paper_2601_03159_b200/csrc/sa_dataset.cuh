@@ -40,6 +40,7 @@ struct Stat {
     unsigned long long bad_field;   // global index of the first field float() rejects
     unsigned long long bad_utf8;    // first invalid byte
     unsigned long long n_headers;
+    unsigned long long nslow;       // fields the fast path left to slow_parse_kernel
     unsigned int nonascii;
     unsigned int ends_with_break;
     unsigned int nonfinite;
@@ -102,6 +103,33 @@ __device__ bool utf8_ok_at(const char* t, int64_t p, int64_t nb) {
 
 // any byte < 0x20 or >= 0x80 in a 4-byte word
 __device__ __forceinline__ bool word_special(uint32_t w) { return (__vcmpltu4(w, 0x20202020u) | (w & 0x80808080u)) != 0; }
+
+// 16 bytes at w (16-aligned offset); bytes at or past nb read as 0
+__device__ __forceinline__ uint4 load16(const char* t, int64_t w, int64_t nb) {
+    if (w + 16 <= nb) return *reinterpret_cast<const uint4*>(t + w);
+    uint32_t x[4] = {0, 0, 0, 0};
+    for (int i = 0; i < 16 && w + i < nb; ++i) x[i >> 2] |= (uint32_t)byte_at(t, w + i) << (8 * (i & 3));
+    return make_uint4(x[0], x[1], x[2], x[3]);
+}
+
+// bit i set where byte i of the 16-byte word equals c
+__device__ __forceinline__ uint32_t match16(uint4 w, uint32_t c4) {
+    uint32_t m = 0;
+    const uint32_t v[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint32_t e = __vcmpeq4(v[k], c4) & 0x01010101u;  // 1 per matching byte
+        m |= ((e * 0x10204080u) >> 28) << (4 * k);           // gather 4 bits
+    }
+    return m;
+}
+
+// bits i with lo <= base + i < hi
+__device__ __forceinline__ uint32_t range16(int64_t base, int64_t lo, int64_t hi) {
+    const int64_t a = lo - base < 0 ? 0 : (lo - base > 16 ? 16 : lo - base);
+    const int64_t b = hi - base < 0 ? 0 : (hi - base > 16 ? 16 : hi - base);
+    return (uint32_t)(((1u << b) - 1) & ~((1u << a) - 1)) & 0xffffu;
+}
 
 // ---------------------------------------------------------------- segmentation
 __device__ __forceinline__ int thread_breaks(const char* t, int64_t nb, int64_t a, int64_t b, bool validate,
@@ -297,37 +325,45 @@ __device__ void strip_serial(const char* t, int64_t* pa, int64_t* pb) {
     *pb = b;
 }
 
+__device__ __forceinline__ bool ascii_graph(uint8_t c) { return c > 0x20 && c < 0x7f; }
+
 __global__ void __launch_bounds__(256) line_kernel(const char* __restrict__ t, int64_t nb, Lines L, Stat* st) {
     const int lane = threadIdx.x & 31;
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const bool aligned = ((uintptr_t)t & 15) == 0;
     for (int64_t k = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); k < L.n; k += nw) {
         const int64_t a = k == 0 ? 0 : L.bnext[k - 1];
         const int64_t b = k < L.nbreaks ? L.bstart[k] : nb;
-        // first non-whitespace character
+        // str.strip(): the common line starts and ends with a printable ASCII byte
         int64_t s = b;
-        for (int64_t p0 = a; p0 < b; p0 += 32) {
-            const int64_t p = p0 + lane;
-            const bool hit = p < b && nonws_char_at(t, p, b);
-            const unsigned m = __ballot_sync(0xffffffffu, hit);
-            if (m) {
-                s = p0 + __ffs(m) - 1;
-                break;
+        if (a < b && ascii_graph(byte_at(t, a))) {
+            s = a;
+        } else {
+            for (int64_t p0 = a; p0 < b; p0 += 32) {
+                const int64_t p = p0 + lane;
+                const unsigned m = __ballot_sync(0xffffffffu, p < b && nonws_char_at(t, p, b));
+                if (m) {
+                    s = p0 + __ffs(m) - 1;
+                    break;
+                }
             }
         }
-        // end of the last non-whitespace character
         int64_t e = s;
-        for (int64_t p1 = b; p1 > s; p1 -= 32) {
-            const int64_t p = p1 - 1 - lane;
-            const bool hit = p >= s && nonws_char_at(t, p, b);
-            const unsigned m = __ballot_sync(0xffffffffu, hit);
-            if (m) {
-                int64_t q = p1 - 1 - (__ffs(m) - 1);  // lowest lane = highest position
-                uint32_t cp;
-                e = q + sa::utf8_decode(t, q, b, &cp);
-                break;
+        if (s < b && ascii_graph(byte_at(t, b - 1))) {
+            e = b;
+        } else {
+            for (int64_t p1 = b; p1 > s; p1 -= 32) {
+                const int64_t p = p1 - 1 - lane;
+                const unsigned m = __ballot_sync(0xffffffffu, p >= s && nonws_char_at(t, p, b));
+                if (m) {
+                    const int64_t q = p1 - 1 - (__ffs(m) - 1);  // lowest lane = highest position
+                    uint32_t cp;
+                    e = q + sa::utf8_decode(t, q, b, &cp);
+                    break;
+                }
             }
         }
-        // last ':' in [s, e)
+        // last ':' in [s, e) (labels are short: found in the first step)
         int64_t colon = -1;
         for (int64_t p1 = e; p1 > s; p1 -= 32) {
             const int64_t p = p1 - 1 - lane;
@@ -337,13 +373,24 @@ __global__ void __launch_bounds__(256) line_kernel(const char* __restrict__ t, i
                 break;
             }
         }
-        // commas in [s, e) and in [s, colon)
+        // commas in [s, e) and in [s, colon): 16 bytes per lane per step
         int64_t call = 0, cval = 0;
-        for (int64_t p0 = s; p0 < e; p0 += 32) {
-            const int64_t p = p0 + lane;
-            const bool c = p < e && t[p] == ',';
-            call += __popc(__ballot_sync(0xffffffffu, c));
-            cval += __popc(__ballot_sync(0xffffffffu, c && p < colon));
+        if (aligned) {
+            for (int64_t w = (s & ~(int64_t)15) + 16 * lane; w < e; w += 512) {
+                const uint32_t m = match16(load16(t, w, nb), 0x2c2c2c2cu);
+                call += __popc(m & range16(w, s, e));
+                cval += __popc(m & range16(w, s, colon));
+            }
+        } else {
+            for (int64_t p = s + lane; p < e; p += 32) {
+                const bool c = t[p] == ',';
+                call += c;
+                cval += c && p < colon;
+            }
+        }
+        for (int d = 16; d; d >>= 1) {
+            call += __shfl_xor_sync(0xffffffffu, call, d);
+            cval += __shfl_xor_sync(0xffffffffu, cval, d);
         }
         if (lane == 0) {
             uint8_t f = 0;
@@ -454,6 +501,105 @@ __global__ void __launch_bounds__(256) parse_kernel(const char* __restrict__ t, 
     }
 }
 
+// Fused field split + float(): warp per data line, the line streamed
+// through shared memory in 1 KB windows (coalesced 16-byte loads); commas
+// found with byte-compare masks and a warp prefix count; each lane parses
+// whole fields out of shared memory and the row's values are stored
+// coalesced at field_off[k] + j (the batch is row-major n x width).
+constexpr int kParseWarps = 8;
+constexpr int kWin = 1024;
+
+struct SlowField {
+    int64_t gi, a, b;  // global field index, byte range
+};
+
+__device__ __forceinline__ void put_value(int64_t gi, const char* t, int64_t fa, int64_t fb, bool ok, double v,
+                                          double* out, Stat* st, SlowField* slow, int64_t slow_cap) {
+    if (!ok) {  // left for slow_parse_kernel (full grammar, exact rounding, Unicode, errors)
+        const unsigned long long q = atomicAdd(&st->nslow, 1ull);
+        if ((int64_t)q < slow_cap) slow[q] = SlowField{gi, fa, fb};
+        return;
+    }
+    if (((uint64_t)__double_as_longlong(v) & 0x7ff0000000000000ull) == 0x7ff0000000000000ull) st->nonfinite = 1;
+    out[gi] = v;
+}
+
+// field text without surrounding ASCII whitespace, fast path only
+__device__ __forceinline__ bool parse_fast(const char* t, int64_t a, int64_t b, double* v) {
+    while (a < b && sa::py_isspace(t[a])) ++a;
+    while (b > a && sa::py_isspace(t[b - 1])) --b;
+    return b - a <= 64 && sa::parse_simple(t + a, (int)(b - a), v);
+}
+
+__global__ void __launch_bounds__(kParseWarps * 32) rows_parse_kernel(const char* __restrict__ t, int64_t nb, Lines L,
+                                                                      const int64_t* __restrict__ nfields,
+                                                                      const int64_t* __restrict__ field_off,
+                                                                      double* __restrict__ out, Stat* st,
+                                                                      SlowField* slow, int64_t slow_cap) {
+    __shared__ __align__(16) char win[kParseWarps][kWin];
+    __shared__ uint16_t cpos[kParseWarps][kWin];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    char* buf = win[wid];
+    uint16_t* cp = cpos[wid];
+    const bool ts = st->format != 0;
+    const int64_t nwarps = (int64_t)gridDim.x * kParseWarps;
+    for (int64_t k = blockIdx.x * (int64_t)kParseWarps + wid; k < L.n; k += nwarps) {
+        const int64_t nf = nfields[k];
+        if (nf == 0) continue;
+        const int64_t s = L.s[k];
+        const int64_t vend = ts ? L.colon[k] : L.e[k];
+        const int64_t base = field_off[k];
+        int64_t fstart = s;  // start of the field in progress
+        int64_t j = 0;       // fields completed
+        for (int64_t w0 = s & ~(int64_t)15; w0 < vend; w0 += kWin) {
+            // stage [w0, w0 + kWin) and mark commas; lane covers 32 contiguous bytes
+            const int64_t wa = w0 + 32 * lane;
+            const uint4 v0 = load16(t, wa, nb), v1 = load16(t, wa + 16, nb);
+            *reinterpret_cast<uint4*>(buf + 32 * lane) = v0;
+            *reinterpret_cast<uint4*>(buf + 32 * lane + 16) = v1;
+            const uint32_t m = (match16(v0, 0x2c2c2c2cu) & range16(wa, s, vend)) |
+                               ((match16(v1, 0x2c2c2c2cu) & range16(wa + 16, s, vend)) << 16);
+            const int c = __popc(m);
+            int incl = c;
+            for (int d = 1; d < 32; d <<= 1) {
+                const int u = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += u;
+            }
+            int o = incl - c;
+            for (uint32_t mm = m; mm; mm &= mm - 1) cp[o++] = (uint16_t)(32 * lane + __ffs(mm) - 1);
+            const int ncomma = __shfl_sync(0xffffffffu, incl, 31);
+            __syncwarp();
+            for (int q = lane; q < ncomma; q += 32) {
+                const int64_t fb = w0 + cp[q];
+                const int64_t fa = q == 0 ? fstart : w0 + cp[q - 1] + 1;
+                double v = 0.0;
+                const bool ok = fa >= w0 ? parse_fast(buf - w0, fa, fb, &v) : parse_fast(t, fa, fb, &v);
+                put_value(base + j + q, t, fa, fb, ok, v, out, st, slow, slow_cap);
+            }
+            if (ncomma) fstart = w0 + cp[ncomma - 1] + 1;
+            j += ncomma;
+            __syncwarp();
+        }
+        if (lane == 0) {  // the last field ends at the values' end
+            double v = 0.0;
+            const bool ok = parse_fast(t, fstart, vend, &v);
+            put_value(base + nf - 1, t, fstart, vend, ok, v, out, st, slow, slow_cap);
+        }
+    }
+}
+
+// the fields the fast path could not decide: full float() semantics
+__global__ void __launch_bounds__(128) slow_parse_kernel(const char* __restrict__ t, const SlowField* __restrict__ slow,
+                                                        int64_t n, char* scratch, double* out, Stat* st) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const SlowField f = slow[i];
+        double v = 0.0;
+        if (!parse_field(t, f.a, f.b, scratch, &v)) atomicMin(&st->bad_field, (unsigned long long)f.gi);
+        if (((uint64_t)__double_as_longlong(v) & 0x7ff0000000000000ull) == 0x7ff0000000000000ull) st->nonfinite = 1;
+        out[f.gi] = v;
+    }
+}
+
 // join the selected ranges with a trailing '\n' each at off[k]
 __global__ void __launch_bounds__(256) gather_kernel(const char* __restrict__ t, const int64_t* sel, const int64_t* a,
                                                     const int64_t* off, int64_t n, char* out) {
@@ -480,10 +626,7 @@ __global__ void __launch_bounds__(256) row_size_kernel(const double* __restrict_
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += nw) {
         int64_t tot = 0;
-        for (int64_t j = lane; j < len; j += 32) {
-            char buf[32];
-            tot += repr_format(v[r * len + j], buf);
-        }
+        for (int64_t j = lane; j < len; j += 32) tot += sa::repr_len(sa::repr_decompose(v[r * len + j]));
         for (int d = 16; d; d >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, d);
         if (lane == 0) {
             tot += len - 1 + 1;  // commas + '\n'
@@ -493,41 +636,91 @@ __global__ void __launch_bounds__(256) row_size_kernel(const double* __restrict_
     }
 }
 
-__global__ void __launch_bounds__(256) row_write_kernel(const double* __restrict__ v, int64_t n, int64_t len, int ts,
-                                                       const char* __restrict__ labels,
-                                                       const int64_t* __restrict__ lab_off,
-                                                       const int64_t* __restrict__ row_off, char* out) {
-    const int lane = threadIdx.x & 31;
-    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += nw) {
-        int64_t pos = row_off[r];
+// Warp per row: 32 values at a time are rendered into a shared-memory
+// staging buffer at their prefix-summed offsets, and full 32-byte runs are
+// flushed with coalesced stores (one sector per warp store).
+constexpr int kFmtWarps = 8;
+constexpr int kStage = 2048;
+
+__device__ __forceinline__ void flush_stage(char* out, int64_t pos, const char* stg, int nbytes, int lane) {
+    // byte-coalesced copy; 4-byte stores once the destination is aligned
+    int i = 0;
+    const int head = (int)((4 - (pos & 3)) & 3) < nbytes ? (int)((4 - (pos & 3)) & 3) : nbytes;
+    if (lane < head) out[pos + lane] = stg[lane];
+    i = head;
+    const int nw = (nbytes - i) >> 2;
+    uint32_t* o4 = reinterpret_cast<uint32_t*>(out + pos + i);
+    for (int q = lane; q < nw; q += 32) {
+        const char* src = stg + i + 4 * q;
+        o4[q] = (uint32_t)(uint8_t)src[0] | ((uint32_t)(uint8_t)src[1] << 8) | ((uint32_t)(uint8_t)src[2] << 16) |
+                ((uint32_t)(uint8_t)src[3] << 24);
+    }
+    i += 4 * nw;
+    if (lane < nbytes - i) out[pos + i + lane] = stg[i + lane];
+}
+
+__global__ void __launch_bounds__(kFmtWarps * 32) row_write_kernel(const double* __restrict__ v, int64_t n, int64_t len,
+                                                                  int ts, const char* __restrict__ labels,
+                                                                  const int64_t* __restrict__ lab_off,
+                                                                  const int64_t* __restrict__ row_off, char* out) {
+    __shared__ char stage[kFmtWarps][kStage + 64];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    char* stg = stage[wid];
+    const int64_t nw = (int64_t)gridDim.x * kFmtWarps;
+    for (int64_t r = blockIdx.x * (int64_t)kFmtWarps + wid; r < n; r += nw) {
+        int64_t pos = row_off[r];  // file offset of stg[0]
+        int fill = 0;              // bytes staged
         for (int64_t j0 = 0; j0 < len; j0 += 32) {
             const int64_t j = j0 + lane;
-            char buf[32];
+            sa::Repr rp;
             int k = 0;
             if (j < len) {
-                k = repr_format(v[r * len + j], buf);
-                if (j + 1 < len) buf[k++] = ',';
+                rp = sa::repr_decompose(v[r * len + j]);
+                k = sa::repr_len(rp) + (j + 1 < len ? 1 : 0);
             }
             int incl = k;
             for (int d = 1; d < 32; d <<= 1) {
                 const int u = __shfl_up_sync(0xffffffffu, incl, d);
                 if (lane >= d) incl += u;
             }
-            char* dst = out + pos + incl - k;
-            for (int q = 0; q < k; ++q) dst[q] = buf[q];
-            pos += __shfl_sync(0xffffffffu, incl, 31);
+            const int total = __shfl_sync(0xffffffffu, incl, 31);
+            if (fill + total > kStage) {  // at most 32 * 25 bytes per step
+                flush_stage(out, pos, stg, fill, lane);
+                pos += fill;
+                fill = 0;
+                __syncwarp();
+            }
+            if (j < len) {
+                char* d = stg + fill + incl - k;
+                sa::repr_write(rp, d);
+                if (j + 1 < len) d[k - 1] = ',';
+            }
+            fill += total;
+            __syncwarp();
         }
         if (ts) {
-            if (lane == 0) out[pos] = ':';
-            ++pos;
-            if (lab_off) {
-                const int64_t la = lab_off[r], lb = lab_off[r + 1];
-                for (int64_t q = lane; q < lb - la; q += 32) out[pos + q] = labels[la + q];
-                pos += lb - la;
+            const int64_t la = lab_off ? lab_off[r] : 0, lb = lab_off ? lab_off[r + 1] : 0;
+            if (fill + 1 + (lb - la) + 1 > kStage) {
+                flush_stage(out, pos, stg, fill, lane);
+                pos += fill;
+                fill = 0;
+                __syncwarp();
+            }
+            if (fill + 1 + (lb - la) + 1 <= kStage) {
+                if (lane == 0) stg[fill] = ':';
+                for (int64_t q = lane; q < lb - la; q += 32) stg[fill + 1 + q] = labels[la + q];
+                fill += 1 + (int)(lb - la);
+            } else {  // a label longer than the stage goes straight out
+                if (lane == 0) out[pos] = ':';
+                for (int64_t q = lane; q < lb - la; q += 32) out[pos + 1 + q] = labels[la + q];
+                pos += 1 + (lb - la);
             }
         }
-        if (lane == 0) out[pos] = '\n';
+        if (lane == 0) stg[fill] = '\n';
+        ++fill;
+        __syncwarp();
+        flush_stage(out, pos, stg, fill, lane);
+        __syncwarp();
     }
 }
 

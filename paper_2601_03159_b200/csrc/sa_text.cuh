@@ -160,39 +160,94 @@ __device__ Decimal shortest_decimal(uint64_t bits) {
 }
 
 // ------------------------------------------------------------ repr(float)
-// Writes CPython's repr of a double into dst (>= 25 bytes); returns the
-// number of bytes.
-__device__ int repr_format(double v, char* dst) {
-    uint64_t bits = (uint64_t)__double_as_longlong(v);
-    int n = 0;
-    if ((bits & 0x7ff0000000000000ull) == 0x7ff0000000000000ull) {
-        if (bits & 0x000fffffffffffffull) {  // nan prints unsigned
-            dst[0] = 'n'; dst[1] = 'a'; dst[2] = 'n';
-            return 3;
-        }
-        if (bits >> 63) dst[n++] = '-';
-        dst[n++] = 'i'; dst[n++] = 'n'; dst[n++] = 'f';
-        return n;
+// CPython's float_repr (mode 'r', Py_DTSF_ADD_DOT_0): shortest digits; the
+// exponent form 'd[.ddd]e[+-]XX' iff the decimal point position decpt is
+// <= -4 or > 16, else fixed notation with at least one fractional digit.
+struct Repr {
+    uint64_t digits;
+    int nd;     // digit count of `digits`
+    int decpt;  // value = 0.digits * 10^decpt
+    int kind;   // 0 finite non-zero, 1 zero, 2 inf, 3 nan
+    bool neg;
+};
+
+__device__ __forceinline__ int digit_count(uint64_t v) {
+    int n = 1;
+    uint64_t p = 10;
+    while (n < 20 && v >= p) {
+        ++n;
+        p *= 10;
     }
-    if (bits >> 63) {
-        dst[n++] = '-';
-        bits &= ~(1ull << 63);
+    return n;
+}
+
+__device__ __forceinline__ Repr repr_decompose(double v) {
+    uint64_t bits = (uint64_t)__double_as_longlong(v);
+    Repr r;
+    r.neg = (bits >> 63) != 0;
+    bits &= ~(1ull << 63);
+    r.digits = 0;
+    r.nd = 0;
+    r.decpt = 0;
+    if (bits >= 0x7ff0000000000000ull) {
+        r.kind = bits > 0x7ff0000000000000ull ? 3 : 2;
+        if (r.kind == 3) r.neg = false;  // nan prints unsigned
+        return r;
     }
     if (bits == 0) {
-        dst[n++] = '0'; dst[n++] = '.'; dst[n++] = '0';
-        return n;
+        r.kind = 1;
+        return r;
     }
+    r.kind = 0;
     const Decimal d = shortest_decimal(bits);
-    char dig[20];
-    int nd = 0;
-    for (uint64_t t = d.digits; t; t /= 10) dig[nd++] = (char)('0' + (int)(t % 10));  // reversed
-    const int decpt = d.exp10 + nd;
+    r.digits = d.digits;
+    r.nd = digit_count(d.digits);
+    r.decpt = d.exp10 + r.nd;
+    return r;
+}
+
+__device__ __forceinline__ int repr_len(const Repr& r) {
+    int n = r.neg ? 1 : 0;
+    if (r.kind != 0) return n + 3;  // "0.0" / "inf" / "nan"
+    const int nd = r.nd, decpt = r.decpt;
     if (decpt <= -4 || decpt > 16) {
-        dst[n++] = dig[nd - 1];
-        if (nd > 1) {
-            dst[n++] = '.';
-            for (int k = nd - 2; k >= 0; --k) dst[n++] = dig[k];
+        const int x = decpt - 1 < 0 ? 1 - decpt : decpt - 1;
+        return n + nd + (nd > 1 ? 1 : 0) + 2 + (x >= 100 ? 3 : 2);
+    }
+    if (decpt <= 0) return n + 2 - decpt + nd;
+    if (decpt >= nd) return n + decpt + 2;
+    return n + nd + 1;
+}
+
+// writes repr_len(r) bytes at dst
+__device__ __forceinline__ void repr_write(const Repr& r, char* dst) {
+    int n = 0;
+    if (r.neg) dst[n++] = '-';
+    if (r.kind == 1) {
+        dst[n] = '0'; dst[n + 1] = '.'; dst[n + 2] = '0';
+        return;
+    }
+    if (r.kind == 2) {
+        dst[n] = 'i'; dst[n + 1] = 'n'; dst[n + 2] = 'f';
+        return;
+    }
+    if (r.kind == 3) {
+        dst[n] = 'n'; dst[n + 1] = 'a'; dst[n + 2] = 'n';
+        return;
+    }
+    const int nd = r.nd, decpt = r.decpt;
+    // digit k (0 = most significant) lands at pos(k); written from the last
+    // digit backwards so each division yields one character
+    if (decpt <= -4 || decpt > 16) {
+        uint64_t t = r.digits;
+        for (int k = nd - 1; k >= 1; --k) {
+            const uint64_t q = t / 10;
+            dst[n + 1 + k] = (char)('0' + (int)(t - 10 * q));
+            t = q;
         }
+        dst[n] = (char)('0' + (int)t);
+        if (nd > 1) dst[n + 1] = '.';
+        n += nd + (nd > 1 ? 1 : 0);
         dst[n++] = 'e';
         int x = decpt - 1;
         dst[n++] = x < 0 ? '-' : '+';
@@ -200,22 +255,48 @@ __device__ int repr_format(double v, char* dst) {
         if (x >= 100) dst[n++] = (char)('0' + x / 100);
         dst[n++] = (char)('0' + (x / 10) % 10);
         dst[n++] = (char)('0' + x % 10);
-    } else if (decpt <= 0) {
+        return;
+    }
+    if (decpt <= 0) {
         dst[n++] = '0';
         dst[n++] = '.';
         for (int k = 0; k < -decpt; ++k) dst[n++] = '0';
-        for (int k = nd - 1; k >= 0; --k) dst[n++] = dig[k];
-    } else if (decpt >= nd) {
-        for (int k = nd - 1; k >= 0; --k) dst[n++] = dig[k];
-        for (int k = 0; k < decpt - nd; ++k) dst[n++] = '0';
-        dst[n++] = '.';
-        dst[n++] = '0';
-    } else {
-        for (int k = nd - 1; k >= nd - decpt; --k) dst[n++] = dig[k];
-        dst[n++] = '.';
-        for (int k = nd - decpt - 1; k >= 0; --k) dst[n++] = dig[k];
+        uint64_t t = r.digits;
+        for (int k = nd - 1; k >= 0; --k) {
+            const uint64_t q = t / 10;
+            dst[n + k] = (char)('0' + (int)(t - 10 * q));
+            t = q;
+        }
+        return;
     }
-    return n;
+    if (decpt >= nd) {
+        uint64_t t = r.digits;
+        for (int k = nd - 1; k >= 0; --k) {
+            const uint64_t q = t / 10;
+            dst[n + k] = (char)('0' + (int)(t - 10 * q));
+            t = q;
+        }
+        n += nd;
+        for (int k = 0; k < decpt - nd; ++k) dst[n++] = '0';
+        dst[n] = '.';
+        dst[n + 1] = '0';
+        return;
+    }
+    uint64_t t = r.digits;  // digits 0..decpt-1, '.', digits decpt..nd-1
+    for (int k = nd - 1; k >= 0; --k) {
+        const uint64_t q = t / 10;
+        dst[n + k + (k >= decpt ? 1 : 0)] = (char)('0' + (int)(t - 10 * q));
+        t = q;
+    }
+    dst[n + decpt] = '.';
+}
+
+// Writes CPython's repr of a double into dst (>= 25 bytes); returns the
+// number of bytes.
+__device__ __forceinline__ int repr_format(double v, char* dst) {
+    const Repr r = repr_decompose(v);
+    repr_write(r, dst);
+    return repr_len(r);
 }
 
 // ------------------------------------------------------------ exact big integers
@@ -332,143 +413,11 @@ __device__ __forceinline__ uint64_t pack_double(uint64_t m, int e2) {
     return ((uint64_t)(e2 + 52 + 1023) << 52) | (m & ((1ull << 52) - 1));
 }
 
-// CPython float(): [+-] (digits['.'digits] | '.'digits) [e[+-]digits] with
-// '_' allowed between digits, or inf / infinity / nan (case-insensitive).
-// s[0..n) is already stripped of surrounding whitespace.
-__device__ bool parse_pyfloat(const char* s, int n, double* out) {
-    int i = 0;
-    bool neg = false;
-    if (i < n && (s[i] == '+' || s[i] == '-')) {
-        neg = s[i] == '-';
-        ++i;
-    }
-    if (i < n && !is_digit(s[i]) && s[i] != '.') {
-        const int len = n - i;
-        char w[8];
-        if (len != 3 && len != 8) return false;
-        for (int k = 0; k < len; ++k) {
-            const char c = s[i + k];
-            w[k] = (c >= 'A' && c <= 'Z') ? (char)(c + 32) : c;
-        }
-        const bool inf = (len == 3 && w[0] == 'i' && w[1] == 'n' && w[2] == 'f') ||
-                         (len == 8 && w[0] == 'i' && w[1] == 'n' && w[2] == 'f' && w[3] == 'i' && w[4] == 'n' &&
-                          w[5] == 'i' && w[6] == 't' && w[7] == 'y');
-        const bool nan = len == 3 && w[0] == 'n' && w[1] == 'a' && w[2] == 'n';
-        if (!inf && !nan) return false;
-        const uint64_t bits = inf ? 0x7ff0000000000000ull : 0x7ff8000000000000ull;
-        *out = __longlong_as_double((long long)(bits | (neg ? 1ull << 63 : 0)));
-        return true;
-    }
-    // mantissa: digit runs separated by single '_' between digits
-    const int m0 = i;
-    int dot = -1, nint = 0, nfrac = 0;
-    for (bool frac = false;;) {
-        int run = 0;
-        while (i < n && (is_digit(s[i]) || (s[i] == '_' && run > 0 && i + 1 < n && is_digit(s[i + 1])))) {
-            if (s[i] != '_') {
-                if (frac) ++nfrac;
-                else ++nint;
-            }
-            ++run;
-            ++i;
-        }
-        if (!frac && i < n && s[i] == '.') {
-            dot = i++;
-            frac = true;
-            continue;
-        }
-        break;
-    }
-    if (nint + nfrac == 0) return false;
-    const int m1 = i;
-    long long ex = 0;
-    if (i < n && (s[i] == 'e' || s[i] == 'E')) {
-        ++i;
-        bool eneg = false;
-        if (i < n && (s[i] == '+' || s[i] == '-')) {
-            eneg = s[i] == '-';
-            ++i;
-        }
-        int ed = 0;
-        while (i < n && (is_digit(s[i]) || (s[i] == '_' && ed > 0 && i + 1 < n && is_digit(s[i + 1])))) {
-            if (s[i] != '_') {
-                if (ex < 1000000000ll) ex = ex * 10 + (s[i] - '0');
-                ++ed;
-            }
-            ++i;
-        }
-        if (ed == 0) return false;
-        if (eneg) ex = -ex;
-    }
-    if (i != n) return false;
-
-    // significant digits: first non-zero digit onwards
-    int p0 = m0;
-    while (p0 < m1 && (s[p0] == '0' || s[p0] == '_' || s[p0] == '.')) ++p0;
-    const uint64_t sgn = neg ? 1ull << 63 : 0;
-    if (p0 == m1) {  // all digits zero
-        *out = __longlong_as_double((long long)sgn);
-        return true;
-    }
-    int nd = 0;
-    uint64_t w19 = 0;
-    bool trunc = false;
-    for (int k = p0; k < m1; ++k) {
-        if (!is_digit(s[k])) continue;
-        if (nd < 19) w19 = w19 * 10 + (uint64_t)(s[k] - '0');
-        else if (s[k] != '0') trunc = true;
-        ++nd;
-    }
-    // value = (all significant digits as an integer) * 10^(ex - nfrac)
-    const long long e_last = ex - nfrac;
-    const int n19 = nd < 19 ? nd : 19;
-    const long long q_ll = e_last + (nd - n19);  // exponent of w19's last digit
-    if (q_ll + n19 <= -324) {                  // < 10^-324: rounds to zero
-        *out = __longlong_as_double((long long)sgn);
-        return true;
-    }
-    if (q_ll + n19 - 1 >= 309) {               // >= 10^309: rounds to inf
-        *out = __longlong_as_double((long long)(sgn | 0x7ff0000000000000ull));
-        return true;
-    }
-    const int q = (int)q_ll;  // in [-342, 308] here
-
-    // ---- fast path: normalised w19 times the 128-bit power of five
-    const int lz = __clzll(w19);
-    const uint64_t wn = w19 << lz;
-    const uint64_t* T = kLemirePow5[q + 342];
-    const U128 a = mul64(wn, T[1]);
-    const U128 b = mul64(wn, T[0]);
-    uint64_t mid = a.lo + b.hi;
-    uint64_t hi = a.hi + (mid < a.lo ? 1 : 0);
-    uint64_t low = b.lo;
-    int lead = 191;
-    if (!(hi >> 63)) {
-        hi = (hi << 1) | (mid >> 63);
-        mid = (mid << 1) | (low >> 63);
-        low <<= 1;
-        lead = 190;
-    }
-    // T = 5^q * 2^(127 - floor(log2 5^q)) (+-1); value ~ P * 2^(q - lz - s)
-    const int fl5 = q >= 0 ? pow5bits(q) - 1 : -pow5bits(-q);
-    const int E = lead + q - lz - (127 - fl5);  // unbiased exponent of the leading bit
-    uint64_t mant = hi >> 11;                   // 53 bits
-    const uint64_t rem = hi & 0x7ff;            // the 139-bit remainder is rem:mid:low
-    // |product error| < 2^65 low-units: the rounding is decided unless the
-    // remainder lies within 2 mid-units of the halfway pattern 0x400:0:0
-    const bool near_half = (rem == 0x400 && mid <= 1) || (rem == 0x3ff && mid >= ~1ull);
-    if (!trunc && !near_half && E >= -1022 && E <= 1023) {
-        uint64_t m = mant + ((rem > 0x400 || (rem == 0x400 && mid > 1)) ? 1 : 0);
-        int e2 = E - 52;
-        if (m == (1ull << 53)) {
-            m >>= 1;
-            ++e2;
-        }
-        *out = __longlong_as_double((long long)(sgn | pack_double(m, e2)));
-        return true;
-    }
-
-    // ---- exact path: big-integer comparisons around the candidate
+// Exact decision by big-integer comparison around the candidate m * 2^e2
+// (halfway-close products, > 19 significant digits, subnormals).  Kept out of
+// line: the fast path stays small and register-light.
+__device__ __noinline__ uint64_t parse_exact(const char* s, int p0, int m1, int nd, long long e_last, int E,
+                                             uint64_t mant) {
     const int K = nd < 800 ? nd : 800;
     bool sticky = false;
     {
@@ -510,7 +459,146 @@ __device__ bool parse_pyfloat(const char* s, int n, double* out) {
         ++m;
         if (m == (1ull << 53)) { m = 1ull << 52; ++e2; }
     }
-    *out = __longlong_as_double((long long)(sgn | pack_double(m, e2)));
+    return pack_double(m, e2);
+}
+
+__device__ __noinline__ bool parse_special(const char* s, int i, int n, bool neg, double* out) {
+    const int len = n - i;
+    char w[8];
+    if (len != 3 && len != 8) return false;
+    for (int k = 0; k < len; ++k) {
+        const char c = s[i + k];
+        w[k] = (c >= 'A' && c <= 'Z') ? (char)(c + 32) : c;
+    }
+    const bool inf = (len == 3 && w[0] == 'i' && w[1] == 'n' && w[2] == 'f') ||
+                     (len == 8 && w[0] == 'i' && w[1] == 'n' && w[2] == 'f' && w[3] == 'i' && w[4] == 'n' &&
+                      w[5] == 'i' && w[6] == 't' && w[7] == 'y');
+    const bool nan = len == 3 && w[0] == 'n' && w[1] == 'a' && w[2] == 'n';
+    if (!inf && !nan) return false;
+    const uint64_t bits = inf ? 0x7ff0000000000000ull : 0x7ff8000000000000ull;
+    *out = __longlong_as_double((long long)(bits | (neg ? 1ull << 63 : 0)));
+    return true;
+}
+
+// CPython float(): [+-] (digits['.'digits] | '.'digits) [e[+-]digits] with
+// '_' allowed between two digits, or inf / infinity / nan (case-insensitive).
+// s[0..n) is already stripped of surrounding whitespace.  One pass collects
+// the first 19 significant digits; the 64x128-bit product decides the
+// rounding unless it is too close to a halfway point (parse_exact).
+__device__ __noinline__ bool parse_pyfloat(const char* s, int n, double* out) {
+    int i = 0;
+    bool neg = false;
+    if (i < n && (s[i] == '+' || s[i] == '-')) {
+        neg = s[i] == '-';
+        ++i;
+    }
+    if (i < n && !is_digit(s[i]) && s[i] != '.') return parse_special(s, i, n, neg, out);
+    // mantissa, one pass
+    const int m0 = i;
+    int ndig = 0, nfrac = 0, nd = 0, p0 = -1;
+    bool frac = false, trunc = false;
+    uint64_t w19 = 0;
+    for (; i < n; ++i) {
+        const char c = s[i];
+        const unsigned d = (unsigned)(c - '0');
+        if (d < 10) {
+            ++ndig;
+            nfrac += frac;
+            if (d != 0 || nd > 0) {
+                if (nd == 0) p0 = i;
+                if (nd < 19) w19 = w19 * 10 + d;
+                else trunc |= d != 0;
+                ++nd;
+            }
+        } else if (c == '_') {
+            if (i == m0 || i + 1 >= n || !is_digit(s[i - 1]) || !is_digit(s[i + 1])) return false;
+        } else if (c == '.' && !frac) {
+            frac = true;
+        } else {
+            break;
+        }
+    }
+    if (ndig == 0) return false;
+    const int m1 = i;
+    long long ex = 0;
+    if (i < n && (s[i] == 'e' || s[i] == 'E')) {
+        ++i;
+        bool eneg = false;
+        if (i < n && (s[i] == '+' || s[i] == '-')) {
+            eneg = s[i] == '-';
+            ++i;
+        }
+        int ed = 0;
+        for (; i < n; ++i) {
+            const unsigned d = (unsigned)(s[i] - '0');
+            if (d < 10) {
+                if (ex < 1000000000ll) ex = ex * 10 + d;
+                ++ed;
+            } else if (s[i] == '_' && ed > 0 && i + 1 < n && is_digit(s[i + 1])) {
+                continue;
+            } else {
+                break;
+            }
+        }
+        if (ed == 0) return false;
+        if (eneg) ex = -ex;
+    }
+    if (i != n) return false;
+
+    const uint64_t sgn = neg ? 1ull << 63 : 0;
+    if (nd == 0) {  // all digits zero
+        *out = __longlong_as_double((long long)sgn);
+        return true;
+    }
+    // value = (all significant digits as an integer) * 10^(ex - nfrac)
+    const long long e_last = ex - nfrac;
+    const int n19 = nd < 19 ? nd : 19;
+    const long long q_ll = e_last + (nd - n19);  // exponent of w19's last digit
+    if (q_ll + n19 <= -324) {                  // < 10^-324: rounds to zero
+        *out = __longlong_as_double((long long)sgn);
+        return true;
+    }
+    if (q_ll + n19 - 1 >= 309) {               // >= 10^309: rounds to inf
+        *out = __longlong_as_double((long long)(sgn | 0x7ff0000000000000ull));
+        return true;
+    }
+    const int q = (int)q_ll;  // in [-342, 308] here
+
+    // ---- fast path: normalised w19 times the 128-bit power of five
+    const int lz = __clzll(w19);
+    const uint64_t wn = w19 << lz;
+    const uint64_t* T = kLemirePow5[q + 342];
+    const U128 a = mul64(wn, T[1]);
+    const U128 b = mul64(wn, T[0]);
+    uint64_t mid = a.lo + b.hi;
+    uint64_t hi = a.hi + (mid < a.lo ? 1 : 0);
+    int lead = 191;
+    if (!(hi >> 63)) {
+        hi = (hi << 1) | (mid >> 63);
+        mid = (mid << 1) | (b.lo >> 63);
+        lead = 190;
+    }
+    // T = 5^q * 2^(127 - floor(log2 5^q)) (+-1); value ~ P * 2^(q - lz - s)
+    const int fl5 = q >= 0 ? pow5bits(q) - 1 : -pow5bits(-q);
+    const int E = lead + q - lz - (127 - fl5);  // unbiased exponent of the leading bit
+    const uint64_t mant = hi >> 11;             // 53 bits
+    const uint64_t rem = hi & 0x7ff;            // the 139-bit remainder is rem:mid:low
+    // |product error| < 2^65 low-units: the rounding is decided unless the
+    // remainder lies within 2 mid-units of the halfway pattern 0x400:0:0
+    const bool near_half = (rem == 0x400 && mid <= 1) || (rem == 0x3ff && mid >= ~1ull);
+    uint64_t bits;
+    if (!trunc && !near_half && E >= -1022 && E <= 1023) {
+        uint64_t m = mant + ((rem > 0x400 || (rem == 0x400 && mid > 1)) ? 1 : 0);
+        int e2 = E - 52;
+        if (m == (1ull << 53)) {
+            m >>= 1;
+            ++e2;
+        }
+        bits = pack_double(m, e2);
+    } else {
+        bits = parse_exact(s, p0, m1, nd, e_last, E, mant);
+    }
+    *out = __longlong_as_double((long long)(sgn | bits));
     return true;
 }
 
@@ -551,34 +639,115 @@ __device__ __forceinline__ bool py_isspace(char c) { return c == ' ' || (c >= 9 
 // mapped (Unicode whitespace -> ' ', Nd digits -> ASCII, anything else
 // fails) into scratch[a:...] (same size as text, may be null when the text is
 // ASCII), then ASCII whitespace is stripped and the rest parsed.
+// Fast path for the common spelling [+-]digits[.digits][(e|E)[+-]d{1,4}]
+// with at most 19 digits and no '_': one tight loop, then the 64x128-bit
+// product.  Returns false when it cannot decide (other grammar, more digits,
+// near-halfway products, subnormal / overflow range); the caller then runs
+// the full parser, which gives the same answer for every input it accepts.
+__device__ __forceinline__ bool parse_simple(const char* s, int n, double* out) {
+    int i = (n > 0 && (s[0] == '-' || s[0] == '+')) ? 1 : 0;
+    const bool neg = n > 0 && s[0] == '-';
+    uint64_t w = 0;
+    int ndig = 0, dot = -1;
+    for (; i < n; ++i) {
+        const unsigned d = (unsigned)(uint8_t)s[i] - (unsigned)'0';
+        if (d < 10) {
+            w = w * 10 + d;
+            ++ndig;
+        } else if (s[i] == '.' && dot < 0) {
+            dot = ndig;
+        } else {
+            break;
+        }
+    }
+    if (ndig == 0 || ndig > 19) return false;
+    int ex = 0;
+    if (i < n) {
+        if ((s[i] | 0x20) != 'e') return false;
+        ++i;
+        const bool eneg = i < n && s[i] == '-';
+        if (i < n && (s[i] == '-' || s[i] == '+')) ++i;
+        const int e0 = i;
+        for (; i < n; ++i) {
+            const unsigned d = (unsigned)(uint8_t)s[i] - (unsigned)'0';
+            if (d >= 10) return false;
+            ex = ex * 10 + (int)d;
+        }
+        if (i == e0 || i - e0 > 4) return false;
+        if (eneg) ex = -ex;
+    }
+    const uint64_t sgn = neg ? 1ull << 63 : 0;
+    if (w == 0) {
+        *out = __longlong_as_double((long long)sgn);
+        return true;
+    }
+    const int q = ex - (dot >= 0 ? ndig - dot : 0);
+    if (q < -342 || q > 308) return false;
+    const int lz = __clzll(w);
+    const uint64_t wn = w << lz;
+    const uint64_t* T = kLemirePow5[q + 342];
+    const U128 a = mul64(wn, T[1]);
+    const U128 b = mul64(wn, T[0]);
+    uint64_t mid = a.lo + b.hi;
+    uint64_t hi = a.hi + (mid < a.lo ? 1 : 0);
+    int lead = 191;
+    if (!(hi >> 63)) {
+        hi = (hi << 1) | (mid >> 63);
+        mid = (mid << 1) | (b.lo >> 63);
+        lead = 190;
+    }
+    const int fl5 = q >= 0 ? pow5bits(q) - 1 : -pow5bits(-q);
+    const int E = lead + q - lz - (127 - fl5);
+    const uint64_t rem = hi & 0x7ff;
+    const bool near_half = (rem == 0x400 && mid <= 1) || (rem == 0x3ff && mid >= ~1ull);
+    if (near_half || E < -1022 || E > 1023) return false;
+    uint64_t m = (hi >> 11) + ((rem > 0x400 || (rem == 0x400 && mid > 1)) ? 1 : 0);
+    int e2 = E - 52;
+    if (m == (1ull << 53)) {
+        m >>= 1;
+        ++e2;
+    }
+    *out = __longlong_as_double((long long)(sgn | pack_double(m, e2)));
+    return true;
+}
+
+__device__ __noinline__ bool parse_field_unicode(const char* text, int64_t a, int64_t b, char* scratch,
+                                                 double* out) {
+    int64_t w = a;
+    for (int64_t p = a; p < b;) {
+        uint32_t cp;
+        const int k = utf8_decode(text, p, b, &cp);
+        p += k;
+        char c;
+        if (cp < 127) c = (char)cp;
+        else if (is_unicode_space(cp)) c = ' ';
+        else {
+            const int d = unicode_decimal(cp);
+            if (d < 0) return false;
+            c = (char)('0' + d);
+        }
+        scratch[w++] = c;
+    }
+    b = w;
+    while (a < b && py_isspace(scratch[a])) ++a;
+    while (b > a && py_isspace(scratch[b - 1])) --b;
+    if (b - a > 0x7fffffff) return false;
+    return parse_pyfloat(scratch + a, (int)(b - a), out);
+}
+
 __device__ bool parse_field(const char* text, int64_t a, int64_t b, char* scratch, double* out) {
+    int64_t s = a, e = b;
+    while (s < e && py_isspace(text[s])) ++s;
+    while (e > s && py_isspace(text[e - 1])) --e;
+    if (e - s <= 0x7fffffff) {
+        if (parse_simple(text + s, (int)(e - s), out)) return true;
+        if (parse_pyfloat(text + s, (int)(e - s), out)) return true;
+    }
+    // failed: non-ASCII text is first mapped like CPython, then parsed again
     bool ascii = true;
     for (int64_t p = a; p < b; ++p) ascii &= (uint8_t)text[p] < 0x80;
-    const char* s = text;
-    if (!ascii) {
-        if (scratch == nullptr) return false;
-        int64_t w = a;
-        for (int64_t p = a; p < b;) {
-            uint32_t cp;
-            const int k = utf8_decode(text, p, b, &cp);
-            p += k;
-            char c;
-            if (cp < 127) c = (char)cp;
-            else if (is_unicode_space(cp)) c = ' ';
-            else {
-                const int d = unicode_decimal(cp);
-                if (d < 0) return false;
-                c = (char)('0' + d);
-            }
-            scratch[w++] = c;
-        }
-        s = scratch;
-        b = w;
-    }
-    while (a < b && py_isspace(s[a])) ++a;
-    while (b > a && py_isspace(s[b - 1])) --b;
-    if (b - a > 0x7fffffff) return false;
-    return parse_pyfloat(s + a, (int)(b - a), out);
+    if (ascii || scratch == nullptr) return false;
+    return parse_field_unicode(text, a, b, scratch, out);
 }
 
 }  // namespace sa

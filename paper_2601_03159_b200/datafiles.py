@@ -18,6 +18,7 @@ keep the batch in HBM for device-resident flows (``augment_file``).
 from __future__ import annotations
 
 import ctypes
+import threading
 from dataclasses import dataclass, replace
 from typing import Optional
 
@@ -79,21 +80,44 @@ def _cur_stream(torch, dev):
     return _vp(torch.cuda.current_stream(dev).cuda_stream)
 
 
-def _to_device_bytes(data, dev):
-    """Host bytes -> (cuda uint8 tensor, nbytes); page-locked staging so the
-    copy runs at PCIe speed."""
-    import torch
+_staging: dict = {}
+_staging_lock = threading.Lock()
 
+
+def _staging_buffer(nbytes: int) -> np.ndarray:
+    """A grow-only page-locked host buffer (one per process): file bytes are
+    read into it and text is copied out of it at PCIe speed without a
+    page-locked allocation per call.  Callers hold _staging_lock."""
     from .memory import pinned_empty
+
+    buf = _staging.get("buf")
+    if buf is None or buf.size < nbytes:
+        cap = max(nbytes, 1 << 20)
+        if buf is not None:
+            cap = max(cap, 2 * buf.size)
+        buf = pinned_empty((cap,), np.uint8)
+        _staging["buf"] = buf
+    return buf
+
+
+def _to_device_bytes(data, dev):
+    """Host bytes -> (cuda uint8 tensor, nbytes) through the pinned staging
+    buffer (or straight from `data` when it already is that buffer)."""
+    import torch
 
     mv = memoryview(data).cast("B")
     n = mv.nbytes
-    host = pinned_empty((max(n, 1),), np.uint8)
-    if n:
-        host[:n] = np.frombuffer(mv, dtype=np.uint8)
     d = torch.empty(max(n, 1), dtype=torch.uint8, device=f"cuda:{dev}")
-    d.copy_(torch.from_numpy(host), non_blocking=True)
-    torch.cuda.current_stream(dev).synchronize()
+    if n == 0:
+        return d, 0
+    with _staging_lock:
+        host = _staging_buffer(n)
+        src = np.frombuffer(mv, dtype=np.uint8)
+        if not np.shares_memory(src, host):
+            host[:n] = src
+            src = host[:n]
+        d.copy_(torch.from_numpy(src), non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
     return d, n
 
 
@@ -125,11 +149,27 @@ def _raise_status(info, host_bytes) -> None:
     if st == _abi.SA_DS_NONFINITE:
         raise InvalidInputError("batch contains non-finite values (NaN or Inf)")
     if st == _abi.SA_DS_BAD_UTF8:
-        bytes(host_bytes).decode("utf-8")  # raises the decoder's own UnicodeDecodeError
+        raw = host_bytes.tobytes() if hasattr(host_bytes, "tobytes") else bytes(host_bytes)
+        raw.decode("utf-8")  # raises the decoder's own UnicodeDecodeError
     raise RuntimeError(f"dataset parse: unexpected status {st}")
 
 
-def _parse_device(d_text, nbytes: int, host_bytes, fmt, validate: bool) -> DeviceDataset:
+def _timed(events, fn):
+    """Run fn(); if `events` is a list, bracket it with CUDA events on the
+    current stream (bench.py times the dominant kernel this way)."""
+    if events is None:
+        return fn()
+    import torch
+
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    r = fn()
+    b.record()
+    events.append((a, b))
+    return r
+
+
+def _parse_device(d_text, nbytes: int, host_bytes, fmt, validate: bool, events=None) -> DeviceDataset:
     import torch
 
     if fmt is not None and fmt not in FORMATS:
@@ -151,8 +191,8 @@ def _parse_device(d_text, nbytes: int, host_bytes, fmt, validate: bool) -> Devic
         values = None
         if info.status == _abi.SA_DS_OK:
             values = torch.empty((info.n_series, info.length), dtype=torch.float64, device=d_text.device)
-            _native.check(L.sa_dataset_values(handle, _vp(values.data_ptr()), ctypes.byref(info)),
-                          "sa_dataset_values")
+            _native.check(_timed(events, lambda: L.sa_dataset_values(handle, _vp(values.data_ptr()),
+                                                                     ctypes.byref(info))), "sa_dataset_values")
         if info.status != _abi.SA_DS_OK:
             _raise_status(info, host_bytes)
         fmt_name = FORMATS[info.format]
@@ -194,19 +234,47 @@ def _to_host(dd: DeviceDataset) -> DatasetFile:
 
 def read_dataset(path, fmt: Optional[str] = None) -> DatasetFile:
     """Reference datafiles.py:119-124: errors are prefixed with the path."""
-    from .memory import pinned_empty
-
-    with open(path, "rb") as fh:
-        size = fh.seek(0, 2)
-        fh.seek(0)
-        host = pinned_empty((max(size, 1),), np.uint8)
-        got = fh.readinto(memoryview(host)[:size]) if size else 0
-    data = memoryview(host)[:got]
     try:
-        dd = parse_dataset_device(data, fmt)
+        dd = _read_device(path, fmt)
     except InvalidInputError as exc:
         raise InvalidInputError(f"{path}: {exc}") from None
     return _to_host(dd)
+
+
+def _read_device(path, fmt) -> DeviceDataset:
+    """File -> pinned staging (one read) -> HBM -> device parse."""
+    import torch
+
+    dev = _native.current_device()
+    with open(path, "rb") as fh:
+        size = fh.seek(0, 2)
+        fh.seek(0)
+        with _staging_lock:
+            host = _staging_buffer(max(size, 1))
+            got = fh.readinto(memoryview(host)[:size]) if size else 0
+            d = torch.empty(max(got, 1), dtype=torch.uint8, device=f"cuda:{dev}")
+            if got:
+                d.copy_(torch.from_numpy(host[:got]), non_blocking=True)
+                torch.cuda.current_stream(dev).synchronize()
+            # the host copy is needed only to word an error; keep the bytes
+            # only if the parse fails
+    try:
+        return _parse_device(d, got, _LazyHostBytes(d, got), fmt, True)
+    finally:
+        del d
+
+
+class _LazyHostBytes:
+    """Host view of device text, fetched only when an error message needs it."""
+
+    def __init__(self, d, n):
+        self.d, self.n = d, n
+
+    def __getitem__(self, sl):
+        return self.d[: self.n].cpu().numpy().tobytes()[sl]
+
+    def tobytes(self):
+        return self.d[: self.n].cpu().numpy().tobytes()
 
 
 # ------------------------------------------------------------------ format
@@ -234,6 +302,26 @@ def _label_blob(labels, n: int):
 
 def format_dataset_device(values, fmt: str = "csv", header_lines=(), labels=None) -> bytes:
     """The file bytes of format_dataset for an (n, L) CUDA float64 tensor."""
+    out = format_dataset_to_device(values, fmt, header_lines, labels)
+    return _fetch(out, lambda mv: bytes(mv))
+
+
+def _fetch(d_out, consume):
+    """D2H of a device byte buffer through the pinned staging buffer; the
+    bytes are handed to `consume(memoryview)` while the staging is held."""
+    import torch
+
+    n = int(d_out.numel())
+    with _staging_lock:
+        host = _staging_buffer(max(n, 1))
+        if n:
+            torch.from_numpy(host[:n]).copy_(d_out, non_blocking=True)
+            torch.cuda.current_stream(d_out.device.index).synchronize()
+        return consume(memoryview(host)[:n])
+
+
+def format_dataset_to_device(values, fmt: str = "csv", header_lines=(), labels=None, events=None):
+    """format_dataset's bytes as a CUDA uint8 tensor (no host copy)."""
     import torch
 
     if fmt not in FORMATS:
@@ -258,17 +346,11 @@ def format_dataset_device(values, fmt: str = "csv", header_lines=(), labels=None
     out = torch.empty(total.value, dtype=torch.uint8, device=values.device)
     if head:
         out[:len(head)].copy_(torch.frombuffer(bytearray(head), dtype=torch.uint8))
-    _native.check(L.sa_dataset_format_write(_vp(values.data_ptr()), n, length, _FMT_CODE[fmt],
-                                            _vp(d_lab.data_ptr()) if d_lab is not None else None,
-                                            _vp(d_off.data_ptr()) if d_off is not None else None,
-                                            _vp(row_off.data_ptr()), _vp(out.data_ptr()), stream),
-                  "sa_dataset_format_write")
-    from .memory import pinned_empty
-
-    host = pinned_empty((total.value,), np.uint8)
-    torch.from_numpy(host).copy_(out, non_blocking=True)
-    torch.cuda.current_stream(dev).synchronize()
-    return host.tobytes()
+    _native.check(_timed(events, lambda: L.sa_dataset_format_write(
+        _vp(values.data_ptr()), n, length, _FMT_CODE[fmt], _vp(d_lab.data_ptr()) if d_lab is not None else None,
+        _vp(d_off.data_ptr()) if d_off is not None else None, _vp(row_off.data_ptr()), _vp(out.data_ptr()),
+        stream)), "sa_dataset_format_write")
+    return out
 
 
 def format_dataset(ds: DatasetFile) -> str:
@@ -278,7 +360,8 @@ def format_dataset(ds: DatasetFile) -> str:
     dev = _native.current_device()
     values = torch.from_numpy(np.ascontiguousarray(ds.batch.values)).to(f"cuda:{dev}")
     labels = ds.labels
-    return format_dataset_device(values, ds.format, ds.header_lines, labels).decode("utf-8", "surrogatepass")
+    out = format_dataset_to_device(values, ds.format, ds.header_lines, labels)
+    return _fetch(out, lambda mv: str(mv, "utf-8", "surrogatepass"))
 
 
 def write_dataset(path, ds: DatasetFile) -> None:
@@ -287,34 +370,32 @@ def write_dataset(path, ds: DatasetFile) -> None:
 
     dev = _native.current_device()
     values = torch.from_numpy(np.ascontiguousarray(ds.batch.values)).to(f"cuda:{dev}")
-    _write_bytes(path, format_dataset_device(values, ds.format, ds.header_lines, ds.labels), ds)
+    _write_device(path, format_dataset_to_device(values, ds.format, ds.header_lines, ds.labels), ds)
 
 
-def _write_bytes(path, data: bytes, ds_like) -> None:
+def _write_device(path, d_out, ds_like) -> None:
     try:  # the reference's text-mode write fails on unencodable labels/headers
         for s in tuple(ds_like.header_lines) + tuple(ds_like.labels or ()):
             s.encode("utf-8")
     except UnicodeEncodeError:
+        text = _fetch(d_out, lambda mv: str(mv, "utf-8", "surrogatepass"))
         with open(path, "w", encoding="utf-8") as fh:
-            fh.write(data.decode("utf-8", "surrogatepass"))
+            fh.write(text)
         return
-    with open(path, "wb") as fh:
-        fh.write(data)
+
+    def write(mv):
+        with open(path, "wb") as fh:
+            fh.write(mv)
+
+    _fetch(d_out, write)
 
 
 def augment_file(src, dst, pipeline, fmt: Optional[str] = None) -> DeviceDataset:
     """The reference's `seriesaug augment` data path (cli.py:48-54) with the
     batch resident in HBM: read -> parse -> pipeline -> format -> write, one
     H2D of the input text and one D2H of the output text."""
-    from .memory import pinned_empty
-
-    with open(src, "rb") as fh:
-        size = fh.seek(0, 2)
-        fh.seek(0)
-        host = pinned_empty((max(size, 1),), np.uint8)
-        got = fh.readinto(memoryview(host)[:size]) if size else 0
     try:
-        dd = parse_dataset_device(memoryview(host)[:got], fmt)
+        dd = _read_device(src, fmt)
     except InvalidInputError as exc:
         raise InvalidInputError(f"{src}: {exc}") from None
     out = pipeline.run_device(dd.values)
@@ -323,5 +404,5 @@ def augment_file(src, dst, pipeline, fmt: Optional[str] = None) -> DeviceDataset
         r = out.shape[0] // dd.values.shape[0]
         labels = tuple(lab for lab in labels for _ in range(r))
     res = DeviceDataset(values=out, format=dd.format, header_lines=dd.header_lines, labels=labels)
-    _write_bytes(dst, format_dataset_device(out, dd.format, dd.header_lines, labels), res)
+    _write_device(dst, format_dataset_to_device(out, dd.format, dd.header_lines, labels), res)
     return res
