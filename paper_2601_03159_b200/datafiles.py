@@ -245,8 +245,8 @@ def _read_device(path, fmt) -> DeviceDataset:
     """File -> pinned staging (one read) -> HBM -> device parse."""
     import torch
 
-    dev = _native.current_device()
-    with open(path, "rb") as fh:
+    with open(path, "rb") as fh:  # I/O errors first, as the reference's open()
+        dev = _native.current_device()
         size = fh.seek(0, 2)
         fh.seek(0)
         with _staging_lock:
