@@ -100,8 +100,11 @@ __device__ __forceinline__ void stockham_pass(const double2* __restrict__ src, d
     for (int j = lane; j < Q; j += 32) {
         const int k = j & (Ns - 1);
         double2 v[R];
+        // the swizzle term of j + rQ is the same for every r (fft_any only
+        // swizzles when Q is a multiple of R_prev^2), so it is applied once
+        const double2* sj = src + sin(j);
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[r] = src[sin(j + r * Q)];
+        for (int r = 0; r < R; ++r) v[r] = sj[r * Q];
         if (Ns > 1) {
             double2 w1 = __ldg(&tw[k * tstep]);
             if (INV) w1.y = -w1.y;
@@ -128,8 +131,11 @@ __device__ __forceinline__ void stockham_pass(const double2* __restrict__ src, d
         if (R == 4) dft4<INV>(v);
         if (R == 8) dft8<INV>(v);
         const int base = ((j >> lns) << (lns + (R == 8 ? 3 : (R == 4 ? 2 : 1)))) + k;
+        // output swizzle only on pass 0 (Ns == 1, base a multiple of R): one
+        // XOR term for the whole butterfly
+        const int xo = (base >> sout.sh) & sout.mask;
 #pragma unroll
-        for (int r = 0; r < R; ++r) dst[sout(base + r * Ns)] = v[r];
+        for (int r = 0; r < R; ++r) dst[(base + r * Ns) ^ xo] = v[r];
     }
     __syncwarp();
 }
@@ -201,7 +207,8 @@ __device__ __forceinline__ double2* fft_any(double2* a, double2* b, const FftGeo
             const int lr = (R == 8 ? 3 : (R == 4 ? 2 : 1));
             const int tstep = L >> (lns + lr);  // L / (Ns R)
             // swizzle pass 0's output when pass 1 is a power-of-two pass too
-            const bool swz = (p == 0 && R > 2 && g.npass > 1 && (g.radix[1] & (g.radix[1] - 1)) == 0);
+            const bool swz = (p == 0 && R > 2 && g.npass > 1 && (g.radix[1] & (g.radix[1] - 1)) == 0 &&
+                              (g.N / g.radix[1]) % (R * R) == 0);
             const Swz out = swz ? Swz{lr, R - 1} : Swz{0, 0};
             if (R == 8) stockham_pass<8, false>(src, dst, g.N, lns, tw, tstep, lane, carry, out);
             else if (R == 4) stockham_pass<4, false>(src, dst, g.N, lns, tw, tstep, lane, carry, out);

@@ -771,19 +771,44 @@ __device__ __forceinline__ bool op_pool(const DevStage& st, double*& cur, int L,
     return false;
 }
 
-// BASELINE M4 Convolve (taps in params.aux)
+// BASELINE M4 Convolve (taps in params.aux).  Each lane computes two
+// outputs (t, t + 32) as independent chains; chunks whose taps stay inside
+// the series skip the edge clamp.  Per output the taps are summed in order
+// k = 0..S-1 exactly as before.
 __device__ __forceinline__ bool op_convolve(const DevStage& st, const double* aux, double*& cur, double*& oth, int L, Warp& w, bool& bad) {
     const double* taps = aux + st.aux_off;
     const int S = st.aux_len, h = S / 2;
-    for (int t = w.lane; t < L; t += 32) {
-        double acc = 0.0;
-        for (int k = 0; k < S; ++k) {
-            int u = t + k - h;
-            u = u < 0 ? 0 : (u > L - 1 ? L - 1 : u);
-            acc = acc + taps[k] * cur[u];
+    const int t_hi = L - S + h;  // outputs t in [h, t_hi] read only cur[0 .. L-1]
+    for (int t0 = 0; t0 < L; t0 += 64) {
+        const int ta = t0 + w.lane, tb = ta + 32;
+        double a0 = 0.0, a1 = 0.0;
+        if (t0 >= h && t0 + 63 <= t_hi) {  // warp-uniform interior chunk
+            const double* pa = cur + ta - h;
+            const double* pb = cur + tb - h;
+            for (int k = 0; k < S; ++k) {
+                const double c = taps[k];
+                a0 = a0 + c * pa[k];
+                a1 = a1 + c * pb[k];
+            }
+        } else {
+            for (int k = 0; k < S; ++k) {
+                const double c = taps[k];
+                int u = ta + k - h;
+                u = u < 0 ? 0 : (u > L - 1 ? L - 1 : u);
+                int v = tb + k - h;
+                v = v < 0 ? 0 : (v > L - 1 ? L - 1 : v);
+                a0 = a0 + c * cur[u];
+                a1 = a1 + c * cur[v];
+            }
         }
-        oth[t] = acc;
-        bad |= nonfinite(acc);
+        if (ta < L) {
+            oth[ta] = a0;
+            bad |= nonfinite(a0);
+        }
+        if (tb < L) {
+            oth[tb] = a1;
+            bad |= nonfinite(a1);
+        }
     }
     __syncwarp();
     swapbuf(cur, oth);
@@ -818,24 +843,20 @@ __device__ __forceinline__ bool op_speed_warp(const DevStage& st, WStream& s, do
     int* sbt = reinterpret_cast<int*>(w.iscr);  // segment starts sb[m], m <= K
     for (int m = w.lane; m <= K; m += 32) sbt[m] = (int)(((int64_t)m * L + K) / segs);
     __syncwarp();
-    int sbr[16];  // segment starts in registers (K < 16); smem table otherwise
-#pragma unroll
-    for (int q = 0; q < 16; ++q) sbr[q] = q <= K ? sbt[q] : 0x7fffffff;
-    auto tau_raw = [&](int t) {
-        int m = 0;  // floor(t * segs / L) == #{q in 1..K : sb[q] <= t}
-        if (K < 16) {
-#pragma unroll
-            for (int q = 1; q < 16; ++q) m += (t >= sbr[q]) ? 1 : 0;
-        } else {
-            for (int q = 1; q <= K; ++q) m += (t >= sbt[q]) ? 1 : 0;
-        }
-        return base[m] + speeds[m] * (double)(t - sbt[m]);
+    // segment of t: m = #{q in 1..K : sb[q] <= t}; a lane's t only grows, so
+    // m is tracked incrementally (usually no step per element)
+    auto seg_of = [&](int t, int m) {
+        while (m < K && t >= sbt[m + 1]) ++m;
+        return m;
     };
-    const double f = ((double)L - 1.0) / tau_raw(L - 1);
+    auto tau_at = [&](int t, int m) { return base[m] + speeds[m] * (double)(t - sbt[m]); };
+    const double f = ((double)L - 1.0) / tau_at(L - 1, seg_of(L - 1, 0));
     const bool cubic = st.i[1] != 0;
+    int m = 0;
 #pragma unroll 2
     for (int t = w.lane; t < L; t += 32) {
-        const double tau = (t == L - 1) ? (double)L - 1.0 : tau_raw(t) * f;
+        m = seg_of(t, m);
+        const double tau = (t == L - 1) ? (double)L - 1.0 : tau_at(t, m) * f;
         int j = (int)floor(tau);
         j = j < 0 ? 0 : (j > L - 2 ? L - 2 : j);
         const double fr = tau - (double)j;
