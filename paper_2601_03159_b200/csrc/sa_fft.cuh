@@ -111,15 +111,15 @@ __device__ __forceinline__ void stockham_pass(const double2* __restrict__ src, d
             if (R == 2) {
                 v[1] = cmul(v[1], w1);
             } else {
-                double2 w2 = __ldg(&tw[2 * k * tstep]);
-                if (INV) w2.y = -w2.y;
+                // one table load per butterfly: W^2k and W^4k by squaring
+                // (the table sits in L2 -- shared memory holds the series)
+                const double2 w2 = cmul(w1, w1);
                 const double2 w3 = cmul(w1, w2);
                 v[1] = cmul(v[1], w1);
                 v[2] = cmul(v[2], w2);
                 v[3] = cmul(v[3], w3);
                 if (R == 8) {
-                    double2 w4 = __ldg(&tw[4 * k * tstep]);
-                    if (INV) w4.y = -w4.y;
+                    const double2 w4 = cmul(w2, w2);
                     v[4] = cmul(v[4], w4);
                     v[5] = cmul(v[5], cmul(w1, w4));
                     v[6] = cmul(v[6], cmul(w2, w4));
@@ -151,43 +151,43 @@ struct FftGeo {
 };
 
 // Generic radix-R Stockham pass (any R | N): each output is the direct sum
-// V[u] = sum_r src[j + rQ] * W_N^(r*k*N/(Ns R) + (r*u mod R)*N/R).  The
-// exponents advance by steps < N, so a conditional subtraction keeps them
-// reduced (no integer division in the inner loop); two outputs of the same
-// input column are accumulated together (shared loads, two FMA chains).
+// V[u] = sum_r src[j + rQ] * W_N^(r * (k*N/(Ns R) + u*N/R)), a geometric
+// progression in r: one table load for its ratio, then one complex multiply
+// per term (rounding grows ~R ulp, far inside the FFT tolerance) instead of
+// a table load per term.  Four outputs u0 + {0,1,2,3}*q of the same input
+// column are accumulated together (shared loads, four independent chains).
 __device__ __forceinline__ void generic_pass(const double2* __restrict__ src, double2* __restrict__ dst, int N, int Ns,
                                              int R, const double2* __restrict__ tw, int L, int lane) {
     const int Q = N / R;
     const int ts = L / N;               // table stride for W_N
     const int a = N / (Ns * R), b = N / R;
-    const int half = (R + 1) / 2;       // outputs u and u + half share the column j
-    for (int idx = lane; idx < Q * half; idx += 32) {
-        const int j = idx % Q, u0 = idx / Q, u1 = u0 + half;
-        const bool two = u1 < R;
+    const int q = (R + 3) / 4;          // outputs u0 + c*q, c < 4, share the column j
+    for (int idx = lane; idx < Q * q; idx += 32) {
+        const int j = idx % Q, u0 = idx / Q;
         const int k = j % Ns;
         const int ka = k * a;            // < N
-        const int s0 = u0 * b, s1 = two ? u1 * b : 0;  // < N
-        double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
-        int e1 = 0, e20 = 0, e21 = 0;    // r*k*a mod N, (r*u mod R)*b
+        double2 t[4], st[4], acc[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int u = u0 + c * q;
+            int e = ka + (u < R ? u : 0) * b;  // both terms < N
+            e = e >= N ? e - N : e;
+            st[c] = __ldg(&tw[e * ts]);
+            t[c] = make_double2(1.0, 0.0);
+            acc[c] = make_double2(0.0, 0.0);
+        }
         for (int r = 0; r < R; ++r) {
             const double2 v = src[j + r * Q];
-            int e = e1 + e20;
-            e = e >= N ? e - N : e;
-            acc0 = cadd(acc0, cmul(v, __ldg(&tw[e * ts])));
-            if (two) {
-                int f = e1 + e21;
-                f = f >= N ? f - N : f;
-                acc1 = cadd(acc1, cmul(v, __ldg(&tw[f * ts])));
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                acc[c] = cadd(acc[c], cmul(v, t[c]));
+                t[c] = cmul(t[c], st[c]);
             }
-            e1 += ka;
-            e1 = e1 >= N ? e1 - N : e1;
-            e20 += s0;
-            e20 = e20 >= N ? e20 - N : e20;
-            e21 += s1;
-            e21 = e21 >= N ? e21 - N : e21;
         }
-        dst[(j - k) * R + k + u0 * Ns] = acc0;
-        if (two) dst[(j - k) * R + k + u1 * Ns] = acc1;
+        const int o = (j - k) * R + k;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            if (u0 + c * q < R) dst[o + (u0 + c * q) * Ns] = acc[c];
     }
     __syncwarp();
 }
