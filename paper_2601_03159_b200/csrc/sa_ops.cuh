@@ -897,8 +897,10 @@ __device__ __forceinline__ void perturb_spectrum(const DevStage& st, WStream& s,
         const bool even = (L % 2 == 0);
         const int hi = even ? bins - 1 : bins;
         double* ph = scratch + bins;  // scratch holds >= 2 * bins doubles
-        normals(s, w.lane, bins, w.zig, [&](int k, double z) { amp[k] = 0.0 + sa * z; });
-        normals(s, w.lane, bins, w.zig, [&](int k, double z) { ph[k] = 0.0 + sp * z; });
+        // `bins` magnitude normals then `bins` phase normals (freqaugment.py:
+        // 113-114): consecutive draws of one stream, taken in one walk;
+        // ph = amp + bins, so draw k lands at scratch[k] scaled by its sigma
+        normals(s, w.lane, 2 * bins, w.zig, [&](int k, double z) { amp[k] = 0.0 + (k < bins ? sa : sp) * z; });
         __syncwarp();
         // r' = max(|X| + amp, 0) at angle atan2(im, re) + ph (freqaugment.py:
         // 117-122), evaluated as a rotation of X by ph scaled by r'/|X|: the
