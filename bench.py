@@ -413,6 +413,34 @@ def ds_cpu_baseline(data: bytes, n: int, target_rows: int = 3000):
             "parse_bps": nbytes / (t1 - t0), "format_bps": nbytes / (t2 - t1)}
 
 
+def run_side_reference(args, rank):
+    """--impl reference for the transforms / dtw legs: the CPU path alone."""
+    if rank != 0:
+        return
+    from bench_inputs import ar2_input, host_input
+
+    if args.workload == "transforms":
+        host = ar2_input(4000, TR_SHAPE[1])
+        for _ in range(args.warmup):
+            transforms_cpu(host, rows=500)
+        base = [transforms_cpu(host) for _ in range(args.steps)]
+        metric, unit, wl = "transformed points/s", "points/s", TR_WORKLOAD
+    else:
+        a = host_input(2, 64)
+        b = a[:, ::-1].copy()
+        for _ in range(args.warmup):
+            dtw_cpu(a, b, pairs=8)
+        base = [dtw_cpu(a, b) for _ in range(args.steps)]
+        metric, unit, wl = "DTW cells/s", "cells/s", DTW_WORKLOAD
+    v = sum(x["value"] for x in base) / len(base)
+    print(json.dumps({
+        "impl": "reference", "metric": metric, "value": v, "unit": unit, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "replicas",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": {"workload": wl},
+        "cpu_baseline": dict(base[-1], value=v),
+        "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}), flush=True)
+
+
 def run_datafiles_reference(args, rank):
     """The reference algorithm on the host (oracle port), bounded sample."""
     if rank != 0:
@@ -529,6 +557,210 @@ def run_datafiles(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+TR_SHAPE = (50_000, 2048)
+TR_WORKLOAD = ("transforms: fft_forward + fft_inverse + dct_forward + dct_inverse (orthonormal) on 50,000 x 2,048 "
+               "AR(2) series (config 3 shape), device resident")
+
+
+def _timed_steps(fn, steps, warmup, stream=None):
+    import torch
+
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    with Clocks(0) as clk:
+        ev[0].record()
+        for k in range(steps):
+            fn()
+            ev[k + 1].record()
+        torch.cuda.synchronize()
+    per = [ev[k].elapsed_time(ev[k + 1]) for k in range(steps)]
+    return sum(per) / steps, clk.summary()
+
+
+def run_transforms(args, rank):
+    """One step = rfft + irfft + DCT-II + DCT-III of the whole batch
+    (freqtransform.py:91-116) through the C ABI on resident buffers."""
+    import ctypes
+
+    import torch
+
+    from bench_inputs import ar2_input
+    from paper_2601_03159_b200 import Batch, _native, dct_forward, dct_inverse, fft_forward, fft_inverse
+
+    if rank != 0:
+        return
+    torch.cuda.set_device(0)
+    _native.ensure_device(0)
+    n, L = TR_SHAPE
+    if args.n_series:
+        n = args.n_series
+    host = ar2_input(n, L)
+    x = torch.from_numpy(host).cuda()
+    B = L // 2 + 1
+    re = torch.empty((n, B), dtype=torch.float64, device="cuda")
+    im = torch.empty_like(re)
+    back = torch.empty_like(x)
+    dc = torch.empty_like(x)
+    idc = torch.empty_like(x)
+    lib = _native.lib()
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    launches0 = _native.launch_count()
+
+    def step():
+        _native.check(lib.sa_fft_forward(x.data_ptr(), n, L, re.data_ptr(), im.data_ptr(), st))
+        _native.check(lib.sa_fft_inverse(re.data_ptr(), im.data_ptr(), n, L, back.data_ptr(), st))
+        _native.check(lib.sa_dct_forward(x.data_ptr(), n, L, dc.data_ptr(), st))
+        _native.check(lib.sa_dct_inverse(dc.data_ptr(), n, L, idc.data_ptr(), st))
+
+    ms, clocks = _timed_steps(step, args.steps, args.warmup)
+    launches = (_native.launch_count() - launches0) // (args.steps + args.warmup) * args.steps
+    err = max(float((back - x).abs().max()), float((idc - x).abs().max()))
+    if err > 1e-8 * max(1.0, float(x.abs().max())):
+        raise RuntimeError(f"transform round trip error {err}")
+    pts = 4 * n * L
+    byts = 8 * n * (L + 2 * B) * 2 + 8 * n * L * 4  # rfft/irfft: L + 2B each; dct/idct: 2L each
+    # e2e through the public API (host Batch in, host arrays out)
+    b = Batch(host)
+    spec = fft_forward(b)  # warm-up: staging buffers
+    fft_inverse(spec)
+    dct_inverse(dct_forward(b))
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        spec = fft_forward(b)
+        fft_inverse(spec)
+        dct_inverse(dct_forward(b))
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    peak, src = measured_peak()
+    ach = byts / (ms / 1e3) / 1e9
+    line = {
+        "metric": "transformed points/s", "value": pts / (ms / 1e3), "unit": "points/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "replicas", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded AR(2), BASELINE config 3 distribution)",
+        "config": {"workload": TR_WORKLOAD, "n_series": n, "len": L, "round_trip_max_err": err,
+                   "l2": "inputs larger than L2 (no flush needed)"},
+        "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                     "traffic": None, "peak_source": src, "algorithmic_bytes_per_step": byts,
+                     "scope": "rfft_kernel + irfft_kernel + 2 x dct_kernel"},
+        "e2e": {"value": pts / e2e_s, "unit": "points/s", "h2d_bytes_per_step": 8 * n * L * 3 + 16 * n * B,
+                "d2h_bytes_per_step": 8 * n * L * 3 + 16 * n * B},
+        "gpu_launches": int(launches), "clocks": clocks,
+    }
+    if not args.no_cpu:
+        line["cpu_baseline"] = transforms_cpu(host)
+    print(json.dumps(line), flush=True)
+
+
+def transforms_cpu(host, rows=4000):
+    """The reference's own CPU path: numpy.fft.rfft/irfft and scipy.fft.dct/
+    idct (freqtransform.py:93-116), one core as the reference calls them."""
+    import scipy.fft
+
+    x = host[:rows]
+    L = x.shape[1]
+    t0 = time.perf_counter()
+    spec = np.fft.rfft(x, axis=1)
+    np.fft.irfft(spec, n=L, axis=1)
+    c = scipy.fft.dct(x, type=2, norm="ortho", axis=1)
+    scipy.fft.idct(c, type=2, norm="ortho", axis=1)
+    dt = time.perf_counter() - t0
+    return {"value": 4 * x.size / dt, "unit": "points/s", "cores": 1, "kind": "reference",
+            "sample": f"{rows} of {host.shape[0]} series through numpy/scipy pocketfft ({dt:.2f} s)"}
+
+
+DTW_SHAPE = (10_000, 1024)
+DTW_WORKLOAD = ("dtw: DTW distance of 10,000 (original, augmented) pairs of length 1,024 (config 2 walks vs their "
+                "config-2-pipeline output at full length), one launch")
+
+
+def run_dtw(args, rank):
+    """One step = the DTW distance of every pair (the `quality` command's
+    work, dtw.py:40-86) in one batched launch."""
+    import ctypes
+
+    import torch
+
+    from bench_inputs import host_input
+    from paper_2601_03159_b200 import (Batch, Drift, Jitter, Pipeline, Quantize, Reverse, _native,
+                                       dtw_distances)
+
+    if rank != 0:
+        return
+    torch.cuda.set_device(0)
+    _native.ensure_device(0)
+    n, L = DTW_SHAPE
+    if args.n_series:
+        n = args.n_series
+    a_host = host_input(2, n)
+    pipe = Pipeline(stages=(Jitter(0.1), Drift(0.5, 5, probability=0.5), Quantize(16, probability=0.5),
+                            Reverse(probability=0.5)), master_seed=1)
+    b_host = pipe.run(Batch(a_host)).values
+    a, b = torch.from_numpy(a_host).cuda(), torch.from_numpy(b_host).cuda()
+    dist = torch.empty(n, dtype=torch.float64, device="cuda")
+    lib = _native.lib()
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    launches0 = _native.launch_count()
+
+    def step():
+        _native.check(lib.sa_dtw_batch(a.data_ptr(), b.data_ptr(), n, L, L, dist.data_ptr(), st))
+
+    ms, clocks = _timed_steps(step, args.steps, args.warmup)
+    launches = (_native.launch_count() - launches0) // (args.steps + args.warmup) * args.steps
+    # spot check against the oracle (bitwise: one addition per cell)
+    from oracle import oracle as O
+
+    got = dist.cpu().numpy()
+    for i in (0, n // 2, n - 1):
+        if O.dtw(a_host[i], b_host[i])[0] != got[i]:
+            raise RuntimeError("DTW distance differs from the oracle")
+    cells = n * L * L
+    ba, bb = Batch(a_host), Batch(b_host)
+    dtw_distances(ba, bb)  # warm-up: staging buffers
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        dtw_distances(ba, bb)
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    peak, src = measured_peak()
+    byts = 8 * n * 2 * L + 8 * n
+    ach = byts / (ms / 1e3) / 1e9
+    line = {
+        "metric": "DTW cells/s", "value": cells / (ms / 1e3), "unit": "cells/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "replicas",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded walks and their augmented copies)",
+        "config": {"workload": DTW_WORKLOAD, "pairs": n, "len_a": L, "len_b": L,
+                   "l2": "inputs smaller than L2: compute bound, L2 residency irrelevant"},
+        "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                     "traffic": None, "peak_source": src, "algorithmic_bytes_per_step": byts,
+                     "scope": "dtw_batch_kernel (an O(L^2) dynamic programme per pair: issue bound, not HBM)"},
+        "e2e": {"value": cells / e2e_s, "unit": "cells/s", "h2d_bytes_per_step": 16 * n * L,
+                "d2h_bytes_per_step": 8 * n},
+        "gpu_launches": int(launches), "clocks": clocks,
+    }
+    if not args.no_cpu:
+        line["cpu_baseline"] = dtw_cpu(a_host, b_host)
+    print(json.dumps(line), flush=True)
+
+
+def dtw_cpu(a, b, pairs=None):
+    """The reference algorithm restated in C (oracle sao_dtw), all host
+    threads over a sample of pairs."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle as O
+
+    threads = os.cpu_count() or 1
+    pairs = pairs or 32 * threads
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(lambda i: O.dtw(a[i], b[i]), range(pairs)))
+    dt = time.perf_counter() - t0
+    cells = pairs * a.shape[1] * b.shape[1]
+    return {"value": cells / dt, "unit": "cells/s", "cores": threads, "kind": "port",
+            "sample": f"{pairs} pairs through the C oracle ({dt:.2f} s)"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -540,10 +772,18 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--suite", action="store_true", help="configs 1-5 + sweep, device-resident, one JSON")
-    ap.add_argument("--workload", default="pipeline", choices=["pipeline", "datafiles"],
-                    help="datafiles: the dataset parse/format codec (SURVEY.md §8(f) next-3)")
+    ap.add_argument("--workload", default="pipeline", choices=["pipeline", "datafiles", "transforms", "dtw"],
+                    help="datafiles / transforms / dtw: the SURVEY.md §8(f) next rows")
     args = ap.parse_args()
     rank, world, local_rank = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    if args.workload in ("transforms", "dtw"):
+        if args.impl == "reference":
+            run_side_reference(args, rank)
+        elif args.workload == "transforms":
+            run_transforms(args, rank)
+        else:
+            run_dtw(args, rank)
+        return
     if args.workload == "datafiles":
         if args.impl == "reference":
             run_datafiles_reference(args, rank)

@@ -172,6 +172,18 @@ int sa_dtw_batch(const double* d_a, const double* d_b, int64_t n_pairs, int64_t 
 int sa_dtw_path(const double* d_a, int64_t len_a, const double* d_b, int64_t len_b, double* d_acc,
                 int32_t* d_path, int32_t* d_path_len, double* d_dist, void* stream);
 
+/* ---- host-buffer transforms (freqtransform.py / dtw.py on numpy arrays) --
+ * The reference API's arrays live in ordinary host memory.  These run the
+ * device entry points above through the host-staging runtime (chunks of rows,
+ * parallel copies into page-locked staging overlapped with H2D, kernel and
+ * D2H; page-locked buffers are used in place).  Synchronous. */
+int sa_fft_forward_host(const double* h_in, int64_t n, int64_t len, double* h_re, double* h_im);
+int sa_fft_inverse_host(const double* h_re, const double* h_im, int64_t n, int64_t len, double* h_out);
+int sa_dct_forward_host(const double* h_in, int64_t n, int64_t len, double* h_out);
+int sa_dct_inverse_host(const double* h_in, int64_t n, int64_t len, double* h_out);
+int sa_dtw_batch_host(const double* h_a, const double* h_b, int64_t n_pairs, int64_t len_a, int64_t len_b,
+                      double* h_dist);
+
 /* ---- text codec (dataset files, reference datafiles.py) ----------------
  * repr(float(v)) of each value into a 32-byte slot of d_out (length in
  * d_len), bit-exact with CPython's shortest round-trip repr. Async. */

@@ -103,30 +103,26 @@ def launch_device(stages, values, out, flags, seed: int, series_offset: int = 0,
 
 
 def fft_forward_host(values: np.ndarray):
-    import torch
-
-    dev = _native.current_device()
-    x = torch.from_numpy(np.ascontiguousarray(values)).to(f"cuda:{dev}")
+    """rfft of each row: host arrays through sa_fft_forward_host (staged)."""
+    x = np.ascontiguousarray(values, dtype=np.float64)
     n, L = x.shape
+    _native.current_device()
     bins = L // 2 + 1
-    re = torch.empty((n, bins), dtype=torch.float64, device=x.device)
-    im = torch.empty_like(re)
-    st = torch.cuda.current_stream().cuda_stream
-    _native.check(_native.lib().sa_fft_forward(x.data_ptr(), n, L, re.data_ptr(), im.data_ptr(), st))
-    return re.cpu().numpy(), im.cpu().numpy()
+    re = np.empty((n, bins), dtype=np.float64)
+    im = np.empty((n, bins), dtype=np.float64)
+    _native.check(_native.lib().sa_fft_forward_host(_ptr(x), n, L, _ptr(re), _ptr(im)), "sa_fft_forward_host")
+    return re, im
 
 
 def fft_inverse_host(re: np.ndarray, im: np.ndarray, L: int) -> np.ndarray:
-    import torch
-
-    dev = _native.current_device()
-    tre = torch.from_numpy(np.ascontiguousarray(re)).to(f"cuda:{dev}")
-    tim = torch.from_numpy(np.ascontiguousarray(im)).to(f"cuda:{dev}")
-    n = tre.shape[0]
-    out = torch.empty((n, L), dtype=torch.float64, device=tre.device)
-    st = torch.cuda.current_stream().cuda_stream
-    _native.check(_native.lib().sa_fft_inverse(tre.data_ptr(), tim.data_ptr(), n, L, out.data_ptr(), st))
-    return out.cpu().numpy()
+    """irfft(n=L) of each half spectrum (sa_fft_inverse_host)."""
+    re = np.ascontiguousarray(re, dtype=np.float64)
+    im = np.ascontiguousarray(im, dtype=np.float64)
+    _native.current_device()
+    n = re.shape[0]
+    out = np.empty((n, L), dtype=np.float64)
+    _native.check(_native.lib().sa_fft_inverse_host(_ptr(re), _ptr(im), n, L, _ptr(out)), "sa_fft_inverse_host")
+    return out
 
 
 def augment_spectrum_host(stage, seed: int, re: np.ndarray, im: np.ndarray, L: int):
@@ -146,14 +142,11 @@ def augment_spectrum_host(stage, seed: int, re: np.ndarray, im: np.ndarray, L: i
 
 
 def dct_host(values: np.ndarray, inverse: bool) -> np.ndarray:
-    """Orthonormal DCT-II (inverse: DCT-III) of each row on the device."""
-    import torch
-
-    dev = _native.current_device()
-    x = torch.from_numpy(np.ascontiguousarray(values, dtype=np.float64)).to(f"cuda:{dev}")
+    """Orthonormal DCT-II (inverse: DCT-III) of each row (sa_dct_*_host)."""
+    x = np.ascontiguousarray(values, dtype=np.float64)
     n, L = x.shape
-    out = torch.empty_like(x)
-    st = torch.cuda.current_stream().cuda_stream
-    fn = _native.lib().sa_dct_inverse if inverse else _native.lib().sa_dct_forward
-    _native.check(fn(x.data_ptr(), n, L, out.data_ptr(), st))
-    return out.cpu().numpy()
+    _native.current_device()
+    out = np.empty_like(x)
+    fn = _native.lib().sa_dct_inverse_host if inverse else _native.lib().sa_dct_forward_host
+    _native.check(fn(_ptr(x), n, L, _ptr(out)), "sa_dct_host")
+    return out

@@ -61,6 +61,11 @@ def lib() -> ctypes.CDLL:
         L.sa_dtw_batch.argtypes = [_vp, _vp, _i64, _i64, _i64, _vp, _vp]
         L.sa_dtw_path.argtypes = [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp]
         L.sa_augment_spectrum.argtypes = [_stp, _u64, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _vp]
+        L.sa_fft_forward_host.argtypes = [_vp, _i64, _i64, _vp, _vp]
+        L.sa_fft_inverse_host.argtypes = [_vp, _vp, _i64, _i64, _vp]
+        L.sa_dct_forward_host.argtypes = [_vp, _i64, _i64, _vp]
+        L.sa_dct_inverse_host.argtypes = [_vp, _i64, _i64, _vp]
+        L.sa_dtw_batch_host.argtypes = [_vp, _vp, _i64, _i64, _i64, _vp]
         L.sa_repr_values.argtypes = [_vp, _i64, _vp, _vp, _vp]
         L.sa_parse_values.argtypes = [_vp, _vp, _i64, _vp, _vp, _vp, _vp]
         _infop = ctypes.POINTER(_abi.SaDatasetInfo)
@@ -78,7 +83,8 @@ def lib() -> ctypes.CDLL:
                    "sa_augment_spectrum", "sa_host_alloc", "sa_host_free", "sa_dct_forward",
                    "sa_dct_inverse", "sa_dtw_batch", "sa_dtw_path", "sa_repr_values", "sa_parse_values", "sa_dataset_open",
                    "sa_dataset_values", "sa_dataset_labels", "sa_dataset_headers", "sa_dataset_close",
-                   "sa_dataset_format_size", "sa_dataset_format_write"):
+                   "sa_dataset_format_size", "sa_dataset_format_write", "sa_fft_forward_host", "sa_fft_inverse_host",
+                   "sa_dct_forward_host", "sa_dct_inverse_host", "sa_dtw_batch_host"):
             getattr(L, fn).restype = ctypes.c_int
         if L.sa_abi_version() != _abi.SA_ABI_VERSION:
             raise UnsupportedPlatformError("backend library ABI version mismatch")

@@ -15,35 +15,46 @@
 namespace sa {
 
 // Returns acc[n-1][m-1]; if acc != nullptr every cell is also stored
-// (row-major n x m) for the path backtrack.  `prow` is smem of >= m doubles.
+// (row-major n x m) for the path backtrack.  `prow` is smem of >= m doubles
+// (the previous strip's last row), >= 2 m with stage_b (then a copy of b).
+//
+// Boundary cells use +inf for missing neighbours, so every cell is
+// c + min(diag, up, left) (the first cell: c + 0); min selects one of the
+// already-final neighbours and the single addition is the reference's, so
+// the values are bitwise dtw.py's.  Within a strip lane 31 writes column
+// t - 31 of prow while lane 0 reads columns t and t - 1: no step-level
+// barrier is needed, only one per strip.
 __device__ double dtw_warp(const double* __restrict__ a, int n, const double* __restrict__ b, int m,
-                           double* prow, double* acc, int lane) {
+                           double* prow, double* acc, int lane, bool stage_b) {
+    const double INF = __longlong_as_double(0x7ff0000000000000ll);
+    const double* bs = b;
+    if (stage_b) {
+        double* cp = prow + m;
+        for (int j = lane; j < m; j += 32) cp[j] = b[j];
+        __syncwarp();
+        bs = cp;
+    }
     double result = 0.0;
     for (int i0 = 0; i0 < n; i0 += 32) {
         const int i = i0 + lane;
         const double ai = i < n ? a[i] : 0.0;
-        double left = 0.0, up = 0.0, diag = 0.0;
+        // lane 0 of the first strip sits on row 0: no row above
+        double left = INF, up = INF, diag = (i == 0) ? 0.0 : INF;
         const int steps = m + 31;
         for (int t = 0; t < steps; ++t) {
             const int j = t - lane;
-            if (lane == 0 && i0 > 0 && j < m) {
-                up = prow[j];
-                diag = j > 0 ? prow[j - 1] : 0.0;
+            const bool jin = (j >= 0) && (j < m);
+            const int jc = jin ? j : 0;
+            if (lane == 0 && i0 > 0 && jin) {
+                up = prow[jc];
+                diag = j > 0 ? prow[jc - 1] : INF;
             }
-            double v = 0.0;
-            const bool live = (j >= 0) && (j < m) && (i < n);
+            const double c = fabs(ai - bs[jc]);
+            const double best = fmin(fmin(diag, up), left);
+            double v = c + best;
+            const bool live = jin && (i < n);
+            v = live ? v : INF;
             if (live) {
-                const double c = fabs(ai - b[j]);
-                if (i == 0) {
-                    v = (j == 0) ? c : left + c;
-                } else if (j == 0) {
-                    v = up + c;
-                } else {
-                    double best = diag;
-                    if (up < best) best = up;
-                    if (left < best) best = left;
-                    v = c + best;
-                }
                 left = v;
                 if (acc) acc[(int64_t)i * m + j] = v;
                 if (i == n - 1 && j == m - 1) result = v;
@@ -51,14 +62,14 @@ __device__ double dtw_warp(const double* __restrict__ a, int n, const double* __
             // lane l+1 needs this cell as its "up" next step; its diagonal is
             // the "up" it used this step
             const double nu = __shfl_up_sync(0xffffffffu, v, 1);
-            __syncwarp();
             if (lane == 31 && live) prow[j] = v;
             if (lane > 0) {
                 diag = up;
                 up = nu;
             }
-            __syncwarp();
+            if (i == 0 && j == 0) diag = INF;  // row 0 after its first cell: no row above
         }
+        __syncwarp();
     }
     // the cell (n-1, m-1) belongs to lane (n-1) % 32
     return __shfl_sync(0xffffffffu, result, (n - 1) & 31);

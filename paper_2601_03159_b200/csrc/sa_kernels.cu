@@ -17,11 +17,14 @@
 
 #include <algorithm>
 #include <cmath>
+#include <condition_variable>
+#include <thread>
 #include <cstdio>
 #include <cstring>
 #include <map>
 #include <mutex>
 #include <string>
+#include <functional>
 #include <vector>
 
 #include "../../include/seriesaug_b200.h"
@@ -373,6 +376,7 @@ struct DtwParams {
     int32_t* path_len;
     int64_t pairs;
     int32_t n, m;
+    int32_t stage_b;  // 1: dtw_warp copies b into shared memory
 };
 
 // one warp per pair: distance only
@@ -380,7 +384,7 @@ __global__ void __launch_bounds__(32) dtw_batch_kernel(const __grid_constant__ D
     extern __shared__ __align__(16) unsigned char smem[];
     double* prow = reinterpret_cast<double*>(smem);
     for (int64_t q = blockIdx.x; q < p.pairs; q += gridDim.x) {
-        const double d = dtw_warp(p.a + q * p.n, p.n, p.b + q * p.m, p.m, prow, nullptr, threadIdx.x);
+        const double d = dtw_warp(p.a + q * p.n, p.n, p.b + q * p.m, p.m, prow, nullptr, threadIdx.x, p.stage_b != 0);
         if (threadIdx.x == 0) p.dist[q] = d;
         __syncwarp();
     }
@@ -390,7 +394,7 @@ __global__ void __launch_bounds__(32) dtw_batch_kernel(const __grid_constant__ D
 __global__ void __launch_bounds__(32) dtw_path_kernel(const __grid_constant__ DtwParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     double* prow = reinterpret_cast<double*>(smem);
-    const double d = dtw_warp(p.a, p.n, p.b, p.m, prow, p.acc, threadIdx.x);
+    const double d = dtw_warp(p.a, p.n, p.b, p.m, prow, p.acc, threadIdx.x, p.stage_b != 0);
     __syncwarp();
     __threadfence_block();
     if (threadIdx.x == 0) {
@@ -495,13 +499,10 @@ struct DeviceState {
     int sms = 0;
     size_t smem_optin = 0;
     std::map<int, double2*> twiddles;  // by length
-    // host-path workspaces (two streams)
-    static constexpr int NS = 3;  // host-path pipeline depth (H2D / kernel / D2H in flight)
+    // host-buffer path (sa_host_stage.inc): slot streams and flag words
+    static constexpr int NS = 3;  // pipeline depth (copy-in / H2D+kernel+D2H / copy-out in flight)
     cudaStream_t hs[NS] = {nullptr, nullptr, nullptr};
-    double* din[NS] = {nullptr, nullptr, nullptr};
-    double* dout[NS] = {nullptr, nullptr, nullptr};
     uint32_t* dflags = nullptr;
-    size_t in_cap = 0, out_cap = 0;
 };
 // Per-device state in a fixed array: lookups never reallocate, so readers
 // need no lock; initialisation and the caches inside are guarded by g_mu,
@@ -922,6 +923,8 @@ int fft_plan_smem(int dev, int64_t L, int* lcap, size_t* smem, int* grid, const 
     return SA_OK;
 }
 
+#include "sa_host_stage.inc"
+
 }  // namespace
 
 // ====================================================================== C ABI
@@ -1001,61 +1004,103 @@ int sa_pipeline_run_host(const sa_stage* stages, int32_t n_stages, const double*
     const int64_t r = plan.p.repeat_r;
     std::lock_guard<std::mutex> lk(g_host_mu[dev < 0 ? 0 : (dev >= kMaxDevices ? kMaxDevices - 1 : dev)]);
     DeviceState& ds = dev_state(dev);
-    // Chunks of ~128 MB of rows, round-robin over NS streams: stream s runs
-    // chunks s, s + NS, ... (H2D -> fused kernel -> D2H), so the two copy
-    // engines and the SMs work on different chunks at the same time.
-    constexpr int NS = DeviceState::NS;
-    const int64_t row_in_b = 8 * len_in, row_out_b = 8 * len_out * r;
-    int64_t chunk = std::max<int64_t>(1, (128ll << 20) / std::max<int64_t>(row_in_b, row_out_b));
-    chunk = std::min<int64_t>(chunk, std::max<int64_t>((n + NS - 1) / NS, 1));
-    size_t need_in = (size_t)(chunk * row_in_b), need_out = (size_t)(chunk * row_out_b);
+    // chunks of rows through the host-staging runtime (sa_host_stage.inc);
+    // each slot accumulates the kernel's status bits in its own flag word
+    const HostIn in{h_in, 8 * len_in};
+    const HostOut out{h_out, 8 * len_out * r};
     if (!ds.hs[0]) {
-        for (int k = 0; k < NS; ++k) SA_CUDA(cudaStreamCreateWithFlags(&ds.hs[k], cudaStreamNonBlocking));
-        SA_CUDA(cudaMalloc(&ds.dflags, NS * sizeof(uint32_t)));
+        rc = ensure_cap(g_host_stage[dev < 0 ? 0 : (dev >= kMaxDevices ? kMaxDevices - 1 : dev)], ds, 0, 0, 0,
+                        false, 0);
+        if (rc) return rc;
     }
-    if (need_in > ds.in_cap || need_out > ds.out_cap) {
-        for (int k = 0; k < NS; ++k) {
-            SA_CUDA(cudaStreamSynchronize(ds.hs[k]));
-            if (ds.din[k]) cudaFree(ds.din[k]);
-            if (ds.dout[k]) cudaFree(ds.dout[k]);
-            ds.din[k] = ds.dout[k] = nullptr;
-        }
-        ds.in_cap = std::max(need_in, ds.in_cap);
-        ds.out_cap = std::max(need_out, ds.out_cap);
-        for (int k = 0; k < NS; ++k) {
-            SA_CUDA(cudaMalloc(&ds.din[k], ds.in_cap));
-            SA_CUDA(cudaMalloc(&ds.dout[k], ds.out_cap));
-        }
-    }
-    uint32_t hflags[NS] = {0, 0, 0};
-    SA_CUDA(cudaMemset(ds.dflags, 0, NS * sizeof(uint32_t)));
-    int c = 0;
-    for (int64_t r0 = 0; r0 < n; r0 += chunk, ++c) {
-        const int64_t rows = std::min(chunk, n - r0);
-        const int k = c % NS;
-        cudaStream_t st = ds.hs[k];
-        SA_CUDA(cudaMemcpyAsync(ds.din[k], h_in + r0 * len_in, (size_t)(rows * row_in_b),
-                                cudaMemcpyHostToDevice, st));
-        Plan pl = plan;
-        pl.p.offset = series_offset + r0;
-        pl.p.rows_out = rows * r;
-        pl.grid = (int)std::max<int64_t>(1, std::min<int64_t>(plan.grid, (pl.p.rows_out + plan.warps - 1) / plan.warps));
-        pl.p.in = ds.din[k];
-        pl.p.out = ds.dout[k];
-        pl.p.flags = ds.dflags + k;
-        pl.p.bulk_in = ((len_in & 1) == 0) ? 1 : 0;
-        {
-            int rc2 = launch_chain(&pl, st);
-            if (rc2) return rc2;
-        }
-        SA_CUDA(cudaMemcpyAsync(h_out + r0 * r * len_out, ds.dout[k], (size_t)(rows * row_out_b),
-                                cudaMemcpyDeviceToHost, st));
-    }
-    for (int k = 0; k < NS; ++k) SA_CUDA(cudaStreamSynchronize(ds.hs[k]));
-    SA_CUDA(cudaMemcpy(hflags, ds.dflags, NS * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    for (int k = 0; k < DeviceState::NS; ++k)  // ordered before each slot's kernels
+        SA_CUDA(cudaMemsetAsync(ds.dflags + k, 0, sizeof(uint32_t), ds.hs[k]));
+    rc = run_rows_host(dev, n, &in, 1, &out, 1,
+                       [&](int k, int64_t r0, int64_t rows, const void* const* d_in, void* const* d_out,
+                           cudaStream_t st) -> int {
+                           Plan pl = plan;
+                           pl.p.offset = series_offset + r0;
+                           pl.p.rows_out = rows * r;
+                           pl.grid = (int)std::max<int64_t>(
+                               1, std::min<int64_t>(plan.grid, (pl.p.rows_out + plan.warps - 1) / plan.warps));
+                           pl.p.in = (const double*)d_in[0];
+                           pl.p.out = (double*)d_out[0];
+                           pl.p.flags = ds.dflags + k;
+                           pl.p.bulk_in = ((len_in & 1) == 0) ? 1 : 0;
+                           return launch_chain(&pl, st);
+                       });
+    if (rc) return rc;
+    uint32_t hflags[DeviceState::NS] = {0, 0, 0};
+    SA_CUDA(cudaMemcpy(hflags, ds.dflags, DeviceState::NS * sizeof(uint32_t), cudaMemcpyDeviceToHost));
     uint32_t f = 0;
-    for (int k = 0; k < NS; ++k) f |= hflags[k];
+    for (int k = 0; k < DeviceState::NS; ++k) f |= hflags[k];
     return flags_status(f);
+}
+
+// Row-wise transforms over host buffers (the reference API's numpy arrays):
+// the host-staging runtime around the device entry points below.
+static int host_rows(int64_t n, const HostIn* ins, int nin, const HostOut* outs, int nout,
+                     const std::function<int(const void* const*, void* const*, int64_t, cudaStream_t)>& fn,
+                     int64_t min_chunk = 1) {
+    int dev;
+    int rc = ensure_device(&dev);
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(g_host_mu[dev < 0 ? 0 : (dev >= kMaxDevices ? kMaxDevices - 1 : dev)]);
+    return run_rows_host(dev, n, ins, nin, outs, nout,
+                         [&](int, int64_t, int64_t rows, const void* const* d_in, void* const* d_out,
+                             cudaStream_t st) -> int { return fn(d_in, d_out, rows, st); },
+                         min_chunk);
+}
+
+int sa_fft_forward_host(const double* h_in, int64_t n, int64_t len, double* h_re, double* h_im) {
+    if (n < 0 || len < 1) return fail(SA_ERR_INVALID_ARG, "bad batch shape");
+    const int64_t bins = len / 2 + 1;
+    const HostIn in{h_in, 8 * len};
+    const HostOut out[2] = {{h_re, 8 * bins}, {h_im, 8 * bins}};
+    return host_rows(n, &in, 1, out, 2, [&](const void* const* di, void* const* dout, int64_t rows, cudaStream_t st) {
+        return sa_fft_forward((const double*)di[0], rows, len, (double*)dout[0], (double*)dout[1], st);
+    });
+}
+
+int sa_fft_inverse_host(const double* h_re, const double* h_im, int64_t n, int64_t len, double* h_out) {
+    if (n < 0 || len < 1) return fail(SA_ERR_INVALID_ARG, "bad batch shape");
+    const int64_t bins = len / 2 + 1;
+    const HostIn in[2] = {{h_re, 8 * bins}, {h_im, 8 * bins}};
+    const HostOut out{h_out, 8 * len};
+    return host_rows(n, in, 2, &out, 1, [&](const void* const* di, void* const* dout, int64_t rows, cudaStream_t st) {
+        return sa_fft_inverse((const double*)di[0], (const double*)di[1], rows, len, (double*)dout[0], st);
+    });
+}
+
+int sa_dct_forward_host(const double* h_in, int64_t n, int64_t len, double* h_out) {
+    if (n < 0 || len < 1) return fail(SA_ERR_INVALID_ARG, "bad batch shape");
+    const HostIn in{h_in, 8 * len};
+    const HostOut out{h_out, 8 * len};
+    return host_rows(n, &in, 1, &out, 1, [&](const void* const* di, void* const* dout, int64_t rows, cudaStream_t st) {
+        return sa_dct_forward((const double*)di[0], rows, len, (double*)dout[0], st);
+    });
+}
+
+int sa_dct_inverse_host(const double* h_in, int64_t n, int64_t len, double* h_out) {
+    if (n < 0 || len < 1) return fail(SA_ERR_INVALID_ARG, "bad batch shape");
+    const HostIn in{h_in, 8 * len};
+    const HostOut out{h_out, 8 * len};
+    return host_rows(n, &in, 1, &out, 1, [&](const void* const* di, void* const* dout, int64_t rows, cudaStream_t st) {
+        return sa_dct_inverse((const double*)di[0], rows, len, (double*)dout[0], st);
+    });
+}
+
+int sa_dtw_batch_host(const double* h_a, const double* h_b, int64_t n_pairs, int64_t len_a, int64_t len_b,
+                      double* h_dist) {
+    if (n_pairs < 0 || len_a < 1 || len_b < 1) return fail(SA_ERR_INVALID_ARG, "bad batch shape");
+    const HostIn in[2] = {{h_a, 8 * len_a}, {h_b, 8 * len_b}};
+    const HostOut out{h_dist, 8};
+    return host_rows(n_pairs, in, 2, &out, 1,
+                     [&](const void* const* di, void* const* dout, int64_t rows, cudaStream_t st) {
+                         return sa_dtw_batch((const double*)di[0], (const double*)di[1], rows, len_a, len_b,
+                                             (double*)dout[0], st);
+                     },
+                     std::max<int64_t>(1, (1ll << 30) / (8 * (len_a + len_b) + 8)));  // few, large launches
 }
 
 int sa_fft_forward(const double* d_in, int64_t n, int64_t len, double* d_re, double* d_im, void* stream) {
@@ -1138,10 +1183,11 @@ int sa_dtw_batch(const double* d_a, const double* d_b, int64_t n_pairs, int64_t 
     if (rc) return rc;
     if (len_a < 1 || len_b < 1) return fail(SA_ERR_INVALID_ARG, "DTW needs non-empty series");
     DeviceState& ds = dev_state(dev);
-    const size_t smem = sizeof(double) * (size_t)len_b;
+    size_t smem = sizeof(double) * (size_t)len_b;
     if (smem > ds.smem_optin) return fail(SA_ERR_UNSUPPORTED, "second series too long for DTW row buffer");
     DtwParams p{};
     p.a = d_a; p.b = d_b; p.dist = d_dist; p.pairs = n_pairs; p.n = (int32_t)len_a; p.m = (int32_t)len_b;
+    p.stage_b = 0;  // b from L1: staging it halves the resident warps (measured slower)
     if (n_pairs == 0) return SA_OK;
     int per_sm = 0;
     SA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dtw_batch_kernel, 32, smem));
@@ -1159,10 +1205,12 @@ int sa_dtw_path(const double* d_a, int64_t len_a, const double* d_b, int64_t len
     if (rc) return rc;
     if (len_a < 1 || len_b < 1) return fail(SA_ERR_INVALID_ARG, "DTW needs non-empty series");
     DeviceState& ds = dev_state(dev);
-    const size_t smem = sizeof(double) * (size_t)len_b;
+    size_t smem = sizeof(double) * (size_t)len_b;
     if (smem > ds.smem_optin) return fail(SA_ERR_UNSUPPORTED, "second series too long for DTW row buffer");
     DtwParams p{};
-    p.a = d_a; p.b = d_b; p.dist = d_dist; p.acc = d_acc; p.path = d_path; p.path_len = d_path_len;
+    p.a = d_a; p.b = d_b; p.dist = d_dist; p.acc = d_acc;
+    p.path = d_path; p.path_len = d_path_len;
+    p.stage_b = 0;
     p.pairs = 1; p.n = (int32_t)len_a; p.m = (int32_t)len_b;
     dtw_path_kernel<<<1, 32, smem, (cudaStream_t)stream>>>(p);
     SA_CUDA(cudaGetLastError());

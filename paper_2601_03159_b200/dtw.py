@@ -75,23 +75,21 @@ def dtw_similarity(a, b) -> float:
 
 
 def dtw_distances(a: Batch, b: Batch) -> np.ndarray:
-    """Row-wise DTW distances of two batches (one warp per pair)."""
-    import torch
-
+    """Row-wise DTW distances of two batches (one warp per pair), host
+    arrays through the staging runtime (sa_dtw_batch_host)."""
     from . import _native
 
     if a.n != b.n:
         raise InvalidInputError(
             f"batches must have the same number of series, got {a.n} and {b.n}"
         )
-    dev = _native.current_device()
-    ta = torch.from_numpy(a.values).to(f"cuda:{dev}")
-    tb = torch.from_numpy(b.values).to(f"cuda:{dev}")
-    dist = torch.empty(a.n, dtype=torch.float64, device=ta.device)
-    st = torch.cuda.current_stream().cuda_stream
-    _native.check(_native.lib().sa_dtw_batch(ta.data_ptr(), tb.data_ptr(), a.n, a.length, b.length,
-                                             dist.data_ptr(), st))
-    return dist.cpu().numpy()
+    _native.current_device()
+    va = np.ascontiguousarray(a.values)
+    vb = np.ascontiguousarray(b.values)
+    dist = np.empty(a.n, dtype=np.float64)
+    _native.check(_native.lib().sa_dtw_batch_host(va.ctypes.data, vb.ctypes.data, a.n, a.length, b.length,
+                                                  dist.ctypes.data), "sa_dtw_batch_host")
+    return dist
 
 
 def mean_similarity(a: Batch, b: Batch) -> float:

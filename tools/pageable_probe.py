@@ -10,3 +10,11 @@ b = Batch._from_device_checked(x)
 pipe.run(b)
 t = time.perf_counter(); out = pipe.run(b); dt = time.perf_counter() - t
 print(f"Pipeline.run pageable numpy {n}x1024: {dt*1e3:.0f} ms -> {n*1024/dt/1e9:.2f} Gpts/s ({2*x.nbytes/dt/1e9:.1f} GB/s moved)")
+# second call: output pages already touched? (fresh output array each call)
+t = time.perf_counter(); out = pipe.run(b); dt = time.perf_counter() - t
+print(f"Pipeline.run pageable numpy (2nd) {dt*1e3:.0f} ms -> {n*1024/dt/1e9:.2f} Gpts/s")
+from paper_2601_03159_b200 import pinned_empty
+o = pinned_empty(x.shape)
+pipe.run(b, out=o)
+t = time.perf_counter(); pipe.run(b, out=o); dt = time.perf_counter() - t
+print(f"Pipeline.run pageable in, pinned out: {dt*1e3:.0f} ms -> {n*1024/dt/1e9:.2f} Gpts/s")
