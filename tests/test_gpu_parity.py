@@ -372,3 +372,25 @@ def test_concurrent_callers_match_sequential():
         t.join()
     for k in range(len(xs)):
         assert np.array_equal(got[k], want[k]), k
+
+
+@pytest.mark.parametrize("n,m", [(1, 1), (1, 70), (70, 1), (31, 33), (63, 64), (64, 63), (64, 64), (65, 130),
+                                 (127, 129), (128, 128), (130, 64), (200, 61), (61, 200), (257, 300)])
+def test_dtw_shapes_bitwise(n, m):
+    """Every strip / ramp / steady-state split of the DTW wavefront (64-row
+    strips, two rows per lane) against the oracle, distances and paths."""
+    import torch
+
+    from oracle import oracle as O
+    from paper_2601_03159_b200 import Batch, dtw_distance, dtw_distances
+
+    rng = np.random.default_rng(n * 1000 + m)
+    a = np.cumsum(rng.normal(0, 1, (5, n)), axis=1)
+    b = np.cumsum(rng.normal(0, 1, (5, m)), axis=1)
+    got = dtw_distances(Batch(a), Batch(b))
+    for i in range(5):
+        d, path = O.dtw(a[i], b[i])
+        assert got[i] == d, (i, got[i], d)
+    res = dtw_distance(a[0], b[0])
+    d, path = O.dtw(a[0], b[0])
+    assert res.distance == d and [tuple(p) for p in res.path] == [tuple(p) for p in path]
