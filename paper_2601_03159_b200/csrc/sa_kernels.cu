@@ -173,6 +173,7 @@ __global__ void __launch_bounds__(384) chain_kernel(const __grid_constant__ Chai
         double* cur = A;
         double* oth = B;
         int L = p.len_in;
+        double2* held = nullptr;  // the row's half spectrum between fused spectral stages
         for (int j = 0; j < p.ns; ++j) {
             if ((p.sync_mask >> j) & 1ull) __syncthreads();
             if (!active || !((fire_lo >> j) & 1ull)) continue;
@@ -205,7 +206,18 @@ __global__ void __launch_bounds__(384) chain_kernel(const __grid_constant__ Chai
                 case SA_OP_NOISE_SLOPE: arith = op_slope(st, s, cur, L, w, bad); break;
                 case SA_OP_APP:
                 case SA_OP_FREQ_MASK:
-                case SA_OP_SINUSOID: arith = op_spectral(st, s, cur, oth, L, w); break;
+                case SA_OP_SINUSOID: {
+                    // Consecutive spectral stages share one spectrum: the
+                    // reference's irfft -> rfft between them is the identity
+                    // up to rounding once DC (and Nyquist) imaginary parts
+                    // are re-pinned to 0 (freqaugment.py:40-45), so the row
+                    // stays in the frequency domain until the last one.
+                    const uint64_t later = (j + 1 < 64) ? (fire_lo >> (j + 1)) : 0;
+                    const int nx = later ? j + 1 + __ffsll((long long)later) - 1 : p.ns;
+                    const bool keep = nx < p.ns && is_spectral_op(p.st[nx].op) && !spectral_noop(p.st[nx]);
+                    arith = op_spectral(st, s, cur, oth, L, w, held, keep, bad);
+                    break;
+                }
                 case SA_OP_TIME_WARP: arith = op_time_warp(st, s, cur, oth, L, w, flags, bad); break;
                 case SA_OP_WINDOW_WARP: arith = op_window_warp(st, s, cur, oth, L, w, flags, bad); break;
                 case SA_OP_DROPOUT: arith = op_dropout(st, s, cur, L, w); break;

@@ -963,11 +963,36 @@ __device__ __forceinline__ void perturb_spectrum(const DevStage& st, WStream& s,
 }
 
 // freqaugment.py:37-47 SpectralAugmenter._apply (time-domain entry)
-__device__ __forceinline__ bool op_spectral(const DevStage& st, WStream& s, double*& cur, double*& oth, int L, Warp& w) {
+__device__ __forceinline__ bool is_spectral_op(int op) {
+    return op == SA_OP_APP || op == SA_OP_FREQ_MASK || op == SA_OP_SINUSOID;
+}
+
+// rfft -> perturb -> irfft (freqaugment.py:37-47).  `held` != nullptr: the
+// row is already held as its half spectrum (the previous stage kept it).
+// keep: leave the result as a spectrum in `held` for the next spectral stage
+// (no finiteness check of a time-domain row then; the bins are checked).
+__device__ __forceinline__ bool op_spectral(const DevStage& st, WStream& s, double*& cur, double*& oth, int L, Warp& w,
+                                            double2*& held, bool keep, bool& bad) {
     if (spectral_noop(st)) return false;
-    double2* X = rfft_any(cur, oth, L, st.fft, st.tw, w.lane);
+    double2* X;
+    if (held) {
+        X = held;
+        held = nullptr;
+        if (w.lane == 0) {  // the pins _apply puts on every fresh rfft
+            X[0].y = 0.0;
+            if ((L & 1) == 0) X[L / 2].y = 0.0;
+        }
+        __syncwarp();
+    } else {
+        X = rfft_any(cur, oth, L, st.fft, st.tw, w.lane);
+    }
     double* free_buf = (reinterpret_cast<double*>(X) == cur) ? oth : cur;
     perturb_spectrum(st, s, X, L, free_buf, w);
+    if (keep) {
+        held = X;
+        for (int k = w.lane; k < L / 2 + 1; k += 32) bad |= nonfinite(X[k].x) | nonfinite(X[k].y);
+        return false;
+    }
     double2* other = reinterpret_cast<double2*>(free_buf);
     double* y = irfft_any(X, other, L, st.fft, st.tw, w.lane);
     if (y != cur) swapbuf(cur, oth);
