@@ -771,43 +771,41 @@ __device__ __forceinline__ bool op_pool(const DevStage& st, double*& cur, int L,
     return false;
 }
 
-// BASELINE M4 Convolve (taps in params.aux).  Each lane computes two
-// outputs (t, t + 32) as independent chains; chunks whose taps stay inside
+// BASELINE M4 Convolve (taps in params.aux).  Each lane computes four
+// outputs (t + 32q) as independent chains; chunks whose taps stay inside
 // the series skip the edge clamp.  Per output the taps are summed in order
 // k = 0..S-1 exactly as before.
 __device__ __forceinline__ bool op_convolve(const DevStage& st, const double* aux, double*& cur, double*& oth, int L, Warp& w, bool& bad) {
     const double* taps = aux + st.aux_off;
     const int S = st.aux_len, h = S / 2;
     const int t_hi = L - S + h;  // outputs t in [h, t_hi] read only cur[0 .. L-1]
-    for (int t0 = 0; t0 < L; t0 += 64) {
-        const int ta = t0 + w.lane, tb = ta + 32;
-        double a0 = 0.0, a1 = 0.0;
-        if (t0 >= h && t0 + 63 <= t_hi) {  // warp-uniform interior chunk
-            const double* pa = cur + ta - h;
-            const double* pb = cur + tb - h;
+    for (int t0 = 0; t0 < L; t0 += 128) {
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        if (t0 >= h && t0 + 127 <= t_hi) {  // warp-uniform interior chunk
+            const double* pa = cur + t0 + w.lane - h;
             for (int k = 0; k < S; ++k) {
                 const double c = taps[k];
-                a0 = a0 + c * pa[k];
-                a1 = a1 + c * pb[k];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[q] = acc[q] + c * pa[k + 32 * q];
             }
         } else {
             for (int k = 0; k < S; ++k) {
                 const double c = taps[k];
-                int u = ta + k - h;
-                u = u < 0 ? 0 : (u > L - 1 ? L - 1 : u);
-                int v = tb + k - h;
-                v = v < 0 ? 0 : (v > L - 1 ? L - 1 : v);
-                a0 = a0 + c * cur[u];
-                a1 = a1 + c * cur[v];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    int u = t0 + w.lane + 32 * q + k - h;
+                    u = u < 0 ? 0 : (u > L - 1 ? L - 1 : u);
+                    acc[q] = acc[q] + c * cur[u];
+                }
             }
         }
-        if (ta < L) {
-            oth[ta] = a0;
-            bad |= nonfinite(a0);
-        }
-        if (tb < L) {
-            oth[tb] = a1;
-            bad |= nonfinite(a1);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int t = t0 + w.lane + 32 * q;
+            if (t < L) {
+                oth[t] = acc[q];
+                bad |= nonfinite(acc[q]);
+            }
         }
     }
     __syncwarp();
@@ -852,29 +850,50 @@ __device__ __forceinline__ bool op_speed_warp(const DevStage& st, WStream& s, do
     auto tau_at = [&](int t, int m) { return base[m] + speeds[m] * (double)(t - sbt[m]); };
     const double f = ((double)L - 1.0) / tau_at(L - 1, seg_of(L - 1, 0));
     const bool cubic = st.i[1] != 0;
+    // four elements per lane per step: their segment indices first (a short
+    // serial walk), then four independent interpolations (ILP for the long
+    // tau -> floor -> gather -> cubic chain)
     int m = 0;
-#pragma unroll 2
-    for (int t = w.lane; t < L; t += 32) {
-        m = seg_of(t, m);
-        const double tau = (t == L - 1) ? (double)L - 1.0 : tau_at(t, m) * f;
-        int j = (int)floor(tau);
-        j = j < 0 ? 0 : (j > L - 2 ? L - 2 : j);
-        const double fr = tau - (double)j;
-        const double p1 = cur[j], p2 = cur[j + 1];
-        double y;
-        if (cubic) {
-            const double p0 = cur[j > 0 ? j - 1 : 0], p3 = cur[j + 2 < L ? j + 2 : L - 1];
-            const double a = ((-0.5 * p0 + 1.5 * p1) - 1.5 * p2) + 0.5 * p3;
-            const double b = ((p0 - 2.5 * p1) + 2.0 * p2) - 0.5 * p3;
-            const double c = -0.5 * p0 + 0.5 * p2;
-            y = ((a * fr + b) * fr + c) * fr + p1;
-        } else {
-            y = p1 + (p2 - p1) * fr;
+    for (int t0 = w.lane; t0 < L; t0 += 128) {
+        int ms[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int t = t0 + 32 * q;
+            if (t < L) m = seg_of(t, m);
+            ms[q] = m;
         }
-        y = (tau >= (double)(L - 1)) ? cur[L - 1] : y;
-        y = (tau <= 0.0) ? cur[0] : y;
-        oth[t] = y;
-        bad |= nonfinite(y);
+        double ys[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int t = t0 + 32 * q;
+            const int tt = t < L ? t : L - 1;
+            const double tau = (tt == L - 1) ? (double)L - 1.0 : tau_at(tt, ms[q]) * f;
+            int j = (int)floor(tau);
+            j = j < 0 ? 0 : (j > L - 2 ? L - 2 : j);
+            const double fr = tau - (double)j;
+            const double p1 = cur[j], p2 = cur[j + 1];
+            double y;
+            if (cubic) {
+                const double p0 = cur[j > 0 ? j - 1 : 0], p3 = cur[j + 2 < L ? j + 2 : L - 1];
+                const double a = ((-0.5 * p0 + 1.5 * p1) - 1.5 * p2) + 0.5 * p3;
+                const double b = ((p0 - 2.5 * p1) + 2.0 * p2) - 0.5 * p3;
+                const double c = -0.5 * p0 + 0.5 * p2;
+                y = ((a * fr + b) * fr + c) * fr + p1;
+            } else {
+                y = p1 + (p2 - p1) * fr;
+            }
+            y = (tau >= (double)(L - 1)) ? cur[L - 1] : y;
+            y = (tau <= 0.0) ? cur[0] : y;
+            ys[q] = y;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int t = t0 + 32 * q;
+            if (t < L) {
+                oth[t] = ys[q];
+                bad |= nonfinite(ys[q]);
+            }
+        }
     }
     __syncwarp();
     swapbuf(cur, oth);
