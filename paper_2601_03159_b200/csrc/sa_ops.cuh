@@ -100,17 +100,18 @@ struct Linspace {
     }
 };
 
-// np.interp on a monotone table with precomputed per-interval slopes
-// (numpy precomputes exactly these slopes when len(xp) <= len(x)); the
-// bracketing interval comes from an O(1) guess `hint` refined by compares,
-// which yields the same "largest j with xp[j] <= x" as numpy's search.
+// np.interp on a linspace table xp with precomputed per-interval slopes
+// (numpy precomputes exactly these slopes when len(xp) <= len(x)).  The
+// bracketing interval comes from the O(1) guess hint = (int)(x / step),
+// which on a linspace table is off by at most one (both sides round within
+// an ulp), so one compare each way yields numpy's "largest j with
+// xp[j] <= x"; no search loop, so unrolled calls interleave.  Every caller
+// (Drift anchors, TimeWarp / WindowWarp knots) passes a linspace table.
 __device__ __forceinline__ double interp_slopes(double x, const double* __restrict__ xp, const double* __restrict__ fp,
                                                 const double* __restrict__ sl, int n, int hint) {
     int j = hint < 0 ? 0 : (hint > n - 2 ? n - 2 : hint);
     j = (xp[j + 1] <= x && j < n - 2) ? j + 1 : j;
     j = (xp[j] > x && j > 0) ? j - 1 : j;
-    while (j < n - 2 && xp[j + 1] <= x) ++j;  // never taken for linspace tables
-    while (j > 0 && xp[j] > x) --j;
     const double xj = xp[j], fj = fp[j];
     double r = sl[j] * (x - xj) + fj;
     r = (xj == x) ? fj : r;
