@@ -94,10 +94,13 @@ __global__ void __launch_bounds__(384) chain_kernel(const __grid_constant__ Chai
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     const int nw = blockDim.x >> 5;
-    const Layout lay = make_layout(p.lcap, p.ns, p.small_words, p.iscr_words);
+    // the two row buffers sit in this warp's shared-memory slice, or -- for
+    // series too long for it -- in the warp's slot of a global scratch
+    const Layout lay = make_layout(p.gbuf ? 0 : p.lcap, p.ns, p.small_words, p.iscr_words);
     unsigned char* smem = smem_all + (size_t)wid * lay.total;  // this warp's slice
-    double* A = reinterpret_cast<double*>(smem + lay.buf_a);
-    double* B = reinterpret_cast<double*>(smem + lay.buf_b);
+    double* A = p.gbuf ? p.gbuf + ((int64_t)blockIdx.x * nw + wid) * 2 * (int64_t)p.lcap
+                       : reinterpret_cast<double*>(smem + lay.buf_a);
+    double* B = p.gbuf ? A + p.lcap : reinterpret_cast<double*>(smem + lay.buf_b);
     uint64_t* scache = reinterpret_cast<uint64_t*>(smem + lay.scache);
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + lay.bar);
     Warp w;
@@ -325,12 +328,19 @@ struct FftParams {
     int64_t n;
     int32_t L, lcap;
     const double2* tw;
+    double* gbuf;  // non-null: per-CTA row buffers (2 * lcap doubles) in global memory
 };
+
+// row buffers of the one-warp transform kernels: shared memory, or this
+// CTA's slot of a global scratch for series too long for it
+__device__ __forceinline__ double* row_bufs(unsigned char* smem, double* gbuf, int lcap) {
+    return gbuf ? gbuf + (int64_t)blockIdx.x * 2 * (int64_t)lcap : reinterpret_cast<double*>(smem);
+}
 
 __global__ void __launch_bounds__(32) rfft_kernel(const __grid_constant__ FftParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x;
-    double* A = reinterpret_cast<double*>(smem);
+    double* A = row_bufs(smem, p.gbuf, p.lcap);
     double* B = A + p.lcap;
     const int bins = p.L / 2 + 1;
     for (int64_t row = blockIdx.x; row < p.n; row += gridDim.x) {
@@ -349,7 +359,7 @@ __global__ void __launch_bounds__(32) rfft_kernel(const __grid_constant__ FftPar
 __global__ void __launch_bounds__(32) irfft_kernel(const __grid_constant__ FftParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x;
-    double2* X = reinterpret_cast<double2*>(smem);
+    double2* X = reinterpret_cast<double2*>(row_bufs(smem, p.gbuf, p.lcap));
     double2* O = X + p.lcap / 2;
     const int bins = p.L / 2 + 1;
     for (int64_t row = blockIdx.x; row < p.n; row += gridDim.x) {
@@ -365,7 +375,7 @@ __global__ void __launch_bounds__(32) irfft_kernel(const __grid_constant__ FftPa
 __global__ void __launch_bounds__(32) dct_kernel(const __grid_constant__ FftParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x;
-    double* A = reinterpret_cast<double*>(smem);
+    double* A = row_bufs(smem, p.gbuf, p.lcap);
     double* B = A + p.lcap;
     for (int64_t row = blockIdx.x; row < p.n; row += gridDim.x) {
         const double* src = p.x + row * p.L;
@@ -389,12 +399,13 @@ struct DtwParams {
     int64_t pairs;
     int32_t n, m;
     int32_t stage_b;  // 1: dtw_warp copies b into shared memory
+    double* gprow;    // non-null: the previous-row buffer in global memory (len_b too long for smem)
 };
 
 // one warp per pair: distance only
 __global__ void __launch_bounds__(32) dtw_batch_kernel(const __grid_constant__ DtwParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
-    double* prow = reinterpret_cast<double*>(smem);
+    double* prow = p.gprow ? p.gprow + (int64_t)blockIdx.x * p.m : reinterpret_cast<double*>(smem);
     for (int64_t q = blockIdx.x; q < p.pairs; q += gridDim.x) {
         const double d = dtw_warp(p.a + q * p.n, p.n, p.b + q * p.m, p.m, prow, nullptr, threadIdx.x, p.stage_b != 0);
         if (threadIdx.x == 0) p.dist[q] = d;
@@ -405,7 +416,7 @@ __global__ void __launch_bounds__(32) dtw_batch_kernel(const __grid_constant__ D
 // one pair with the full matrix and the reference's backtracked path
 __global__ void __launch_bounds__(32) dtw_path_kernel(const __grid_constant__ DtwParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
-    double* prow = reinterpret_cast<double*>(smem);
+    double* prow = p.gprow ? p.gprow : reinterpret_cast<double*>(smem);
     const double d = dtw_warp(p.a, p.n, p.b, p.m, prow, p.acc, threadIdx.x, p.stage_b != 0);
     __syncwarp();
     __threadfence_block();
@@ -446,15 +457,16 @@ struct SpecParams {
     double* imo;
     int64_t n;
     int32_t L, lcap;
+    double* gbuf;  // non-null: per-CTA spectrum + scratch in global memory
 };
 
 // SpectralAugmenter.augment_spectrum (freqaugment.py:49-76)
 __global__ void __launch_bounds__(32) spectrum_kernel(const __grid_constant__ SpecParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x;
-    double2* X = reinterpret_cast<double2*>(smem);
+    double2* X = reinterpret_cast<double2*>(row_bufs(smem, p.gbuf, p.lcap));
     double* scratch = reinterpret_cast<double*>(X + p.lcap / 2);
-    uint64_t* win = reinterpret_cast<uint64_t*>(scratch + p.lcap);
+    uint64_t* win = p.gbuf ? reinterpret_cast<uint64_t*>(smem) : reinterpret_cast<uint64_t*>(scratch + p.lcap);
     uint64_t* c = win + SA_WIN;
     Warp w;
     w.lane = lane;
@@ -697,6 +709,7 @@ struct Plan {
     int grid;
     int warps;     // warps (= series in flight) per CTA
     size_t smem;   // dynamic smem per CTA
+    bool global = false;  // row buffers in a global scratch of grid * warps slots
 };
 
 int env_int(const char* k, int d) {
@@ -796,9 +809,14 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
     p.iscr_words = iscr;
     plan->lay = make_layout(p.lcap, ns, small, iscr);
     DeviceState& ds = dev_state(dev);
-    if (plan->lay.total + 256 * sizeof(ZigEntry) > ds.smem_optin)
-        return fail(SA_ERR_UNSUPPORTED, "series too long for one warp's shared memory (" +
-                                            std::to_string(plan->lay.total) + " B)");
+    if (plan->lay.total + 256 * sizeof(ZigEntry) > ds.smem_optin || env_int("SA_FORCE_GLOBAL", 0)) {
+        // long series: the two row buffers move to global memory (L2 / HBM
+        // resident, same code); shared memory keeps the window and scratch
+        plan->global = true;
+        plan->lay = make_layout(0, ns, small, iscr);
+        if (plan->lay.total + 256 * sizeof(ZigEntry) > ds.smem_optin)
+            return fail(SA_ERR_UNSUPPORTED, "stage scratch too large for shared memory");
+    }
     // Stage-major CTAs: `warps` series per CTA walk the chain in lockstep
     // (a barrier every `sync_every` stages) so the SM works through one
     // operator's code at a time (the fused kernel is
@@ -867,6 +885,16 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
     per_sm = std::max(per_sm, 1);
     int64_t ctas_needed = (p.rows_out + warps - 1) / warps;
     int64_t want = (int64_t)ds.sms * per_sm;
+    if (plan->global) {  // bound the scratch: <= 4 GB of row buffers in flight
+        const int64_t slot_b = 16 * (int64_t)p.lcap;
+        const int64_t slots = std::max<int64_t>(1, (4ll << 30) / slot_b);
+        want = std::min<int64_t>(want, std::max<int64_t>(1, slots / warps));
+        if (slots < warps) {
+            plan->warps = warps = (int)slots;
+            plan->smem = (size_t)per_warp * warps + 256 * sizeof(ZigEntry);
+            ctas_needed = (p.rows_out + warps - 1) / warps;
+        }
+    }
     plan->grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, ctas_needed));
     return SA_OK;
 }
@@ -896,9 +924,16 @@ int launch_chain(Plan* plan, cudaStream_t stream) {
         __atomic_add_fetch(&g_launches, 3, __ATOMIC_RELAXED);
         p.order = order;
     }
+    double* gbuf = nullptr;
+    if (plan->global) {
+        SA_CUDA(cudaMallocAsync(&gbuf, sizeof(double) * 2 * (size_t)p.lcap * (size_t)plan->grid * plan->warps, stream));
+        p.gbuf = gbuf;
+        p.bulk_in = 0;  // TMA bulk copies target shared memory only
+    }
     chain_kernel<<<plan->grid, 32 * plan->warps, plan->smem, stream>>>(p);
     SA_CUDA(cudaGetLastError());
     __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
+    if (gbuf) SA_CUDA(cudaFreeAsync(gbuf, stream));
     if (keys) {
         SA_CUDA(cudaFreeAsync(keys, stream));
         SA_CUDA(cudaFreeAsync(hist, stream));
@@ -923,15 +958,30 @@ int flags_status(uint32_t f) {
     return SA_OK;
 }
 
-int fft_plan_smem(int dev, int64_t L, int* lcap, size_t* smem, int* grid, const void* kern, int64_t n) {
+// Buffers of the one-warp transform kernels: 2 * lcap doubles + a Philox
+// window per CTA in shared memory; when that does not fit, the row buffers
+// go to a global scratch of grid slots (<= 4 GB) and only the window stays.
+int fft_plan_smem(int dev, int64_t L, int* lcap, size_t* smem, int* grid, const void* kern, int64_t n,
+                  bool* global) {
     *lcap = (int)((fft_lcap(L) + 1) & ~1LL);
     *smem = (size_t)(*lcap) * 8 * 2 + 8 * SA_WIN + 64;
     DeviceState& ds = dev_state(dev);
-    if (*smem > ds.smem_optin) return fail(SA_ERR_UNSUPPORTED, "series too long");
+    *global = *smem > ds.smem_optin || env_int("SA_FORCE_GLOBAL", 0) != 0;
+    if (*global) *smem = 8 * SA_WIN + 64 + 32;
     int per_sm = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32, *smem);
     if (e != cudaSuccess) return cuda_fail(e, "occupancy");
-    *grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ds.sms * std::max(per_sm, 1), n));
+    int64_t g = (int64_t)ds.sms * std::max(per_sm, 1);
+    if (*global) g = std::min<int64_t>(g, std::max<int64_t>(1, (4ll << 30) / (16 * (int64_t)*lcap)));
+    *grid = (int)std::max<int64_t>(1, std::min<int64_t>(g, n));
+    return SA_OK;
+}
+
+// global scratch for a transform launch (freed stream-ordered by the caller)
+int alloc_row_bufs(bool global, int lcap, int grid, cudaStream_t st, double** out) {
+    *out = nullptr;
+    if (!global) return SA_OK;
+    SA_CUDA(cudaMallocAsync(out, sizeof(double) * 2 * (size_t)lcap * (size_t)grid, st));
     return SA_OK;
 }
 
@@ -1126,13 +1176,17 @@ int sa_fft_forward(const double* d_in, int64_t n, int64_t len, double* d_re, dou
     if (rc) return rc;
     size_t smem;
     int lcap, grid;
-    rc = fft_plan_smem(dev, len, &lcap, &smem, &grid, (const void*)rfft_kernel, n);
+    bool global;
+    rc = fft_plan_smem(dev, len, &lcap, &smem, &grid, (const void*)rfft_kernel, n, &global);
     if (rc) return rc;
     p.lcap = lcap;
     if (n == 0) return SA_OK;
+    rc = alloc_row_bufs(global, lcap, grid, (cudaStream_t)stream, &p.gbuf);
+    if (rc) return rc;
     rfft_kernel<<<grid, 32, smem, (cudaStream_t)stream>>>(p);
     SA_CUDA(cudaGetLastError());
     __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
+    if (p.gbuf) SA_CUDA(cudaFreeAsync(p.gbuf, (cudaStream_t)stream));
     return SA_OK;
 }
 
@@ -1147,13 +1201,17 @@ int sa_fft_inverse(const double* d_re, const double* d_im, int64_t n, int64_t le
     if (rc) return rc;
     size_t smem;
     int lcap, grid;
-    rc = fft_plan_smem(dev, len, &lcap, &smem, &grid, (const void*)irfft_kernel, n);
+    bool global;
+    rc = fft_plan_smem(dev, len, &lcap, &smem, &grid, (const void*)irfft_kernel, n, &global);
     if (rc) return rc;
     p.lcap = lcap;
     if (n == 0) return SA_OK;
+    rc = alloc_row_bufs(global, lcap, grid, (cudaStream_t)stream, &p.gbuf);
+    if (rc) return rc;
     irfft_kernel<<<grid, 32, smem, (cudaStream_t)stream>>>(p);
     SA_CUDA(cudaGetLastError());
     __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
+    if (p.gbuf) SA_CUDA(cudaFreeAsync(p.gbuf, (cudaStream_t)stream));
     return SA_OK;
 }
 
@@ -1170,13 +1228,17 @@ static int dct_launch(const double* d_in, int64_t n, int64_t len, double* d_out,
     if (rc) return rc;
     size_t smem;
     int lcap, grid;
-    rc = fft_plan_smem(dev, 2 * len, &lcap, &smem, &grid, (const void*)dct_kernel, n);  // 2N + 2 doubles
+    bool global;
+    rc = fft_plan_smem(dev, 2 * len, &lcap, &smem, &grid, (const void*)dct_kernel, n, &global);  // 2N + 2 doubles
     if (rc) return rc;
     p.lcap = lcap;
     if (n == 0) return SA_OK;
+    rc = alloc_row_bufs(global, lcap, grid, (cudaStream_t)stream, &p.gbuf);
+    if (rc) return rc;
     dct_kernel<<<grid, 32, smem, (cudaStream_t)stream>>>(p);
     SA_CUDA(cudaGetLastError());
     __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
+    if (p.gbuf) SA_CUDA(cudaFreeAsync(p.gbuf, (cudaStream_t)stream));
     return SA_OK;
 }
 
@@ -1196,7 +1258,8 @@ int sa_dtw_batch(const double* d_a, const double* d_b, int64_t n_pairs, int64_t 
     if (len_a < 1 || len_b < 1) return fail(SA_ERR_INVALID_ARG, "DTW needs non-empty series");
     DeviceState& ds = dev_state(dev);
     size_t smem = sizeof(double) * (size_t)len_b;
-    if (smem > ds.smem_optin) return fail(SA_ERR_UNSUPPORTED, "second series too long for DTW row buffer");
+    const bool global = smem > ds.smem_optin;  // long b: the row buffer lives in global memory
+    if (global) smem = 0;
     DtwParams p{};
     p.a = d_a; p.b = d_b; p.dist = d_dist; p.pairs = n_pairs; p.n = (int32_t)len_a; p.m = (int32_t)len_b;
     p.stage_b = 0;  // b from L1: staging it halves the resident warps (measured slower)
@@ -1204,9 +1267,11 @@ int sa_dtw_batch(const double* d_a, const double* d_b, int64_t n_pairs, int64_t 
     int per_sm = 0;
     SA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dtw_batch_kernel, 32, smem));
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ds.sms * std::max(per_sm, 1), n_pairs));
+    if (global) SA_CUDA(cudaMallocAsync(&p.gprow, sizeof(double) * (size_t)len_b * grid, (cudaStream_t)stream));
     dtw_batch_kernel<<<grid, 32, smem, (cudaStream_t)stream>>>(p);
     SA_CUDA(cudaGetLastError());
     __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
+    if (p.gprow) SA_CUDA(cudaFreeAsync(p.gprow, (cudaStream_t)stream));
     return SA_OK;
 }
 
@@ -1218,15 +1283,18 @@ int sa_dtw_path(const double* d_a, int64_t len_a, const double* d_b, int64_t len
     if (len_a < 1 || len_b < 1) return fail(SA_ERR_INVALID_ARG, "DTW needs non-empty series");
     DeviceState& ds = dev_state(dev);
     size_t smem = sizeof(double) * (size_t)len_b;
-    if (smem > ds.smem_optin) return fail(SA_ERR_UNSUPPORTED, "second series too long for DTW row buffer");
+    const bool global = smem > ds.smem_optin;
+    if (global) smem = 0;
     DtwParams p{};
     p.a = d_a; p.b = d_b; p.dist = d_dist; p.acc = d_acc;
     p.path = d_path; p.path_len = d_path_len;
     p.stage_b = 0;
     p.pairs = 1; p.n = (int32_t)len_a; p.m = (int32_t)len_b;
+    if (global) SA_CUDA(cudaMallocAsync(&p.gprow, sizeof(double) * (size_t)len_b, (cudaStream_t)stream));
     dtw_path_kernel<<<1, 32, smem, (cudaStream_t)stream>>>(p);
     SA_CUDA(cudaGetLastError());
     __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
+    if (p.gprow) SA_CUDA(cudaFreeAsync(p.gprow, (cudaStream_t)stream));
     return SA_OK;
 }
 
@@ -1275,14 +1343,17 @@ int sa_augment_spectrum(const sa_stage* stage, uint64_t master_seed, int64_t ser
     p.re = d_re; p.im = d_im; p.reo = d_re_out; p.imo = d_im_out; p.n = n; p.L = (int32_t)len;
     size_t smem;
     int lcap, grid;
-    rc = fft_plan_smem(dev, len, &lcap, &smem, &grid, (const void*)spectrum_kernel, n);
+    bool global;
+    rc = fft_plan_smem(dev, len, &lcap, &smem, &grid, (const void*)spectrum_kernel, n, &global);
     if (rc) return rc;
     p.lcap = lcap;
-    smem = (size_t)lcap * 8 * 2 + 8 * SA_WIN + 64;
     if (n == 0) return SA_OK;
+    rc = alloc_row_bufs(global, lcap, grid, (cudaStream_t)stream, &p.gbuf);
+    if (rc) return rc;
     spectrum_kernel<<<grid, 32, smem, (cudaStream_t)stream>>>(p);
     SA_CUDA(cudaGetLastError());
     __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
+    if (p.gbuf) SA_CUDA(cudaFreeAsync(p.gbuf, (cudaStream_t)stream));
     SA_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
     return SA_OK;
 }

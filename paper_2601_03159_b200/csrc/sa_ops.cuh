@@ -43,6 +43,7 @@ struct ChainParams {
     const double* in;
     double* out;
     uint32_t* flags;
+    double* gbuf;                  // non-null: row buffers in global memory (series too long for smem)
     double aux[SA_MAX_AUX];
     DevStage st[SA_MAX_STAGES];
 };

@@ -394,3 +394,73 @@ def test_dtw_shapes_bitwise(n, m):
     res = dtw_distance(a[0], b[0])
     d, path = O.dtw(a[0], b[0])
     assert res.distance == d and [tuple(p) for p in res.path] == [tuple(p) for p in path]
+
+
+def _exact_chain(seed=3):
+    from paper_2601_03159_b200 import (Drift, Dropout, InjectNoise, Jitter, PermuteSegments, Pipeline, Pool,
+                                       Quantize, Reverse, SpikeNoise, TimeWarp, WindowWarp)
+
+    return Pipeline(stages=(Jitter(0.05, probability=0.5), Drift(0.5, 5, probability=0.5),
+                            Quantize(16, probability=0.5), Dropout(0.05, probability=0.5),
+                            PermuteSegments(4, probability=0.5), InjectNoise(SpikeNoise(5, 2.0), probability=0.5),
+                            Pool(4, probability=0.5), TimeWarp(5, 0.5, probability=0.5),
+                            WindowWarp(128, 4, 0.5, probability=0.5), Reverse(probability=0.5)),
+                    master_seed=seed)
+
+
+def test_global_row_buffers_bitwise_equal_shared(monkeypatch):
+    """SA_FORCE_GLOBAL moves the row buffers to global memory (the long-series
+    mode): same code, so results are bitwise those of the shared-memory mode,
+    for the chain kernel and the transform kernels."""
+    import torch
+
+    from paper_2601_03159_b200 import (AmplitudePhasePerturb, Batch, FrequencyMask, Pipeline, RandomSinusoid,
+                                       dct_forward, fft_forward)
+
+    x = np.cumsum(np.random.default_rng(7).normal(0, 1, (300, 1024)), axis=1)
+    spectral = Pipeline(stages=(AmplitudePhasePerturb(0.1, 0.1, probability=0.5), FrequencyMask(20),
+                                RandomSinusoid(1.0, probability=0.5)), master_seed=4)
+    runs = []
+    for mode in ("0", "1"):
+        monkeypatch.setenv("SA_FORCE_GLOBAL", mode)
+        xt = torch.from_numpy(x).cuda()
+        runs.append((_exact_chain().run_device(xt).cpu().numpy(), spectral.run_device(xt).cpu().numpy(),
+                     fft_forward(Batch(x)).re, dct_forward(Batch(x)).coeffs))
+    for a, b in zip(*runs):
+        assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+@pytest.mark.parametrize("L", [50_000, 65_536])
+def test_long_series_match_oracle(L):
+    """Series too long for shared memory run with global row buffers."""
+    import torch
+
+    from oracle import oracle as O
+    from paper_2601_03159_b200 import Batch, FrequencyMask, Pipeline, RandomSinusoid, fft_forward, fft_inverse
+    from sa_testutil import assert_matches
+
+    x = np.cumsum(np.random.default_rng(L).normal(0, 1, (4, L)), axis=1)
+    pipe = _exact_chain(seed=11)
+    got = pipe.run_device(torch.from_numpy(x).cuda()).cpu().numpy()
+    want = O.run_pipeline(pipe, x)
+    err = np.abs(got - want).max()  # bitwise except ziggurat-tail normals (<= 1 ulp, DESIGN.md §5)
+    assert err <= 1e-12 * np.abs(want).max(), err
+    spectral = Pipeline(stages=(FrequencyMask(L // 20), RandomSinusoid(1.0)), master_seed=5)
+    assert_matches(spectral.run(Batch(x)).values, O.run_pipeline(spectral, x), exact=False, what="spectral")
+    spec = fft_forward(Batch(x))
+    back = fft_inverse(spec).values
+    assert np.abs(back - x).max() <= 1e-9 * np.abs(x).max()
+
+
+def test_dtw_long_second_series():
+    """b longer than the shared-memory row buffer (> ~29k points): the row
+    buffer moves to global memory; distances stay bitwise."""
+    from oracle import oracle as O
+    from paper_2601_03159_b200 import Batch, dtw_distances
+
+    rng = np.random.default_rng(5)
+    a = np.cumsum(rng.normal(0, 1, (2, 40)), axis=1)
+    b = np.cumsum(rng.normal(0, 1, (2, 30_000)), axis=1)
+    got = dtw_distances(Batch(a), Batch(b))
+    for i in range(2):
+        assert got[i] == O.dtw(a[i], b[i])[0]
