@@ -140,14 +140,24 @@ __device__ __forceinline__ void stockham_pass(const double2* __restrict__ src, d
     __syncwarp();
 }
 
-// Host-built pass plan of an N-point complex FFT (N | L).
+// Host-built pass plan of an N-point complex FFT (N | L).  N with a large
+// prime factor uses Bluestein instead (blue = 1): the N-point DFT as a
+// circular convolution of length M (a power of two >= 2N - 1), i.e. two
+// M-point FFTs and a pointwise product with the precomputed FFT of the
+// chirp kernel -- O(M log M) like pocketfft, instead of the O(N p) generic
+// pass.  M's radix plan and tables ride along.
 #define SA_FFT_MAXPASS 24
 struct FftGeo {
     int32_t N;         // complex transform length
     int32_t packed;    // 1: even L, N = L/2 (real input viewed as complex)
     int32_t npass;
-    int32_t pad;
+    int32_t blue;      // 1: Bluestein
     int16_t radix[SA_FFT_MAXPASS];
+    int32_t M, mpass;  // Bluestein convolution length and its radix plan
+    int16_t mradix[16];
+    const double2* chirp;  // exp(-i pi n^2 / N), n < N
+    const double2* bfft;   // FFT_M of the kernel exp(+i pi m^2 / N), circular
+    const double2* twM;    // exp(-2 pi i k / M), k < M
 };
 
 // Generic radix-R Stockham pass (any R | N): each output is the direct sum
@@ -192,44 +202,76 @@ __device__ __forceinline__ void generic_pass(const double2* __restrict__ src, do
     __syncwarp();
 }
 
-// Forward N-point complex FFT per the plan; data in a, b is scratch.
-__device__ __forceinline__ double2* fft_any(double2* a, double2* b, const FftGeo& g, const double2* tw, int L,
-                                            int lane) {
+// The Stockham passes of an N-point plan (radix list `radix`, npass passes)
+// over a table of W_L (N | L); data in a, b is scratch; returns the buffer
+// holding the result.
+__device__ __forceinline__ double2* fft_passes(double2* a, double2* b, int N, int npass, const int16_t* radix,
+                                               const double2* tw, int L, int lane) {
     int Ns = 1;
     double2* src = a;
     double2* dst = b;
-    const int ts = L / g.N;  // W_N = tw[.. * ts]; the radix passes take the table length L
     int lns = 0;
     Swz carry = {0, 0};  // swizzle of the buffer the next pass reads
-    for (int p = 0; p < g.npass; ++p) {
-        const int R = g.radix[p];
+    for (int p = 0; p < npass; ++p) {
+        const int R = radix[p];
         if (R == 8 || R == 4 || R == 2) {
             const int lr = (R == 8 ? 3 : (R == 4 ? 2 : 1));
             const int tstep = L >> (lns + lr);  // L / (Ns R)
             // swizzle pass 0's output when pass 1 is a power-of-two pass too
-            const bool swz = (p == 0 && R > 2 && g.npass > 1 && (g.radix[1] & (g.radix[1] - 1)) == 0 &&
-                              (g.N / g.radix[1]) % (R * R) == 0);
+            const bool swz = (p == 0 && R > 2 && npass > 1 && (radix[1] & (radix[1] - 1)) == 0 &&
+                              (N / radix[1]) % (R * R) == 0);
             const Swz out = swz ? Swz{lr, R - 1} : Swz{0, 0};
-            if (R == 8) stockham_pass<8, false>(src, dst, g.N, lns, tw, tstep, lane, carry, out);
-            else if (R == 4) stockham_pass<4, false>(src, dst, g.N, lns, tw, tstep, lane, carry, out);
-            else stockham_pass<2, false>(src, dst, g.N, lns, tw, tstep, lane, carry, out);
+            if (R == 8) stockham_pass<8, false>(src, dst, N, lns, tw, tstep, lane, carry, out);
+            else if (R == 4) stockham_pass<4, false>(src, dst, N, lns, tw, tstep, lane, carry, out);
+            else stockham_pass<2, false>(src, dst, N, lns, tw, tstep, lane, carry, out);
             carry = out;
             lns += lr;
         } else {
-            generic_pass(src, dst, g.N, Ns, R, tw, L, lane);
+            generic_pass(src, dst, N, Ns, R, tw, L, lane);
         }
         Ns *= R;
         double2* t = src;
         src = dst;
         dst = t;
     }
-    (void)ts;
     return src;
+}
+
+// Bluestein: X[k] = c[k] * sum_n (x[n] c[n]) conj(c[k - n]), c[n] =
+// exp(-i pi n^2 / N), evaluated as IFFT_M(FFT_M(x c) * FFT_M(conj c)) with
+// IFFT(V) = conj(FFT(conj V)) / M.  a holds x (N points); a and b hold M.
+__device__ __forceinline__ double2* bluestein(double2* a, double2* b, const FftGeo& g, int lane) {
+    const int N = g.N, M = g.M;
+    for (int n = lane; n < M; n += 32) b[n] = n < N ? cmul(a[n], __ldg(&g.chirp[n])) : make_double2(0.0, 0.0);
+    __syncwarp();
+    double2* Y = fft_passes(b, a, M, g.mpass, g.mradix, g.twM, M, lane);
+    for (int k = lane; k < M; k += 32) {
+        const double2 v = cmul(Y[k], __ldg(&g.bfft[k]));
+        Y[k] = make_double2(v.x, -v.y);
+    }
+    __syncwarp();
+    double2* Z = fft_passes(Y, Y == a ? b : a, M, g.mpass, g.mradix, g.twM, M, lane);
+    const double inv = 1.0 / (double)M;
+    for (int k = lane; k < N; k += 32) {
+        const double2 z = Z[k];
+        Z[k] = cmul(make_double2(z.x * inv, -z.y * inv), __ldg(&g.chirp[k]));
+    }
+    __syncwarp();
+    return Z;
+}
+
+// Forward N-point complex FFT per the plan; data in a, b is scratch.
+template <bool BLUE = true>
+__device__ __forceinline__ double2* fft_any(double2* a, double2* b, const FftGeo& g, const double2* tw, int L,
+                                            int lane) {
+    if (BLUE && g.blue) return bluestein(a, b, g, lane);
+    return fft_passes(a, b, g.N, g.npass, g.radix, tw, L, lane);
 }
 
 // rfft of the real series x (length L, in buffer xa) -> X[0 .. L/2]
 // (complex, bins = L/2 + 1).  xb is scratch of the same capacity (>= 2L + 2
 // doubles for odd L).  Returns the buffer holding X; the other is free.
+template <bool BLUE = true>
 __device__ __forceinline__ double2* rfft_any(double* xa, double* xb, int L, const FftGeo& g, const double2* tw,
                                             int lane) {
     double2* za = reinterpret_cast<double2*>(xa);
@@ -237,13 +279,13 @@ __device__ __forceinline__ double2* rfft_any(double* xa, double* xb, int L, cons
     if (!g.packed) {  // odd L: complexify into xb, N = L transform, keep bins
         for (int n = lane; n < L; n += 32) zb[n] = make_double2(xa[n], 0.0);
         __syncwarp();
-        double2* Z = fft_any(zb, za, g, tw, L, lane);
+        double2* Z = fft_any<BLUE>(zb, za, g, tw, L, lane);
         if (lane == 0) Z[0].y = 0.0;
         __syncwarp();
         return Z;
     }
     const int M = L >> 1;
-    double2* Z = fft_any(za, zb, g, tw, L, lane);
+    double2* Z = fft_any<BLUE>(za, zb, g, tw, L, lane);
     double2* X = (Z == za) ? zb : za;
     for (int k = lane; k <= M; k += 32) {
         double2 zk = Z[k == M ? 0 : k];
@@ -267,6 +309,7 @@ __device__ __forceinline__ double2* rfft_any(double* xa, double* xb, int L, cons
 // free scratch.  Uses IFFT(Z) = conj(FFT(conj Z)).  Returns the buffer
 // holding the series.  irfft ignores the imaginary part of the DC bin (and
 // of the Nyquist bin for even L).
+template <bool BLUE = true>
 __device__ __forceinline__ double* irfft_any(double2* X, double2* other, int L, const FftGeo& g, const double2* tw,
                                             int lane) {
     if (!g.packed) {  // odd L: Hermitian completion, full transform, real part
@@ -278,7 +321,7 @@ __device__ __forceinline__ double* irfft_any(double2* X, double2* other, int L, 
             if (k > 0) other[L - k] = v;
         }
         __syncwarp();
-        double2* Z = fft_any(other, X, g, tw, L, lane);
+        double2* Z = fft_any<BLUE>(other, X, g, tw, L, lane);
         double* out = reinterpret_cast<double*>(Z == X ? other : X);
         const double s = 1.0 / (double)L;
         for (int n = lane; n < L; n += 32) out[n] = Z[n].x * s;
@@ -299,7 +342,7 @@ __device__ __forceinline__ double* irfft_any(double2* X, double2* other, int L, 
         other[k] = make_double2(er - o.y, -(ei + o.x));
     }
     __syncwarp();
-    double2* Z = fft_any(other, X, g, tw, L, lane);
+    double2* Z = fft_any<BLUE>(other, X, g, tw, L, lane);
     const double s = 1.0 / (double)M;
     for (int k = lane; k < M; k += 32) {
         double2 z = Z[k];

@@ -89,6 +89,10 @@ __host__ __device__ inline Layout make_layout(int lcap, int ns, int small_words,
 }
 
 // ------------------------------------------------------------ the kernel
+// GMEM: the row buffers live in p.gbuf (long series); the shared-memory
+// instantiation keeps them provably in shared memory (LDS/STS, not generic
+// accesses) -- the two are separate kernels for that reason.
+template <bool GMEM>
 __global__ void __launch_bounds__(384) chain_kernel(const __grid_constant__ ChainParams p) {
     extern __shared__ __align__(16) unsigned char smem_all[];
     const int lane = threadIdx.x & 31;
@@ -96,11 +100,11 @@ __global__ void __launch_bounds__(384) chain_kernel(const __grid_constant__ Chai
     const int nw = blockDim.x >> 5;
     // the two row buffers sit in this warp's shared-memory slice, or -- for
     // series too long for it -- in the warp's slot of a global scratch
-    const Layout lay = make_layout(p.gbuf ? 0 : p.lcap, p.ns, p.small_words, p.iscr_words);
+    const Layout lay = make_layout(GMEM ? 0 : p.lcap, p.ns, p.small_words, p.iscr_words);
     unsigned char* smem = smem_all + (size_t)wid * lay.total;  // this warp's slice
-    double* A = p.gbuf ? p.gbuf + ((int64_t)blockIdx.x * nw + wid) * 2 * (int64_t)p.lcap
-                       : reinterpret_cast<double*>(smem + lay.buf_a);
-    double* B = p.gbuf ? A + p.lcap : reinterpret_cast<double*>(smem + lay.buf_b);
+    double* A = GMEM ? p.gbuf + ((int64_t)blockIdx.x * nw + wid) * 2 * (int64_t)p.lcap
+                     : reinterpret_cast<double*>(smem + lay.buf_a);
+    double* B = GMEM ? A + p.lcap : reinterpret_cast<double*>(smem + lay.buf_b);
     uint64_t* scache = reinterpret_cast<uint64_t*>(smem + lay.scache);
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + lay.bar);
     Warp w;
@@ -333,14 +337,16 @@ struct FftParams {
 
 // row buffers of the one-warp transform kernels: shared memory, or this
 // CTA's slot of a global scratch for series too long for it
+template <bool GMEM>
 __device__ __forceinline__ double* row_bufs(unsigned char* smem, double* gbuf, int lcap) {
-    return gbuf ? gbuf + (int64_t)blockIdx.x * 2 * (int64_t)lcap : reinterpret_cast<double*>(smem);
+    return GMEM ? gbuf + (int64_t)blockIdx.x * 2 * (int64_t)lcap : reinterpret_cast<double*>(smem);
 }
 
+template <bool GMEM>
 __global__ void __launch_bounds__(32) rfft_kernel(const __grid_constant__ FftParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x;
-    double* A = row_bufs(smem, p.gbuf, p.lcap);
+    double* A = row_bufs<GMEM>(smem, p.gbuf, p.lcap);
     double* B = A + p.lcap;
     const int bins = p.L / 2 + 1;
     for (int64_t row = blockIdx.x; row < p.n; row += gridDim.x) {
@@ -356,10 +362,11 @@ __global__ void __launch_bounds__(32) rfft_kernel(const __grid_constant__ FftPar
     }
 }
 
+template <bool GMEM>
 __global__ void __launch_bounds__(32) irfft_kernel(const __grid_constant__ FftParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x;
-    double2* X = reinterpret_cast<double2*>(row_bufs(smem, p.gbuf, p.lcap));
+    double2* X = reinterpret_cast<double2*>(row_bufs<GMEM>(smem, p.gbuf, p.lcap));
     double2* O = X + p.lcap / 2;
     const int bins = p.L / 2 + 1;
     for (int64_t row = blockIdx.x; row < p.n; row += gridDim.x) {
@@ -372,10 +379,11 @@ __global__ void __launch_bounds__(32) irfft_kernel(const __grid_constant__ FftPa
 }
 
 // dct_forward / dct_inverse (reference freqtransform.py:91-98), one warp per row
+template <bool GMEM>
 __global__ void __launch_bounds__(32) dct_kernel(const __grid_constant__ FftParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x;
-    double* A = row_bufs(smem, p.gbuf, p.lcap);
+    double* A = row_bufs<GMEM>(smem, p.gbuf, p.lcap);
     double* B = A + p.lcap;
     for (int64_t row = blockIdx.x; row < p.n; row += gridDim.x) {
         const double* src = p.x + row * p.L;
@@ -461,12 +469,13 @@ struct SpecParams {
 };
 
 // SpectralAugmenter.augment_spectrum (freqaugment.py:49-76)
+template <bool GMEM>
 __global__ void __launch_bounds__(32) spectrum_kernel(const __grid_constant__ SpecParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x;
-    double2* X = reinterpret_cast<double2*>(row_bufs(smem, p.gbuf, p.lcap));
+    double2* X = reinterpret_cast<double2*>(row_bufs<GMEM>(smem, p.gbuf, p.lcap));
     double* scratch = reinterpret_cast<double*>(X + p.lcap / 2);
-    uint64_t* win = p.gbuf ? reinterpret_cast<uint64_t*>(smem) : reinterpret_cast<uint64_t*>(scratch + p.lcap);
+    uint64_t* win = GMEM ? reinterpret_cast<uint64_t*>(smem) : reinterpret_cast<uint64_t*>(scratch + p.lcap);
     uint64_t* c = win + SA_WIN;
     Warp w;
     w.lane = lane;
@@ -571,7 +580,8 @@ int init_device(int dev) {
     int optin = 0;
     SA_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     ds.smem_optin = (size_t)optin;
-    SA_CUDA(cudaFuncSetAttribute(chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(chain_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(chain_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     // The scheduling buffers come from the stream-ordered allocator; keep the
     // pool's memory mapped between calls (the default release threshold of 0
     // unmaps it at every synchronisation and the next cudaMallocAsync pays a
@@ -582,10 +592,14 @@ int init_device(int dev) {
         uint64_t keep = UINT64_MAX;
         SA_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     }
-    SA_CUDA(cudaFuncSetAttribute(rfft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-    SA_CUDA(cudaFuncSetAttribute(irfft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-    SA_CUDA(cudaFuncSetAttribute(spectrum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-    SA_CUDA(cudaFuncSetAttribute(dct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(rfft_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(rfft_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(irfft_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(irfft_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(spectrum_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(spectrum_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(dct_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(dct_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(dtw_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(dtw_path_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaSetDevice(prev));
@@ -629,6 +643,8 @@ int get_twiddles(int dev, int L, const double2** out) {
 // Pass plan of the complex transform used for a real length L: N = L/2
 // (packed) for even L, N = L for odd L; radix 8/4/2 passes first, then one
 // generic pass per remaining prime factor (ascending).
+int env_int(const char* k, int d);
+
 bool make_fft_geo(int64_t L, FftGeo* g) {
     std::memset(g, 0, sizeof(*g));
     if (L < 1) return false;
@@ -659,7 +675,104 @@ bool make_fft_geo(int64_t L, FftGeo* g) {
         }
     }
     g->npass = np;
+    // Large prime factors: the generic passes cost ~N * sum(p) complex MACs;
+    // Bluestein costs ~three M-point power-of-two FFTs.  Switch when that is
+    // clearly cheaper (Bluestein also needs 2M-point buffers, so a margin).
+    int64_t gen = 0;
+    for (int q = 0; q < np; ++q)
+        if (g->radix[q] != 2 && g->radix[q] != 4 && g->radix[q] != 8) gen += N * (int64_t)g->radix[q];
+    if (gen > 0 && env_int("SA_BLUESTEIN", 1)) {
+        int64_t M = 1;
+        while (M < 2 * N - 1) M <<= 1;
+        int lg = 0;
+        while ((1ll << lg) < M) ++lg;
+        const double blu = 4.5 * (double)M * (double)lg;
+        if ((double)gen > 4.0 * blu || env_int("SA_BLUESTEIN", 1) == 2) {
+            if (M > (1ll << 26)) return false;
+            g->blue = 1;
+            g->M = (int32_t)M;
+            int mp = 0;
+            for (int64_t left = M; left > 1;) {
+                const int r = (left >= 8 && left != 16) ? 8 : (left >= 4 ? 4 : 2);
+                g->mradix[mp++] = (int16_t)r;
+                left /= r;
+            }
+            g->mpass = mp;
+        }
+    }
     return true;
+}
+
+// Bluestein tables per (device, N): chirp c[n] = exp(-i pi n^2 / N) (n^2
+// reduced mod 2N exactly) and FFT_M of the circular kernel conj(c[|m|]),
+// both computed in long double on the host.
+std::map<std::pair<int, int>, std::pair<double2*, double2*>> g_blue;
+
+void fft_ld(std::vector<long double>& re, std::vector<long double>& im) {  // in place, radix 2, forward
+    const size_t n = re.size();
+    for (size_t i = 1, j = 0; i < n; ++i) {
+        size_t bit = n >> 1;
+        for (; j & bit; bit >>= 1) j ^= bit;
+        j ^= bit;
+        if (i < j) {
+            std::swap(re[i], re[j]);
+            std::swap(im[i], im[j]);
+        }
+    }
+    const long double pi = 3.141592653589793238462643383279502884L;
+    for (size_t len = 2; len <= n; len <<= 1) {
+        for (size_t k = 0; k < len / 2; ++k) {
+            const long double a = -2.0L * pi * (long double)k / (long double)len;
+            const long double wr = cosl(a), wi = sinl(a);
+            for (size_t i = k; i < n; i += len) {
+                const size_t j = i + len / 2;
+                const long double tr = re[j] * wr - im[j] * wi, ti = re[j] * wi + im[j] * wr;
+                re[j] = re[i] - tr;
+                im[j] = im[i] - ti;
+                re[i] += tr;
+                im[i] += ti;
+            }
+        }
+    }
+}
+
+int finish_geo(int dev, FftGeo* g) {
+    if (!g->blue) return SA_OK;
+    int rc = get_twiddles(dev, g->M, &g->twM);
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto key = std::make_pair(dev, g->N);
+    auto it = g_blue.find(key);
+    if (it == g_blue.end()) {
+        const int64_t N = g->N, M = g->M;
+        const long double pi = 3.141592653589793238462643383279502884L;
+        std::vector<double2> ch((size_t)N);
+        std::vector<long double> hr((size_t)M, 0.0L), hi((size_t)M, 0.0L);
+        for (int64_t n = 0; n < N; ++n) {
+            const int64_t q = (int64_t)(((unsigned __int128)n * (unsigned __int128)n) % (unsigned __int128)(2 * N));
+            const long double a = -pi * (long double)q / (long double)N;
+            const long double c = cosl(a), sn = sinl(a);
+            ch[(size_t)n] = make_double2((double)c, (double)sn);
+            hr[(size_t)n] = c;  // conj(c[n])
+            hi[(size_t)n] = -sn;
+            if (n > 0) {
+                hr[(size_t)(M - n)] = c;
+                hi[(size_t)(M - n)] = -sn;
+            }
+        }
+        fft_ld(hr, hi);
+        std::vector<double2> bf((size_t)M);
+        for (int64_t k = 0; k < M; ++k) bf[(size_t)k] = make_double2((double)hr[(size_t)k], (double)hi[(size_t)k]);
+        double2 *dc = nullptr, *db = nullptr;
+        SA_CUDA(cudaMalloc(&dc, sizeof(double2) * (size_t)N));
+        SA_CUDA(cudaMalloc(&db, sizeof(double2) * (size_t)M));
+        SA_CUDA(cudaMemcpy(dc, ch.data(), sizeof(double2) * (size_t)N, cudaMemcpyHostToDevice));
+        SA_CUDA(cudaMemcpy(db, bf.data(), sizeof(double2) * (size_t)M, cudaMemcpyHostToDevice));
+        it = g_blue.emplace(key, std::make_pair(dc, db)).first;
+    }
+    g->chirp = it->second.first;
+    g->bfft = it->second.second;
+    return SA_OK;
 }
 
 // Plan of a plain N-point complex transform (DCT path).
@@ -699,7 +812,11 @@ int get_dct_twiddles(int dev, int N, const double2** out) {
 }
 
 // doubles per buffer a spectral stage needs at length L
-int64_t fft_lcap(int64_t L) { return (L % 2 == 0) ? L + 2 : 2 * L + 2; }
+// doubles per row buffer for an L-point real transform (Bluestein: M complex)
+int64_t fft_lcap(int64_t L, const FftGeo* g = nullptr) {
+    const int64_t base = (L % 2 == 0) ? L + 2 : 2 * L + 2;
+    return (g && g->blue) ? std::max<int64_t>(base, 2 * (int64_t)g->M + 2) : base;
+}
 
 bool is_spectral(int op) { return op == SA_OP_APP || op == SA_OP_FREQ_MASK || op == SA_OP_SINUSOID; }
 
@@ -778,8 +895,9 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
             if (!make_fft_geo(L, &d.fft))
                 return fail(SA_ERR_UNSUPPORTED, "no FFT plan for length " + std::to_string(L));
             int rc = get_twiddles(dev, (int)L, &d.tw);
+            if (!rc) rc = finish_geo(dev, &d.fft);
             if (rc) return rc;
-            spike_lcap = std::max<int64_t>(spike_lcap, fft_lcap(L));
+            spike_lcap = std::max<int64_t>(spike_lcap, fft_lcap(L, &d.fft));
         }
         if (s.probability == 1.0 && (s.op == SA_OP_CROP || s.op == SA_OP_RESIZE)) L = s.i[0];
         d.len_out = (int32_t)L;
@@ -872,12 +990,13 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
         static std::mutex occ_mu;
         static std::map<std::pair<int, size_t>, int> occ_cache;  // (warps, smem) -> CTAs per SM
         std::lock_guard<std::mutex> lk(occ_mu);
-        auto key = std::make_pair(warps, plan->smem);
+        auto key = std::make_pair(warps * 2 + (plan->global ? 1 : 0), plan->smem);
         auto it = occ_cache.find(key);
         if (it != occ_cache.end()) {
             per_sm = it->second;
         } else {
-            cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chain_kernel, 32 * warps, plan->smem);
+            cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &per_sm, plan->global ? chain_kernel<true> : chain_kernel<false>, 32 * warps, plan->smem);
             if (e != cudaSuccess) return cuda_fail(e, "occupancy");
             occ_cache[key] = per_sm;
         }
@@ -930,7 +1049,8 @@ int launch_chain(Plan* plan, cudaStream_t stream) {
         p.gbuf = gbuf;
         p.bulk_in = 0;  // TMA bulk copies target shared memory only
     }
-    chain_kernel<<<plan->grid, 32 * plan->warps, plan->smem, stream>>>(p);
+    if (plan->global) chain_kernel<true><<<plan->grid, 32 * plan->warps, plan->smem, stream>>>(p);
+    else chain_kernel<false><<<plan->grid, 32 * plan->warps, plan->smem, stream>>>(p);
     SA_CUDA(cudaGetLastError());
     __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
     if (gbuf) SA_CUDA(cudaFreeAsync(gbuf, stream));
@@ -962,8 +1082,8 @@ int flags_status(uint32_t f) {
 // window per CTA in shared memory; when that does not fit, the row buffers
 // go to a global scratch of grid slots (<= 4 GB) and only the window stays.
 int fft_plan_smem(int dev, int64_t L, int* lcap, size_t* smem, int* grid, const void* kern, int64_t n,
-                  bool* global) {
-    *lcap = (int)((fft_lcap(L) + 1) & ~1LL);
+                  bool* global, const FftGeo* geo = nullptr) {
+    *lcap = (int)((fft_lcap(L, geo) + 1) & ~1LL);
     *smem = (size_t)(*lcap) * 8 * 2 + 8 * SA_WIN + 64;
     DeviceState& ds = dev_state(dev);
     *global = *smem > ds.smem_optin || env_int("SA_FORCE_GLOBAL", 0) != 0;
@@ -1173,17 +1293,19 @@ int sa_fft_forward(const double* d_in, int64_t n, int64_t len, double* d_re, dou
     if (!make_fft_geo(len, &p.fft)) return fail(SA_ERR_UNSUPPORTED, "no FFT plan for this length");
     p.x = d_in; p.reo = d_re; p.imo = d_im; p.n = n; p.L = (int32_t)len;
     rc = get_twiddles(dev, (int)len, &p.tw);
+    if (!rc) rc = finish_geo(dev, &p.fft);
     if (rc) return rc;
     size_t smem;
     int lcap, grid;
     bool global;
-    rc = fft_plan_smem(dev, len, &lcap, &smem, &grid, (const void*)rfft_kernel, n, &global);
+    rc = fft_plan_smem(dev, len, &lcap, &smem, &grid, (const void*)rfft_kernel<false>, n, &global, &p.fft);
     if (rc) return rc;
     p.lcap = lcap;
     if (n == 0) return SA_OK;
     rc = alloc_row_bufs(global, lcap, grid, (cudaStream_t)stream, &p.gbuf);
     if (rc) return rc;
-    rfft_kernel<<<grid, 32, smem, (cudaStream_t)stream>>>(p);
+    if (global) rfft_kernel<true><<<grid, 32, smem, (cudaStream_t)stream>>>(p);
+    else rfft_kernel<false><<<grid, 32, smem, (cudaStream_t)stream>>>(p);
     SA_CUDA(cudaGetLastError());
     __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
     if (p.gbuf) SA_CUDA(cudaFreeAsync(p.gbuf, (cudaStream_t)stream));
@@ -1198,17 +1320,19 @@ int sa_fft_inverse(const double* d_re, const double* d_im, int64_t n, int64_t le
     if (!make_fft_geo(len, &p.fft)) return fail(SA_ERR_UNSUPPORTED, "no FFT plan for this length");
     p.re = d_re; p.im = d_im; p.xo = d_out; p.n = n; p.L = (int32_t)len;
     rc = get_twiddles(dev, (int)len, &p.tw);
+    if (!rc) rc = finish_geo(dev, &p.fft);
     if (rc) return rc;
     size_t smem;
     int lcap, grid;
     bool global;
-    rc = fft_plan_smem(dev, len, &lcap, &smem, &grid, (const void*)irfft_kernel, n, &global);
+    rc = fft_plan_smem(dev, len, &lcap, &smem, &grid, (const void*)irfft_kernel<false>, n, &global, &p.fft);
     if (rc) return rc;
     p.lcap = lcap;
     if (n == 0) return SA_OK;
     rc = alloc_row_bufs(global, lcap, grid, (cudaStream_t)stream, &p.gbuf);
     if (rc) return rc;
-    irfft_kernel<<<grid, 32, smem, (cudaStream_t)stream>>>(p);
+    if (global) irfft_kernel<true><<<grid, 32, smem, (cudaStream_t)stream>>>(p);
+    else irfft_kernel<false><<<grid, 32, smem, (cudaStream_t)stream>>>(p);
     SA_CUDA(cudaGetLastError());
     __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
     if (p.gbuf) SA_CUDA(cudaFreeAsync(p.gbuf, (cudaStream_t)stream));
@@ -1225,17 +1349,19 @@ static int dct_launch(const double* d_in, int64_t n, int64_t len, double* d_out,
     rc = get_twiddles(dev, (int)len, &p.tw);
     if (rc) return rc;
     rc = get_dct_twiddles(dev, (int)len, &p.dtw);
+    if (!rc) rc = finish_geo(dev, &p.fft);
     if (rc) return rc;
     size_t smem;
     int lcap, grid;
     bool global;
-    rc = fft_plan_smem(dev, 2 * len, &lcap, &smem, &grid, (const void*)dct_kernel, n, &global);  // 2N + 2 doubles
+    rc = fft_plan_smem(dev, 2 * len, &lcap, &smem, &grid, (const void*)dct_kernel<false>, n, &global, &p.fft);  // 2N + 2 doubles
     if (rc) return rc;
     p.lcap = lcap;
     if (n == 0) return SA_OK;
     rc = alloc_row_bufs(global, lcap, grid, (cudaStream_t)stream, &p.gbuf);
     if (rc) return rc;
-    dct_kernel<<<grid, 32, smem, (cudaStream_t)stream>>>(p);
+    if (global) dct_kernel<true><<<grid, 32, smem, (cudaStream_t)stream>>>(p);
+    else dct_kernel<false><<<grid, 32, smem, (cudaStream_t)stream>>>(p);
     SA_CUDA(cudaGetLastError());
     __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
     if (p.gbuf) SA_CUDA(cudaFreeAsync(p.gbuf, (cudaStream_t)stream));
@@ -1344,13 +1470,14 @@ int sa_augment_spectrum(const sa_stage* stage, uint64_t master_seed, int64_t ser
     size_t smem;
     int lcap, grid;
     bool global;
-    rc = fft_plan_smem(dev, len, &lcap, &smem, &grid, (const void*)spectrum_kernel, n, &global);
+    rc = fft_plan_smem(dev, len, &lcap, &smem, &grid, (const void*)spectrum_kernel<false>, n, &global);
     if (rc) return rc;
     p.lcap = lcap;
     if (n == 0) return SA_OK;
     rc = alloc_row_bufs(global, lcap, grid, (cudaStream_t)stream, &p.gbuf);
     if (rc) return rc;
-    spectrum_kernel<<<grid, 32, smem, (cudaStream_t)stream>>>(p);
+    if (global) spectrum_kernel<true><<<grid, 32, smem, (cudaStream_t)stream>>>(p);
+    else spectrum_kernel<false><<<grid, 32, smem, (cudaStream_t)stream>>>(p);
     SA_CUDA(cudaGetLastError());
     __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
     if (p.gbuf) SA_CUDA(cudaFreeAsync(p.gbuf, (cudaStream_t)stream));

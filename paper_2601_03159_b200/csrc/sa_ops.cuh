@@ -984,6 +984,9 @@ __device__ __forceinline__ void perturb_spectrum(const DevStage& st, WStream& s,
 }
 
 // freqaugment.py:37-47 SpectralAugmenter._apply (time-domain entry)
+#ifndef SA_CHAIN_BLUE
+#define SA_CHAIN_BLUE true
+#endif
 __device__ __forceinline__ bool is_spectral_op(int op) {
     return op == SA_OP_APP || op == SA_OP_FREQ_MASK || op == SA_OP_SINUSOID;
 }
@@ -1005,7 +1008,7 @@ __device__ __forceinline__ bool op_spectral(const DevStage& st, WStream& s, doub
         }
         __syncwarp();
     } else {
-        X = rfft_any(cur, oth, L, st.fft, st.tw, w.lane);
+        X = rfft_any<SA_CHAIN_BLUE>(cur, oth, L, st.fft, st.tw, w.lane);
     }
     double* free_buf = (reinterpret_cast<double*>(X) == cur) ? oth : cur;
     perturb_spectrum(st, s, X, L, free_buf, w);
@@ -1015,7 +1018,7 @@ __device__ __forceinline__ bool op_spectral(const DevStage& st, WStream& s, doub
         return false;
     }
     double2* other = reinterpret_cast<double2*>(free_buf);
-    double* y = irfft_any(X, other, L, st.fft, st.tw, w.lane);
+    double* y = irfft_any<SA_CHAIN_BLUE>(X, other, L, st.fft, st.tw, w.lane);
     if (y != cur) swapbuf(cur, oth);
     return true;
 }

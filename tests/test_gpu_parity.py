@@ -464,3 +464,39 @@ def test_dtw_long_second_series():
     got = dtw_distances(Batch(a), Batch(b))
     for i in range(2):
         assert got[i] == O.dtw(a[i], b[i])[0]
+
+
+@pytest.mark.parametrize("L", [2434, 2722, 10007, 20014])
+def test_bluestein_lengths_match_oracle(L):
+    """Lengths whose FFT has a large prime factor (1217, 1361, 10007) take the
+    Bluestein path: transforms, DCT and spectral chain stay within the FFT
+    tolerance of the oracle, and round trips within 1e-9."""
+    from oracle import oracle as O
+    from paper_2601_03159_b200 import Batch, FrequencyMask, Pipeline, RandomSinusoid, dct_forward, dct_inverse
+    from paper_2601_03159_b200 import fft_forward, fft_inverse
+    from sa_testutil import assert_matches
+
+    x = np.cumsum(np.random.default_rng(L).normal(0, 1, (3, L)), axis=1)
+    spec = fft_forward(Batch(x))
+    re, im = O.fft_forward(x)
+    assert_matches(spec.re, re, exact=False, what="re")
+    assert_matches(spec.im, im, exact=False, what="im")
+    assert np.abs(fft_inverse(spec).values - x).max() <= 1e-9 * np.abs(x).max()
+    assert np.abs(dct_inverse(dct_forward(Batch(x))).values - x).max() <= 1e-9 * np.abs(x).max()
+    pipe = Pipeline(stages=(FrequencyMask(max(1, L // 40)), RandomSinusoid(1.0)), master_seed=6)
+    assert_matches(pipe.run(Batch(x)).values, O.run_pipeline(pipe, x), exact=False, what="chain")
+
+
+def test_bluestein_forced_matches_generic(monkeypatch):
+    """SA_BLUESTEIN=2 forces Bluestein on every non-power-of-two length: same
+    results as the mixed-radix plan to FFT tolerance."""
+    from paper_2601_03159_b200 import Batch, fft_forward
+    from sa_testutil import assert_matches
+
+    x = np.cumsum(np.random.default_rng(3).normal(0, 1, (4, 1500)), axis=1)
+    monkeypatch.setenv("SA_BLUESTEIN", "1")
+    a = fft_forward(Batch(x))
+    monkeypatch.setenv("SA_BLUESTEIN", "2")
+    b = fft_forward(Batch(x))
+    assert_matches(b.re, a.re, exact=False, what="re")
+    assert_matches(b.im, a.im, exact=False, what="im")
