@@ -411,9 +411,10 @@ struct DtwParams {
 };
 
 // one warp per pair: distance only
+template <bool GMEM>
 __global__ void __launch_bounds__(32) dtw_batch_kernel(const __grid_constant__ DtwParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
-    double* prow = p.gprow ? p.gprow + (int64_t)blockIdx.x * p.m : reinterpret_cast<double*>(smem);
+    double* prow = GMEM ? p.gprow + (int64_t)blockIdx.x * p.m : reinterpret_cast<double*>(smem);
     for (int64_t q = blockIdx.x; q < p.pairs; q += gridDim.x) {
         const double d = dtw_warp(p.a + q * p.n, p.n, p.b + q * p.m, p.m, prow, nullptr, threadIdx.x, p.stage_b != 0);
         if (threadIdx.x == 0) p.dist[q] = d;
@@ -422,9 +423,10 @@ __global__ void __launch_bounds__(32) dtw_batch_kernel(const __grid_constant__ D
 }
 
 // one pair with the full matrix and the reference's backtracked path
+template <bool GMEM>
 __global__ void __launch_bounds__(32) dtw_path_kernel(const __grid_constant__ DtwParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
-    double* prow = p.gprow ? p.gprow : reinterpret_cast<double*>(smem);
+    double* prow = GMEM ? p.gprow : reinterpret_cast<double*>(smem);
     const double d = dtw_warp(p.a, p.n, p.b, p.m, prow, p.acc, threadIdx.x, p.stage_b != 0);
     __syncwarp();
     __threadfence_block();
@@ -600,8 +602,10 @@ int init_device(int dev) {
     SA_CUDA(cudaFuncSetAttribute(spectrum_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(dct_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(dct_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-    SA_CUDA(cudaFuncSetAttribute(dtw_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-    SA_CUDA(cudaFuncSetAttribute(dtw_path_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(dtw_batch_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(dtw_batch_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(dtw_path_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(dtw_path_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaSetDevice(prev));
     ds.ready = true;
     return SA_OK;
@@ -1391,10 +1395,11 @@ int sa_dtw_batch(const double* d_a, const double* d_b, int64_t n_pairs, int64_t 
     p.stage_b = 0;  // b from L1: staging it halves the resident warps (measured slower)
     if (n_pairs == 0) return SA_OK;
     int per_sm = 0;
-    SA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dtw_batch_kernel, 32, smem));
+    SA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dtw_batch_kernel<false>, 32, smem));
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ds.sms * std::max(per_sm, 1), n_pairs));
     if (global) SA_CUDA(cudaMallocAsync(&p.gprow, sizeof(double) * (size_t)len_b * grid, (cudaStream_t)stream));
-    dtw_batch_kernel<<<grid, 32, smem, (cudaStream_t)stream>>>(p);
+    if (global) dtw_batch_kernel<true><<<grid, 32, smem, (cudaStream_t)stream>>>(p);
+    else dtw_batch_kernel<false><<<grid, 32, smem, (cudaStream_t)stream>>>(p);
     SA_CUDA(cudaGetLastError());
     __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
     if (p.gprow) SA_CUDA(cudaFreeAsync(p.gprow, (cudaStream_t)stream));
@@ -1417,7 +1422,8 @@ int sa_dtw_path(const double* d_a, int64_t len_a, const double* d_b, int64_t len
     p.stage_b = 0;
     p.pairs = 1; p.n = (int32_t)len_a; p.m = (int32_t)len_b;
     if (global) SA_CUDA(cudaMallocAsync(&p.gprow, sizeof(double) * (size_t)len_b, (cudaStream_t)stream));
-    dtw_path_kernel<<<1, 32, smem, (cudaStream_t)stream>>>(p);
+    if (global) dtw_path_kernel<true><<<1, 32, smem, (cudaStream_t)stream>>>(p);
+    else dtw_path_kernel<false><<<1, 32, smem, (cudaStream_t)stream>>>(p);
     SA_CUDA(cudaGetLastError());
     __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
     if (p.gprow) SA_CUDA(cudaFreeAsync(p.gprow, (cudaStream_t)stream));
