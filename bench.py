@@ -426,7 +426,7 @@ def run_side_reference(args, rank):
         base = [transforms_cpu(host) for _ in range(args.steps)]
         metric, unit, wl = "transformed points/s", "points/s", TR_WORKLOAD
     else:
-        a = host_input(2, 64)
+        a = host_input(2, 32 * (os.cpu_count() or 1))
         b = a[:, ::-1].copy()
         for _ in range(args.warmup):
             dtw_cpu(a, b, pairs=8)
@@ -751,7 +751,7 @@ def dtw_cpu(a, b, pairs=None):
     from oracle import oracle as O
 
     threads = os.cpu_count() or 1
-    pairs = pairs or 32 * threads
+    pairs = min(pairs or 32 * threads, a.shape[0])
     t0 = time.perf_counter()
     with ThreadPoolExecutor(threads) as ex:
         list(ex.map(lambda i: O.dtw(a[i], b[i]), range(pairs)))
