@@ -10,7 +10,6 @@ reference bit for bit.
 
 from __future__ import annotations
 
-import ctypes
 from dataclasses import dataclass
 
 import numpy as np

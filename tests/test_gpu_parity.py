@@ -314,8 +314,6 @@ def test_config5_sweep_vs_oracle():
     (almost) exactly zero bin at APP's input has a rounding-determined phase
     that APP turns into magnitude ~sigma_amp; such rows are
     checked to have that cause."""
-    import dataclasses
-
     import bench_inputs
 
     total, excused = 0, 0

@@ -8,10 +8,9 @@ cases must match bitwise; FFT cases within tests/conftest.spectral_tol.
 """
 
 import numpy as np
-import pytest
 
 from oracle import oracle as O
-from paper_2601_03159_b200 import Batch, Jitter, Pipeline, stage_from_dict
+from paper_2601_03159_b200 import Jitter, Pipeline, stage_from_dict
 from paper_2601_03159_b200.pipeline import lower_stages
 from sa_testutil import assert_matches, spectral_tol
 
