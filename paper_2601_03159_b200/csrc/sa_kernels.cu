@@ -1024,20 +1024,36 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
 
 // Schedule (fire-pattern counting sort) and launch the chain kernel for the
 // rows described by plan->p (in/out/flags/offset/rows_out already set).
+// stream-ordered scratch freed on every return path
+struct StreamScratch {
+    cudaStream_t st;
+    std::vector<void*> ptrs;
+    explicit StreamScratch(cudaStream_t s) : st(s) {}
+    template <class T>
+    cudaError_t alloc(T** p, size_t bytes) {
+        cudaError_t e = cudaMallocAsync((void**)p, bytes, st);
+        if (e == cudaSuccess) ptrs.push_back(*p);
+        return e;
+    }
+    ~StreamScratch() {
+        for (void* q : ptrs) cudaFreeAsync(q, st);
+    }
+};
+
 int launch_chain(Plan* plan, cudaStream_t stream) {
     ChainParams& p = plan->p;
     if (p.rows_out == 0) return SA_OK;
     DeviceState& ds = dev_state(current_device_id());
-    uint32_t* keys = nullptr;
-    uint32_t* hist = nullptr;
-    int32_t* order = nullptr;
+    StreamScratch scratch(stream);
     p.order = nullptr;
     while (p.key_bits > 0 && ((int64_t)1 << p.key_bits) > 4 * p.rows_out) --p.key_bits;
     if (p.key_bits > 0) {
         const int nb = 1 << p.key_bits;
-        SA_CUDA(cudaMallocAsync(&keys, sizeof(uint32_t) * (size_t)p.rows_out, stream));
-        SA_CUDA(cudaMallocAsync(&hist, sizeof(uint32_t) * (size_t)nb, stream));
-        SA_CUDA(cudaMallocAsync(&order, sizeof(int32_t) * (size_t)p.rows_out, stream));
+        uint32_t *keys, *hist;
+        int32_t* order;
+        SA_CUDA(scratch.alloc(&keys, sizeof(uint32_t) * (size_t)p.rows_out));
+        SA_CUDA(scratch.alloc(&hist, sizeof(uint32_t) * (size_t)nb));
+        SA_CUDA(scratch.alloc(&order, sizeof(int32_t) * (size_t)p.rows_out));
         SA_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (size_t)nb, stream));
         const int g = (int)std::min<int64_t>((int64_t)ds.sms * 8, (p.rows_out + 255) / 256);
         key_hist_kernel<<<g, 256, 0, stream>>>(p, keys, hist);
@@ -1047,22 +1063,14 @@ int launch_chain(Plan* plan, cudaStream_t stream) {
         __atomic_add_fetch(&g_launches, 3, __ATOMIC_RELAXED);
         p.order = order;
     }
-    double* gbuf = nullptr;
     if (plan->global) {
-        SA_CUDA(cudaMallocAsync(&gbuf, sizeof(double) * 2 * (size_t)p.lcap * (size_t)plan->grid * plan->warps, stream));
-        p.gbuf = gbuf;
+        SA_CUDA(scratch.alloc(&p.gbuf, sizeof(double) * 2 * (size_t)p.lcap * (size_t)plan->grid * plan->warps));
         p.bulk_in = 0;  // TMA bulk copies target shared memory only
     }
     if (plan->global) chain_kernel<true><<<plan->grid, 32 * plan->warps, plan->smem, stream>>>(p);
     else chain_kernel<false><<<plan->grid, 32 * plan->warps, plan->smem, stream>>>(p);
     SA_CUDA(cudaGetLastError());
     __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
-    if (gbuf) SA_CUDA(cudaFreeAsync(gbuf, stream));
-    if (keys) {
-        SA_CUDA(cudaFreeAsync(keys, stream));
-        SA_CUDA(cudaFreeAsync(hist, stream));
-        SA_CUDA(cudaFreeAsync(order, stream));
-    }
     return SA_OK;
 }
 
