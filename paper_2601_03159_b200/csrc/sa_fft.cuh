@@ -276,16 +276,22 @@ __device__ __forceinline__ double2* rfft_any(double* xa, double* xb, int L, cons
                                             int lane) {
     double2* za = reinterpret_cast<double2*>(xa);
     double2* zb = reinterpret_cast<double2*>(xb);
-    if (!g.packed) {  // odd L: complexify into xb, N = L transform, keep bins
+    // odd L: complexify into xb and take the N = L transform; even L: view
+    // the real series as N = L/2 complex points (one call site either way,
+    // to keep the FFT's code emitted once)
+    if (!g.packed) {
         for (int n = lane; n < L; n += 32) zb[n] = make_double2(xa[n], 0.0);
         __syncwarp();
-        double2* Z = fft_any<BLUE>(zb, za, g, tw, L, lane);
+    }
+    double2* s0 = g.packed ? za : zb;
+    double2* d0 = g.packed ? zb : za;
+    double2* Z = fft_any<BLUE>(s0, d0, g, tw, L, lane);  // one call site: the FFT is emitted once
+    if (!g.packed) {
         if (lane == 0) Z[0].y = 0.0;
         __syncwarp();
         return Z;
     }
     const int M = L >> 1;
-    double2* Z = fft_any<BLUE>(za, zb, g, tw, L, lane);
     double2* X = (Z == za) ? zb : za;
     for (int k = lane; k <= M; k += 32) {
         double2 zk = Z[k == M ? 0 : k];
@@ -312,6 +318,7 @@ __device__ __forceinline__ double2* rfft_any(double* xa, double* xb, int L, cons
 template <bool BLUE = true>
 __device__ __forceinline__ double* irfft_any(double2* X, double2* other, int L, const FftGeo& g, const double2* tw,
                                             int lane) {
+    const int M = L >> 1;
     if (!g.packed) {  // odd L: Hermitian completion, full transform, real part
         const int bins = L / 2 + 1;
         for (int k = lane; k < bins; k += 32) {
@@ -320,29 +327,29 @@ __device__ __forceinline__ double* irfft_any(double2* X, double2* other, int L, 
             other[k] = make_double2(v.x, -v.y);
             if (k > 0) other[L - k] = v;
         }
-        __syncwarp();
-        double2* Z = fft_any<BLUE>(other, X, g, tw, L, lane);
+    } else {  // even L: fold the half spectrum into M complex points
+        for (int k = lane; k < M; k += 32) {
+            double2 xk = X[k];
+            double2 xc = X[M - k];
+            if (k == 0) { xk.y = 0.0; xc.y = 0.0; }
+            xc.y = -xc.y;
+            double er = 0.5 * (xk.x + xc.x), ei = 0.5 * (xk.y + xc.y);
+            double dr = 0.5 * (xk.x - xc.x), di = 0.5 * (xk.y - xc.y);
+            double2 w = __ldg(&tw[k]);
+            w.y = -w.y;
+            double2 o = cmul(make_double2(dr, di), w);
+            other[k] = make_double2(er - o.y, -(ei + o.x));
+        }
+    }
+    __syncwarp();
+    double2* Z = fft_any<BLUE>(other, X, g, tw, L, lane);  // one call site: the FFT is emitted once
+    if (!g.packed) {
         double* out = reinterpret_cast<double*>(Z == X ? other : X);
         const double s = 1.0 / (double)L;
         for (int n = lane; n < L; n += 32) out[n] = Z[n].x * s;
         __syncwarp();
         return out;
     }
-    const int M = L >> 1;
-    for (int k = lane; k < M; k += 32) {
-        double2 xk = X[k];
-        double2 xc = X[M - k];
-        if (k == 0) { xk.y = 0.0; xc.y = 0.0; }
-        xc.y = -xc.y;
-        double er = 0.5 * (xk.x + xc.x), ei = 0.5 * (xk.y + xc.y);
-        double dr = 0.5 * (xk.x - xc.x), di = 0.5 * (xk.y - xc.y);
-        double2 w = __ldg(&tw[k]);
-        w.y = -w.y;
-        double2 o = cmul(make_double2(dr, di), w);
-        other[k] = make_double2(er - o.y, -(ei + o.x));
-    }
-    __syncwarp();
-    double2* Z = fft_any<BLUE>(other, X, g, tw, L, lane);
     const double s = 1.0 / (double)M;
     for (int k = lane; k < M; k += 32) {
         double2 z = Z[k];
