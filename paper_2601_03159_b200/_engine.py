@@ -10,6 +10,7 @@ memory and streams.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 
@@ -37,27 +38,69 @@ def _ptr(a: np.ndarray) -> int:
     return a.ctypes.data
 
 
+def devices_for(parallel: bool) -> list[int]:
+    """The GPUs a host-buffer call uses: the current one, or -- for the
+    reference's ``parallel=True`` -- every visible one (SA_DEVICES, a comma
+    list, overrides; repeats are allowed and only exercise the sharding)."""
+    env = os.environ.get("SA_DEVICES")
+    if env:
+        return [int(d) for d in env.split(",") if d.strip()]
+    dev = _native.current_device()
+    if not parallel:
+        return [dev]
+    import torch
+
+    return list(range(torch.cuda.device_count())) or [dev]
+
+
 def run_host(stages, values: np.ndarray, seed: int, first_index: int = 0, series_offset: int = 0,
              len_out: int | None = None, check_finite: bool = True, repeat_rows: bool = True,
-             out: np.ndarray | None = None) -> np.ndarray:
-    """Run `stages` over a host (n, L) float64 batch; returns a new array."""
+             out: np.ndarray | None = None, devices: list[int] | None = None) -> np.ndarray:
+    """Run `stages` over a host (n, L) float64 batch; returns a new array.
+    With several `devices` the rows are split into contiguous ranges, one
+    host thread per range, each passing its global first row as the series
+    offset (sharding.py) -- bitwise the single-device result."""
     values = np.ascontiguousarray(values, dtype=np.float64)
     n, L = values.shape
     _native.current_device()
     arr, aux = _lower(stages, first_index, repeat_rows)
-    rows = n * _row_factor(stages, repeat_rows)
+    r = _row_factor(stages, repeat_rows)
+    rows = n * r
     L_out = L if len_out is None else int(len_out)
     if out is None:
         out = np.empty((rows, L_out), dtype=np.float64)
     elif out.shape != (rows, L_out) or out.dtype != np.float64 or not out.flags.c_contiguous:
         raise ValueError(f"out must be a C-contiguous float64 array of shape {(rows, L_out)}")
-    rc = _native.lib().sa_pipeline_run_host(
-        arr, len(stages), aux.ctypes.data_as(ctypes.c_void_p), aux.size, int(seed),
-        int(series_offset), _ptr(values), n, L, _ptr(out), L_out,
-    )
-    if rc == _abi.SA_ERR_NONFINITE and not check_finite:
-        return out
-    _native.check(rc, "sa_pipeline_run_host")
+    devices = devices or [_native.current_device()]
+    aux_p = aux.ctypes.data_as(ctypes.c_void_p)
+
+    def shard(k: int) -> int:
+        from .sharding import shard_range
+
+        lo, hi = shard_range(n, k, len(devices))
+        if hi == lo:
+            return _abi.SA_OK
+        if len(devices) > 1:
+            import torch
+
+            torch.cuda.set_device(devices[k])
+            _native.ensure_device(devices[k])
+        return _native.lib().sa_pipeline_run_host(
+            arr, len(stages), aux_p, aux.size, int(seed), int(series_offset) + lo,
+            _ptr(values) + 8 * lo * L, hi - lo, L, _ptr(out) + 8 * lo * r * L_out, L_out,
+        )
+
+    if len(devices) == 1:
+        rcs = [shard(0)]
+    else:
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(len(devices)) as ex:
+            rcs = list(ex.map(shard, range(len(devices))))
+    for rc in rcs:
+        if rc == _abi.SA_ERR_NONFINITE and not check_finite:
+            continue
+        _native.check(rc, "sa_pipeline_run_host")
     return out
 
 

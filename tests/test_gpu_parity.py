@@ -498,3 +498,24 @@ def test_bluestein_forced_matches_generic(monkeypatch):
     b = fft_forward(Batch(x))
     assert_matches(b.re, a.re, exact=False, what="re")
     assert_matches(b.im, a.im, exact=False, what="im")
+
+
+def test_parallel_shards_across_devices_bitwise(monkeypatch):
+    """parallel=True shards rows over the visible GPUs (one host thread per
+    range, global series offsets); SA_DEVICES=0,0,0 runs three shards on one
+    GPU to exercise the split, including a Repeat that expands rows."""
+    import dataclasses
+
+    from paper_2601_03159_b200 import Batch, Repeat
+
+    x = np.cumsum(np.random.default_rng(12).normal(0, 1, (301, 257)), axis=1)
+    base = _exact_chain(seed=8)
+    pipe = dataclasses.replace(base, stages=base.stages + (Repeat(3),))
+    want = pipe.run(Batch(x)).values
+    got_par = dataclasses.replace(pipe, parallel=True).run(Batch(x)).values
+    monkeypatch.setenv("SA_DEVICES", "0,0,0")
+    got_split = pipe.run(Batch(x)).values
+    one = base.stages[0].augment_batch(Batch(x), 8, parallel=True)
+    monkeypatch.delenv("SA_DEVICES")
+    assert np.array_equal(got_par, want) and np.array_equal(got_split, want)
+    assert np.array_equal(one.values, base.stages[0].augment_batch(Batch(x), 8).values)
