@@ -271,6 +271,9 @@ int sa_augment_spectrum(const sa_stage* stage, uint64_t master_seed, int64_t ser
                         double* d_re_out, double* d_im_out, void* stream);
 
 /* ---- page-locked host memory helpers (for zero-staging host batches) ---- */
+/* memcpy between host buffers on the host-staging runtime's copy threads
+ * (what the *_host entry points use to fill their page-locked staging). */
+int sa_host_copy(void* dst, const void* src, int64_t bytes);
 int sa_host_alloc(void** ptr, int64_t bytes);
 int sa_host_free(void* ptr);
 

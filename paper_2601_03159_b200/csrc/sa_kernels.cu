@@ -1499,6 +1499,12 @@ int sa_augment_spectrum(const sa_stage* stage, uint64_t master_seed, int64_t ser
     return SA_OK;
 }
 
+int sa_host_copy(void* dst, const void* src, int64_t bytes) {
+    if (bytes < 0 || (bytes > 0 && (!dst || !src))) return fail(SA_ERR_INVALID_ARG, "sa_host_copy: bad arguments");
+    CopyPool::get().copy(dst, src, (size_t)bytes);
+    return SA_OK;
+}
+
 int sa_host_alloc(void** ptr, int64_t bytes) {
     SA_CUDA(cudaHostAlloc(ptr, (size_t)bytes, cudaHostAllocPortable));
     return SA_OK;

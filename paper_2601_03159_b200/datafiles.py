@@ -114,11 +114,51 @@ def _to_device_bytes(data, dev):
         host = _staging_buffer(n)
         src = np.frombuffer(mv, dtype=np.uint8)
         if not np.shares_memory(src, host):
-            host[:n] = src
+            _copy(host[:n], src)
             src = host[:n]
         d.copy_(torch.from_numpy(src), non_blocking=True)
         torch.cuda.current_stream(dev).synchronize()
     return d, n
+
+
+def _copy(dst: np.ndarray, src: np.ndarray) -> None:
+    """Host memcpy on the runtime's copy threads (sa_host_copy)."""
+    _native.check(_native.lib().sa_host_copy(_vp(dst.ctypes.data), _vp(src.ctypes.data), src.nbytes),
+                  "sa_host_copy")
+
+
+def _to_numpy(t) -> np.ndarray:
+    """A CUDA tensor -> a fresh numpy array: D2H into the pinned staging
+    buffer, then a parallel host copy (a pageable D2H runs at a few GB/s)."""
+    import torch
+
+    n = t.numel() * t.element_size()
+    out = np.empty(tuple(t.shape), dtype=np.dtype(str(t.dtype).replace("torch.", "")))
+    if n == 0:
+        return out
+    with _staging_lock:
+        host = _staging_buffer(n)
+        torch.from_numpy(host[:n]).copy_(t.contiguous().view(torch.uint8).reshape(-1), non_blocking=True)
+        torch.cuda.current_stream(t.device.index).synchronize()
+        _copy(out.reshape(-1).view(np.uint8), host[:n])
+    return out
+
+
+def _to_cuda(a: np.ndarray, dev: int):
+    """A host array -> a CUDA tensor through the pinned staging buffer."""
+    import torch
+
+    a = np.ascontiguousarray(a)
+    d = torch.empty(a.shape, dtype=getattr(torch, a.dtype.name), device=f"cuda:{dev}")
+    n = a.nbytes
+    if n == 0:
+        return d
+    with _staging_lock:
+        host = _staging_buffer(n)
+        _copy(host[:n], a.reshape(-1).view(np.uint8))
+        d.view(torch.uint8).reshape(-1).copy_(torch.from_numpy(host[:n]), non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+    return d
 
 
 def _split_joined(buf: bytes, count: int) -> tuple[str, ...]:
@@ -227,7 +267,7 @@ def parse_dataset(text: str, fmt: Optional[str] = None) -> DatasetFile:
 
 
 def _to_host(dd: DeviceDataset) -> DatasetFile:
-    values = dd.values.cpu().numpy()
+    values = _to_numpy(dd.values)
     return DatasetFile(batch=Batch._from_device_checked(values), format=dd.format,
                        header_lines=dd.header_lines, labels=dd.labels)
 
@@ -358,7 +398,7 @@ def format_dataset(ds: DatasetFile) -> str:
     import torch
 
     dev = _native.current_device()
-    values = torch.from_numpy(np.ascontiguousarray(ds.batch.values)).to(f"cuda:{dev}")
+    values = _to_cuda(ds.batch.values, dev)
     labels = ds.labels
     out = format_dataset_to_device(values, ds.format, ds.header_lines, labels)
     return _fetch(out, lambda mv: str(mv, "utf-8", "surrogatepass"))
@@ -369,7 +409,7 @@ def write_dataset(path, ds: DatasetFile) -> None:
     import torch
 
     dev = _native.current_device()
-    values = torch.from_numpy(np.ascontiguousarray(ds.batch.values)).to(f"cuda:{dev}")
+    values = _to_cuda(ds.batch.values, dev)
     _write_device(path, format_dataset_to_device(values, ds.format, ds.header_lines, ds.labels), ds)
 
 
