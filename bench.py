@@ -132,6 +132,14 @@ def ncu_traffic(cfg):
     return None
 
 
+def ncu_instructions(cfg):
+    p = os.path.join(ROOT, "profiles", "ncu_instructions.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return json.load(fh).get(f"config{cfg}")
+    return None
+
+
 def cpu_baseline(cfg: int, pipe, L_in: int, target_s: float = 8.0, threads: int | None = None):
     """The C oracle (reference algorithm restated, oracle/sa_oracle.c) on a
     bounded sample of the workload, all host threads."""
@@ -309,6 +317,19 @@ def run_b200(args, rank, world, local_rank):
         "gpu_launches": int(launches_all),
         "clocks": clk.summary(),
     }
+    # the kernel is issue bound (numpy-exact RNG and FP64 arithmetic per element):
+    # warp-instructions per launch (ncu capture of this build) over the live
+    # kernel time, against 4 issue slots x SMs x the sampled SM clock
+    instr = ncu_instructions(cfg)
+    if instr and cfg == 5 and N == CONFIG_SHAPES[5][0]:
+        sm_mhz = line["clocks"].get("sm_mhz") or 1965.0
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        peak_issue = 4.0 * sms * sm_mhz * 1e6
+        ach_issue = instr / world / (kern_ms / 1e3)
+        line["issue_roofline"] = {"achieved": ach_issue, "peak": peak_issue, "unit": "warp-instructions/s",
+                                  "frac": ach_issue / peak_issue,
+                                  "instructions_per_launch": instr / world,
+                                  "source": "profiles/ncu_instructions.json (ncu smsp__inst_executed.sum)"}
     if e2e_s is not None:
         line["e2e"] = {"value": pts / e2e_max, "unit": UNIT, "h2d_bytes_per_step": h2d * world,
                        "d2h_bytes_per_step": d2h * world}
