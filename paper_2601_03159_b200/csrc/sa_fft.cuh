@@ -362,27 +362,27 @@ __device__ __forceinline__ double* irfft_any(double2* X, double2* other, int L, 
 
 // ---------------------------------------------------------------- DCT
 // Orthonormal DCT-II / DCT-III (scipy.fft.dct / idct, type 2, norm="ortho";
-// reference freqtransform.py:91-98) of length N through one N-point complex
-// FFT (Makhoul): v[n] = x[2n], v[N-1-n] = x[2n+1], V = FFT(v),
+// reference freqtransform.py:91-98) of length N through one real FFT of
+// length N (Makhoul): v[n] = x[2n], v[N-1-n] = x[2n+1] is real, so its
+// spectrum V is Hermitian and the packed real transform (rfft_any: N/2
+// complex points for even N) gives V[0 .. N/2]; V[k] = conj(V[N-k]) above.
 //   S[k] = Re(e^{-i pi k / 2N} V[k]),  y[k] = g_k S[k],
 //   g_0 = 1/sqrt(N), g_k = sqrt(2/N);
-// inverse: e^{-i pi k / 2N} V[k] = S[k] - i S[N-k] (S[N] = 0), v = IFFT(V).
-// dtw[k] = e^{-i pi k / 2N} (k < N), tw = exp(-2 pi i q / N) (q < N).
-// Buffers xa, xb hold >= 2N + 2 doubles.  Returns the buffer with the result.
+// inverse: V[k] = e^{+i pi k / 2N} (S[k] - i S[N-k]) (S[N] = 0) for
+// k <= N/2, v = irfft(V).  dtw[k] = e^{-i pi k / 2N} (k < N); g / tw: the
+// real-FFT plan and table of length N.  Buffers xa, xb hold the real-FFT
+// capacity (N + 2 doubles for even N).  Returns the buffer with the result.
 __device__ __forceinline__ double* dct2_any(double* xa, double* xb, int N, const FftGeo& g, const double2* tw,
                                            const double2* dtw, int lane) {
-    double2* vb = reinterpret_cast<double2*>(xb);
-    for (int n = lane; n < N; n += 32) {
-        const int src = (2 * n < N) ? 2 * n : 2 * (N - 1 - n) + 1;
-        vb[n] = make_double2(xa[src], 0.0);
-    }
+    for (int n = lane; n < N; n += 32) xb[n] = xa[(2 * n < N) ? 2 * n : 2 * (N - 1 - n) + 1];
     __syncwarp();
-    double2* V = fft_any(vb, reinterpret_cast<double2*>(xa), g, tw, N, lane);
-    double* y = reinterpret_cast<double*>(V == vb ? reinterpret_cast<double2*>(xa) : vb);
+    double2* V = rfft_any(xb, xa, N, g, tw, lane);
+    double* y = (reinterpret_cast<double*>(V) == xa) ? xb : xa;
     const double g0 = 1.0 / sqrt((double)N), gk = sqrt(2.0 / (double)N);
     for (int k = lane; k < N; k += 32) {
         const double2 w = __ldg(&dtw[k]);
-        const double2 v = V[k];
+        double2 v = V[2 * k <= N ? k : N - k];
+        v.y = 2 * k <= N ? v.y : -v.y;
         y[k] = (k == 0 ? g0 : gk) * (v.x * w.x - v.y * w.y);
     }
     __syncwarp();
@@ -393,22 +393,17 @@ __device__ __forceinline__ double* dct3_any(double* ya, double* yb, int N, const
                                            const double2* dtw, int lane) {
     double2* V = reinterpret_cast<double2*>(yb);
     const double i0 = sqrt((double)N), ik = sqrt((double)N / 2.0);
-    for (int k = lane; k < N; k += 32) {
+    for (int k = lane; 2 * k <= N; k += 32) {
         const double sk = ya[k] * (k == 0 ? i0 : ik);
         const double snk = (k == 0) ? 0.0 : ya[N - k] * ik;
         double2 w = __ldg(&dtw[k]);
         w.y = -w.y;  // e^{+i pi k / 2N}
-        const double2 z = cmul(make_double2(sk, -snk), w);
-        V[k] = make_double2(z.x, -z.y);  // conj, so the forward passes give conj(IFFT)*N
+        V[k] = cmul(make_double2(sk, -snk), w);
     }
     __syncwarp();
-    double2* Z = fft_any(V, reinterpret_cast<double2*>(ya), g, tw, N, lane);
-    double* x = reinterpret_cast<double*>(Z == V ? reinterpret_cast<double2*>(ya) : V);
-    const double s = 1.0 / (double)N;
-    for (int n = lane; n < N; n += 32) {
-        const int dst = (2 * n < N) ? 2 * n : 2 * (N - 1 - n) + 1;
-        x[dst] = Z[n].x * s;
-    }
+    double* v = irfft_any(V, reinterpret_cast<double2*>(ya), N, g, tw, lane);
+    double* x = (v == ya) ? yb : ya;
+    for (int n = lane; n < N; n += 32) x[(2 * n < N) ? 2 * n : 2 * (N - 1 - n) + 1] = v[n];
     __syncwarp();
     return x;
 }

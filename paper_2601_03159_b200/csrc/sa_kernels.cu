@@ -779,17 +779,6 @@ int finish_geo(int dev, FftGeo* g) {
     return SA_OK;
 }
 
-// Plan of a plain N-point complex transform (DCT path).
-bool make_fft_geo_complex(int64_t N, FftGeo* g) {
-    if (N < 1) return false;
-    // reuse the factorisation with an odd-length "real" geometry: N stays N
-    if (!make_fft_geo(N % 2 ? N : 2 * N, g)) return false;
-    if (N % 2 == 0) {  // make_fft_geo(2N) planned an N-point transform, packed
-        g->packed = 0;
-    }
-    g->N = (int32_t)N;
-    return true;
-}
 
 std::map<std::pair<int, int>, double2*> g_dct_tw;  // (device, N) -> exp(-i pi k / 2N)
 
@@ -1356,7 +1345,7 @@ static int dct_launch(const double* d_in, int64_t n, int64_t len, double* d_out,
     int rc = ensure_device(&dev);
     if (rc) return rc;
     FftParams p{};
-    if (len < 1 || !make_fft_geo_complex(len, &p.fft)) return fail(SA_ERR_UNSUPPORTED, "no DCT plan for this length");
+    if (len < 1 || !make_fft_geo(len, &p.fft)) return fail(SA_ERR_UNSUPPORTED, "no DCT plan for this length");
     p.x = d_in; p.xo = d_out; p.n = n; p.L = (int32_t)len; p.inverse = inverse;
     rc = get_twiddles(dev, (int)len, &p.tw);
     if (rc) return rc;
@@ -1366,7 +1355,7 @@ static int dct_launch(const double* d_in, int64_t n, int64_t len, double* d_out,
     size_t smem;
     int lcap, grid;
     bool global;
-    rc = fft_plan_smem(dev, 2 * len, &lcap, &smem, &grid, (const void*)dct_kernel<false>, n, &global, &p.fft);  // 2N + 2 doubles
+    rc = fft_plan_smem(dev, len, &lcap, &smem, &grid, (const void*)dct_kernel<false>, n, &global, &p.fft);
     if (rc) return rc;
     p.lcap = lcap;
     if (n == 0) return SA_OK;
