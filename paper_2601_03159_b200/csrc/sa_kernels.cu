@@ -342,6 +342,42 @@ __device__ __forceinline__ double* row_bufs(unsigned char* smem, double* gbuf, i
     return GMEM ? gbuf + (int64_t)blockIdx.x * 2 * (int64_t)lcap : reinterpret_cast<double*>(smem);
 }
 
+// Row input of the one-warp transform kernels.  In shared-memory mode with
+// 16-byte rows, the next row is prefetched by a TMA bulk copy into the buffer
+// the current transform leaves free, so the load overlaps this row's output
+// stores (the kernels were bound on these loads at ~6 warps per SM).
+struct RowPrefetch {
+    uint64_t* bar;
+    uint32_t phase, bytes;
+    bool bulk;
+    __device__ __forceinline__ void start(double* dst, const double* src, int lane) {
+        if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(bar, bytes);
+            bulk_g2s(dst, src, bytes, bar);
+        }
+    }
+    __device__ __forceinline__ void wait() {
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+    }
+};
+
+template <bool GMEM>
+__device__ __forceinline__ RowPrefetch row_prefetch_init(unsigned char* smem, const FftParams& p, double* A, int lane) {
+    RowPrefetch rp;
+    rp.bar = reinterpret_cast<uint64_t*>(smem + 16 * (size_t)p.lcap);  // after the two buffers
+    rp.phase = 0;
+    rp.bytes = 8u * (uint32_t)p.L;
+    rp.bulk = !GMEM && (p.L % 2 == 0) && ((reinterpret_cast<uintptr_t>(p.x) & 15) == 0);
+    if (rp.bulk) {
+        if (lane == 0) mbar_init(rp.bar, 1);
+        __syncwarp();
+        if (blockIdx.x < p.n) rp.start(A, p.x + (int64_t)blockIdx.x * p.L, lane);
+    }
+    return rp;
+}
+
 template <bool GMEM>
 __global__ void __launch_bounds__(32) rfft_kernel(const __grid_constant__ FftParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -349,16 +385,28 @@ __global__ void __launch_bounds__(32) rfft_kernel(const __grid_constant__ FftPar
     double* A = row_bufs<GMEM>(smem, p.gbuf, p.lcap);
     double* B = A + p.lcap;
     const int bins = p.L / 2 + 1;
+    RowPrefetch rp = row_prefetch_init<GMEM>(smem, p, A, lane);
     for (int64_t row = blockIdx.x; row < p.n; row += gridDim.x) {
-        const double* src = p.x + row * p.L;
-        for (int t = lane; t < p.L; t += 32) A[t] = src[t];
+        if (rp.bulk) {
+            rp.wait();
+        } else {
+            const double* src = p.x + row * p.L;
+            for (int t = lane; t < p.L; t += 32) A[t] = src[t];
+        }
         __syncwarp();
         double2* X = rfft_any(A, B, p.L, p.fft, p.tw, lane);
+        double* freeb = (reinterpret_cast<double*>(X) == A) ? B : A;
+        const int64_t next = row + gridDim.x;
+        if (rp.bulk && next < p.n) rp.start(freeb, p.x + next * p.L, lane);
         for (int k = lane; k < bins; k += 32) {
             p.reo[row * bins + k] = X[k].x;
             p.imo[row * bins + k] = X[k].y;
         }
         __syncwarp();
+        if (rp.bulk) {
+            B = reinterpret_cast<double*>(X);
+            A = freeb;
+        }
     }
 }
 
@@ -385,14 +433,26 @@ __global__ void __launch_bounds__(32) dct_kernel(const __grid_constant__ FftPara
     const int lane = threadIdx.x;
     double* A = row_bufs<GMEM>(smem, p.gbuf, p.lcap);
     double* B = A + p.lcap;
+    RowPrefetch rp = row_prefetch_init<GMEM>(smem, p, A, lane);
     for (int64_t row = blockIdx.x; row < p.n; row += gridDim.x) {
-        const double* src = p.x + row * p.L;
-        for (int t = lane; t < p.L; t += 32) A[t] = src[t];
+        if (rp.bulk) {
+            rp.wait();
+        } else {
+            const double* src = p.x + row * p.L;
+            for (int t = lane; t < p.L; t += 32) A[t] = src[t];
+        }
         __syncwarp();
         double* y = p.inverse ? dct3_any(A, B, p.L, p.fft, p.tw, p.dtw, lane)
                               : dct2_any(A, B, p.L, p.fft, p.tw, p.dtw, lane);
+        double* freeb = (y == A) ? B : A;
+        const int64_t next = row + gridDim.x;
+        if (rp.bulk && next < p.n) rp.start(freeb, p.x + next * p.L, lane);
         for (int t = lane; t < p.L; t += 32) p.xo[row * p.L + t] = y[t];
         __syncwarp();
+        if (rp.bulk) {
+            B = y;
+            A = freeb;
+        }
     }
 }
 
