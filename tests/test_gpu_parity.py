@@ -519,3 +519,25 @@ def test_parallel_shards_across_devices_bitwise(monkeypatch):
     monkeypatch.delenv("SA_DEVICES")
     assert np.array_equal(got_par, want) and np.array_equal(got_split, want)
     assert np.array_equal(one.values, base.stages[0].augment_batch(Batch(x), 8).values)
+
+
+@pytest.mark.parametrize("cfg", [3, 4, 5])
+def test_baseline_config_chains_vs_oracle(cfg):
+    """The exact chains bench.py times for configs 3-5 (bench_inputs.pipeline)
+    on a sample of rows at the start AND at the end of the full batch (global
+    series offsets up to N - 1, so every row's stream keys are exercised):
+    config 4 bitwise, the FFT-bearing configs to the spectral tolerance."""
+    import bench_inputs
+    import torch
+
+    N, L = bench_inputs.CONFIG_SHAPES[cfg]
+    pipe = bench_inputs.pipeline(cfg)
+    x = bench_inputs.synthetic_walks(256, L, seed=cfg)
+    for offset in (0, N - 256):
+        want = O.run_pipeline(pipe, x, threads=8, series_offset=offset)
+        got = pipe.run_device(torch.from_numpy(x).cuda(), series_offset=offset).cpu().numpy()
+        if cfg == 4:
+            assert np.array_equal(got, want), (cfg, offset)
+        else:
+            err = np.abs(got - want).max()
+            assert err <= 1e-10 * max(1.0, float(np.abs(want).max())), (cfg, offset, err)
