@@ -1168,6 +1168,12 @@ int alloc_row_bufs(bool global, int lcap, int grid, cudaStream_t st, double** ou
 
 #include "sa_host_stage.inc"
 
+// argument checks of the C ABI, before any device work
+#define SA_REQUIRE(cond, what)                                           \
+    do {                                                                 \
+        if (!(cond)) return fail(SA_ERR_INVALID_ARG, std::string(what)); \
+    } while (0)
+
 }  // namespace
 
 // ====================================================================== C ABI
@@ -1190,6 +1196,7 @@ int sa_init(int32_t device) {
 }
 
 int sa_derive_key(uint64_t seed, uint64_t j, uint64_t i, uint64_t* lo, uint64_t* hi) {
+    SA_REQUIRE(lo && hi, "sa_derive_key: null output");
     auto mix = [](uint64_t z) {
         z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
         z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
@@ -1206,6 +1213,11 @@ int sa_derive_key(uint64_t seed, uint64_t j, uint64_t i, uint64_t* lo, uint64_t*
 int sa_pipeline_launch(const sa_stage* stages, int32_t n_stages, const double* aux, int32_t n_aux,
                        uint64_t master_seed, int64_t series_offset, const double* d_in, int64_t n,
                        int64_t len_in, double* d_out, int64_t len_out, uint32_t* d_flags, void* stream) {
+    SA_REQUIRE(n_stages >= 0 && (n_stages == 0 || stages), "stage table missing");
+    SA_REQUIRE(n_aux >= 0 && (n_aux == 0 || aux), "aux table missing");
+    SA_REQUIRE(n >= 0 && len_in >= 1 && len_out >= 1, "bad batch shape");
+    SA_REQUIRE(n == 0 || (d_in && d_out), "null batch buffer");
+    SA_REQUIRE(d_flags, "null flag word");
     int dev;
     int rc = ensure_device(&dev);
     if (rc) return rc;
@@ -1218,6 +1230,10 @@ int sa_pipeline_launch(const sa_stage* stages, int32_t n_stages, const double* a
 int sa_pipeline_run(const sa_stage* stages, int32_t n_stages, const double* aux, int32_t n_aux,
                     uint64_t master_seed, int64_t series_offset, const double* d_in, int64_t n, int64_t len_in,
                     double* d_out, int64_t len_out, void* stream) {
+    SA_REQUIRE(n_stages >= 0 && (n_stages == 0 || stages), "stage table missing");
+    SA_REQUIRE(n_aux >= 0 && (n_aux == 0 || aux), "aux table missing");
+    SA_REQUIRE(n >= 0 && len_in >= 1 && len_out >= 1, "bad batch shape");
+    SA_REQUIRE(n == 0 || (d_in && d_out), "null batch buffer");
     int dev;
     int rc = ensure_device(&dev);
     if (rc) return rc;
@@ -1238,6 +1254,10 @@ int sa_pipeline_run(const sa_stage* stages, int32_t n_stages, const double* aux,
 int sa_pipeline_run_host(const sa_stage* stages, int32_t n_stages, const double* aux, int32_t n_aux,
                          uint64_t master_seed, int64_t series_offset, const double* h_in, int64_t n,
                          int64_t len_in, double* h_out, int64_t len_out) {
+    SA_REQUIRE(n_stages >= 0 && (n_stages == 0 || stages), "stage table missing");
+    SA_REQUIRE(n_aux >= 0 && (n_aux == 0 || aux), "aux table missing");
+    SA_REQUIRE(n >= 0 && len_in >= 1 && len_out >= 1, "bad batch shape");
+    SA_REQUIRE(n == 0 || (h_in && h_out), "null batch buffer");
     int dev;
     int rc = ensure_device(&dev);
     if (rc) return rc;
@@ -1296,6 +1316,7 @@ static int host_rows(int64_t n, const HostIn* ins, int nin, const HostOut* outs,
 }
 
 int sa_fft_forward_host(const double* h_in, int64_t n, int64_t len, double* h_re, double* h_im) {
+    SA_REQUIRE(n == 0 || (h_in && h_re && h_im), "null buffer");
     if (n < 0 || len < 1) return fail(SA_ERR_INVALID_ARG, "bad batch shape");
     const int64_t bins = len / 2 + 1;
     const HostIn in{h_in, 8 * len};
@@ -1306,6 +1327,7 @@ int sa_fft_forward_host(const double* h_in, int64_t n, int64_t len, double* h_re
 }
 
 int sa_fft_inverse_host(const double* h_re, const double* h_im, int64_t n, int64_t len, double* h_out) {
+    SA_REQUIRE(n == 0 || (h_re && h_im && h_out), "null buffer");
     if (n < 0 || len < 1) return fail(SA_ERR_INVALID_ARG, "bad batch shape");
     const int64_t bins = len / 2 + 1;
     const HostIn in[2] = {{h_re, 8 * bins}, {h_im, 8 * bins}};
@@ -1316,6 +1338,7 @@ int sa_fft_inverse_host(const double* h_re, const double* h_im, int64_t n, int64
 }
 
 int sa_dct_forward_host(const double* h_in, int64_t n, int64_t len, double* h_out) {
+    SA_REQUIRE(n == 0 || (h_in && h_out), "null buffer");
     if (n < 0 || len < 1) return fail(SA_ERR_INVALID_ARG, "bad batch shape");
     const HostIn in{h_in, 8 * len};
     const HostOut out{h_out, 8 * len};
@@ -1325,6 +1348,7 @@ int sa_dct_forward_host(const double* h_in, int64_t n, int64_t len, double* h_ou
 }
 
 int sa_dct_inverse_host(const double* h_in, int64_t n, int64_t len, double* h_out) {
+    SA_REQUIRE(n == 0 || (h_in && h_out), "null buffer");
     if (n < 0 || len < 1) return fail(SA_ERR_INVALID_ARG, "bad batch shape");
     const HostIn in{h_in, 8 * len};
     const HostOut out{h_out, 8 * len};
@@ -1335,6 +1359,7 @@ int sa_dct_inverse_host(const double* h_in, int64_t n, int64_t len, double* h_ou
 
 int sa_dtw_batch_host(const double* h_a, const double* h_b, int64_t n_pairs, int64_t len_a, int64_t len_b,
                       double* h_dist) {
+    SA_REQUIRE(n_pairs <= 0 || (h_a && h_b && h_dist), "null buffer");
     if (n_pairs < 0 || len_a < 1 || len_b < 1) return fail(SA_ERR_INVALID_ARG, "bad batch shape");
     const HostIn in[2] = {{h_a, 8 * len_a}, {h_b, 8 * len_b}};
     const HostOut out{h_dist, 8};
@@ -1347,6 +1372,8 @@ int sa_dtw_batch_host(const double* h_a, const double* h_b, int64_t n_pairs, int
 }
 
 int sa_fft_forward(const double* d_in, int64_t n, int64_t len, double* d_re, double* d_im, void* stream) {
+    SA_REQUIRE(n >= 0 && len >= 1, "bad batch shape");
+    SA_REQUIRE(n == 0 || (d_in && d_re && d_im), "null buffer");
     int dev;
     int rc = ensure_device(&dev);
     if (rc) return rc;
@@ -1374,6 +1401,8 @@ int sa_fft_forward(const double* d_in, int64_t n, int64_t len, double* d_re, dou
 }
 
 int sa_fft_inverse(const double* d_re, const double* d_im, int64_t n, int64_t len, double* d_out, void* stream) {
+    SA_REQUIRE(n >= 0 && len >= 1, "bad batch shape");
+    SA_REQUIRE(n == 0 || (d_re && d_im && d_out), "null buffer");
     int dev;
     int rc = ensure_device(&dev);
     if (rc) return rc;
@@ -1401,6 +1430,8 @@ int sa_fft_inverse(const double* d_re, const double* d_im, int64_t n, int64_t le
 }
 
 static int dct_launch(const double* d_in, int64_t n, int64_t len, double* d_out, void* stream, int inverse) {
+    SA_REQUIRE(n >= 0 && len >= 1, "bad batch shape");
+    SA_REQUIRE(n == 0 || (d_in && d_out), "null buffer");
     int dev;
     int rc = ensure_device(&dev);
     if (rc) return rc;
@@ -1439,6 +1470,8 @@ int sa_dct_inverse(const double* d_in, int64_t n, int64_t len, double* d_out, vo
 
 int sa_dtw_batch(const double* d_a, const double* d_b, int64_t n_pairs, int64_t len_a, int64_t len_b,
                  double* d_dist, void* stream) {
+    SA_REQUIRE(n_pairs >= 0 && len_a >= 1 && len_b >= 1, "bad batch shape");
+    SA_REQUIRE(n_pairs == 0 || (d_a && d_b && d_dist), "null buffer");
     int dev;
     int rc = ensure_device(&dev);
     if (rc) return rc;
@@ -1465,6 +1498,8 @@ int sa_dtw_batch(const double* d_a, const double* d_b, int64_t n_pairs, int64_t 
 
 int sa_dtw_path(const double* d_a, int64_t len_a, const double* d_b, int64_t len_b, double* d_acc, int32_t* d_path,
                 int32_t* d_path_len, double* d_dist, void* stream) {
+    SA_REQUIRE(len_a >= 1 && len_b >= 1, "DTW needs non-empty series");
+    SA_REQUIRE(d_a && d_b && d_acc && d_path && d_path_len && d_dist, "null buffer");
     int dev;
     int rc = ensure_device(&dev);
     if (rc) return rc;
@@ -1488,6 +1523,7 @@ int sa_dtw_path(const double* d_a, int64_t len_a, const double* d_b, int64_t len
 }
 
 int sa_repr_values(const double* d_values, int64_t n, char* d_out, int32_t* d_len, void* stream) {
+    SA_REQUIRE(n >= 0 && (n == 0 || (d_values && d_out && d_len)), "bad arguments");
     int dev;
     int rc = ensure_device(&dev);
     if (rc) return rc;
@@ -1501,6 +1537,7 @@ int sa_repr_values(const double* d_values, int64_t n, char* d_out, int32_t* d_le
 
 int sa_parse_values(const char* d_text, const int64_t* d_offsets, int64_t n, double* d_out, int32_t* d_ok,
                     char* d_scratch, void* stream) {
+    SA_REQUIRE(n >= 0 && (n == 0 || (d_text && d_offsets && d_out && d_ok)), "bad arguments");
     int dev;
     int rc = ensure_device(&dev);
     if (rc) return rc;
@@ -1515,6 +1552,9 @@ int sa_parse_values(const char* d_text, const int64_t* d_offsets, int64_t n, dou
 int sa_augment_spectrum(const sa_stage* stage, uint64_t master_seed, int64_t series_offset, const double* d_re,
                         const double* d_im, int64_t n, int64_t len, double* d_re_out, double* d_im_out,
                         void* stream) {
+    SA_REQUIRE(stage, "null stage");
+    SA_REQUIRE(n >= 0 && len >= 1, "bad batch shape");
+    SA_REQUIRE(n == 0 || (d_re && d_im && d_re_out && d_im_out), "null buffer");
     int dev;
     int rc = ensure_device(&dev);
     if (rc) return rc;
@@ -1555,6 +1595,7 @@ int sa_host_copy(void* dst, const void* src, int64_t bytes) {
 }
 
 int sa_host_alloc(void** ptr, int64_t bytes) {
+    SA_REQUIRE(ptr && bytes >= 0, "bad arguments");
     SA_CUDA(cudaHostAlloc(ptr, (size_t)bytes, cudaHostAllocPortable));
     return SA_OK;
 }

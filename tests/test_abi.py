@@ -110,3 +110,37 @@ def test_no_cpu_fallback_without_device():
 
     with pytest.raises(UnsupportedPlatformError):
         Jitter(0.1).augment_batch(Batch(np.zeros((2, 4))), 1)
+
+
+def test_entry_points_reject_bad_arguments_before_device_work():
+    """Null buffers and negative sizes come back as SA_ERR_INVALID_ARG (no
+    device needed: the checks run before any CUDA call)."""
+    L = _native.lib()
+    E = _abi.SA_ERR_INVALID_ARG
+    null = None
+    st = (_abi.SaStage * 1)()
+    assert L.sa_derive_key(1, 2, 3, None, None) == E
+    for fn in (L.sa_pipeline_run, L.sa_pipeline_run_host):
+        extra = [None] if fn is L.sa_pipeline_run else []
+        assert fn(st, 1, None, 0, 0, 0, null, 4, 8, null, 8, *extra) == E       # null batch
+        assert fn(None, 1, None, 0, 0, 0, null, 0, 8, null, 8, *extra) == E      # stage table missing
+        assert fn(st, 1, None, 3, 0, 0, null, 0, 8, null, 8, *extra) == E        # aux table missing
+        assert fn(st, 1, None, 0, 0, 0, null, -1, 8, null, 8, *extra) == E       # n < 0
+    assert L.sa_pipeline_launch(st, 1, None, 0, 0, 0, null, 0, 8, null, 8, None, None) == E  # flags
+    assert L.sa_fft_forward(None, 2, 8, None, None, None) == E
+    assert L.sa_fft_inverse(None, None, 2, 8, None, None) == E
+    assert L.sa_dct_forward(None, 2, 8, None, None) == E
+    assert L.sa_dct_inverse(None, 2, 0, None, None) == E
+    assert L.sa_fft_forward_host(None, 2, 8, None, None) == E
+    assert L.sa_fft_inverse_host(None, None, 2, 8, None) == E
+    assert L.sa_dct_forward_host(None, 2, 8, None) == E
+    assert L.sa_dct_inverse_host(None, 2, 8, None) == E
+    assert L.sa_dtw_batch(None, None, 2, 8, 8, None, None) == E
+    assert L.sa_dtw_batch_host(None, None, 2, 8, 8, None) == E
+    assert L.sa_dtw_path(None, 8, None, 8, None, None, None, None, None) == E
+    assert L.sa_repr_values(None, 3, None, None, None) == E
+    assert L.sa_parse_values(None, None, 3, None, None, None, None) == E
+    assert L.sa_augment_spectrum(None, 0, 0, None, None, 1, 8, None, None, None) == E
+    assert L.sa_host_copy(None, None, 16) == E
+    assert L.sa_host_alloc(None, 16) == E
+    assert b"null" in L.sa_last_error() or b"bad" in L.sa_last_error()
