@@ -741,7 +741,9 @@ bool make_fft_geo(int64_t L, FftGeo* g) {
     g->npass = np;
     // Large prime factors: the generic passes cost ~N * sum(p) complex MACs;
     // Bluestein costs ~three M-point power-of-two FFTs.  Switch when that is
-    // clearly cheaper (Bluestein also needs 2M-point buffers, so a margin).
+    // clearly cheaper: its 2M-point buffers cost occupancy, so a margin of
+    // 1.8x (measured on the sweep: prime 541 2.1x faster with Bluestein,
+    // 909 = 9 * 101 and 1068 = 12 * 89 faster without).
     int64_t gen = 0;
     for (int q = 0; q < np; ++q)
         if (g->radix[q] != 2 && g->radix[q] != 4 && g->radix[q] != 8) gen += N * (int64_t)g->radix[q];
@@ -751,7 +753,7 @@ bool make_fft_geo(int64_t L, FftGeo* g) {
         int lg = 0;
         while ((1ll << lg) < M) ++lg;
         const double blu = 4.5 * (double)M * (double)lg;
-        if ((double)gen > 4.0 * blu || env_int("SA_BLUESTEIN", 1) == 2) {
+        if ((double)gen > 1.8 * blu || env_int("SA_BLUESTEIN", 1) == 2) {
             if (M > (1ll << 26)) return false;
             g->blue = 1;
             g->M = (int32_t)M;
