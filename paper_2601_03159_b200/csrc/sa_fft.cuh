@@ -315,9 +315,15 @@ __device__ __forceinline__ double2* rfft_any(double* xa, double* xb, int L, cons
 // free scratch.  Uses IFFT(Z) = conj(FFT(conj Z)).  Returns the buffer
 // holding the series.  irfft ignores the imaginary part of the DC bin (and
 // of the Nyquist bin for even L).
+__device__ __forceinline__ bool fin_bad(double v) {  // exponent all ones: inf or nan
+    return (__double2hiint(v) & 0x7ff00000) == 0x7ff00000;
+}
+
+// bad (optional): OR-ed with "some output is non-finite" in the final
+// scaling loop, so callers need no separate pass over the row.
 template <bool BLUE = true>
 __device__ __forceinline__ double* irfft_any(double2* X, double2* other, int L, const FftGeo& g, const double2* tw,
-                                            int lane) {
+                                            int lane, bool* bad = nullptr) {
     const int M = L >> 1;
     if (!g.packed) {  // odd L: Hermitian completion, full transform, real part
         const int bins = L / 2 + 1;
@@ -346,15 +352,25 @@ __device__ __forceinline__ double* irfft_any(double2* X, double2* other, int L, 
     if (!g.packed) {
         double* out = reinterpret_cast<double*>(Z == X ? other : X);
         const double s = 1.0 / (double)L;
-        for (int n = lane; n < L; n += 32) out[n] = Z[n].x * s;
+        bool b = false;
+        for (int n = lane; n < L; n += 32) {
+            const double v = Z[n].x * s;
+            out[n] = v;
+            b |= fin_bad(v);
+        }
+        if (bad) *bad |= b;
         __syncwarp();
         return out;
     }
     const double s = 1.0 / (double)M;
+    bool b = false;
     for (int k = lane; k < M; k += 32) {
         double2 z = Z[k];
-        Z[k] = make_double2(z.x * s, -(z.y * s));
+        const double2 v = make_double2(z.x * s, -(z.y * s));
+        Z[k] = v;
+        b |= fin_bad(v.x) | fin_bad(v.y);
     }
+    if (bad) *bad |= b;
     __syncwarp();
     return reinterpret_cast<double*>(Z);
 }

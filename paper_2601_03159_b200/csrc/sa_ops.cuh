@@ -1018,9 +1018,9 @@ __device__ __forceinline__ bool op_spectral(const DevStage& st, WStream& s, doub
         return false;
     }
     double2* other = reinterpret_cast<double2*>(free_buf);
-    double* y = irfft_any<SA_CHAIN_BLUE>(X, other, L, st.fft, st.tw, w.lane);
+    double* y = irfft_any<SA_CHAIN_BLUE>(X, other, L, st.fft, st.tw, w.lane, &bad);  // checks its outputs
     if (y != cur) swapbuf(cur, oth);
-    return true;
+    return false;
 }
 
 }  // namespace sa
