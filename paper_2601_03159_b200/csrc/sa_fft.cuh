@@ -77,7 +77,43 @@ __device__ __forceinline__ void dft8(double2* v) {
     }
 }
 
-// One Stockham pass of radix R (2, 4, 8) over M points: src -> dst, for
+// 16-point DFT as 4 x 4: n = n1 + 4 n2, k = 4 k1 + k2.  DFT4 over n2 for each
+// n1, multiply by W16^(n1 k2), DFT4 over n1 for each k2.
+template <bool INV>
+__device__ __forceinline__ void dft16(double2* v) {
+    double2 y[16];  // y[4 * n1 + k2]
+#pragma unroll
+    for (int n1 = 0; n1 < 4; ++n1) {
+        double2 t[4] = {v[n1], v[n1 + 4], v[n1 + 8], v[n1 + 12]};
+        dft4<INV>(t);
+#pragma unroll
+        for (int k2 = 0; k2 < 4; ++k2) y[4 * n1 + k2] = t[k2];
+    }
+    // W16^e, e = n1 * k2 in {1, 2, 3, 4, 6, 9}
+    const double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173;  // cos, sin pi/8
+    const double h = 0.70710678118654752440;
+    const double sg = INV ? 1.0 : -1.0;  // forward: exp(-i ...)
+    const double2 w1 = make_double2(c1, sg * s1), w2 = make_double2(h, sg * h), w3 = make_double2(s1, sg * c1);
+    const double2 w6 = make_double2(-h, sg * h), w9 = make_double2(-c1, -sg * s1);
+    y[5] = cmul(y[5], w1);
+    y[6] = cmul(y[6], w2);
+    y[7] = cmul(y[7], w3);
+    y[9] = cmul(y[9], w2);
+    y[10] = rot90<INV>(y[10]);  // W16^4
+    y[11] = cmul(y[11], w6);
+    y[13] = cmul(y[13], w3);
+    y[14] = cmul(y[14], w6);
+    y[15] = cmul(y[15], w9);
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2) {
+        double2 t[4] = {y[k2], y[4 + k2], y[8 + k2], y[12 + k2]};
+        dft4<INV>(t);
+#pragma unroll
+        for (int k1 = 0; k1 < 4; ++k1) v[4 * k1 + k2] = t[k1];
+    }
+}
+
+// One Stockham pass of radix R (2, 4, 8, 16) over M points: src -> dst, for
 // Ns = 2^lns (the power-of-two passes run first, so Ns is a power of two).
 // tw: exp(-2 pi i q / L); W_{Ns R}^{rk} = tw[r k tstep], tstep = L / (Ns R).
 // Twiddles: W^k, W^2k, W^4k are loaded, the odd powers multiplied out.
@@ -111,26 +147,37 @@ __device__ __forceinline__ void stockham_pass(const double2* __restrict__ src, d
             if (R == 2) {
                 v[1] = cmul(v[1], w1);
             } else {
-                // one table load per butterfly: W^2k and W^4k by squaring
+                // one table load per butterfly: W^2k, W^4k (W^8k) by squaring
                 // (the table sits in L2 -- shared memory holds the series)
                 const double2 w2 = cmul(w1, w1);
                 const double2 w3 = cmul(w1, w2);
                 v[1] = cmul(v[1], w1);
                 v[2] = cmul(v[2], w2);
                 v[3] = cmul(v[3], w3);
-                if (R == 8) {
+                if (R >= 8) {
                     const double2 w4 = cmul(w2, w2);
                     v[4] = cmul(v[4], w4);
                     v[5] = cmul(v[5], cmul(w1, w4));
                     v[6] = cmul(v[6], cmul(w2, w4));
                     v[7] = cmul(v[7], cmul(w3, w4));
+                    if (R == 16) {
+                        const double2 w8 = cmul(w4, w4);
+#pragma unroll
+                        for (int r = 1; r < 8; ++r) {
+                            const double2 wr = r == 1 ? w1 : r == 2 ? w2 : r == 3 ? w3 : r == 4 ? w4
+                                             : r == 5 ? cmul(w1, w4) : r == 6 ? cmul(w2, w4) : cmul(w3, w4);
+                            v[8 + r] = cmul(v[8 + r], cmul(wr, w8));
+                        }
+                        v[8] = cmul(v[8], w8);
+                    }
                 }
             }
         }
         if (R == 2) dft2<INV>(v);
         if (R == 4) dft4<INV>(v);
         if (R == 8) dft8<INV>(v);
-        const int base = ((j >> lns) << (lns + (R == 8 ? 3 : (R == 4 ? 2 : 1)))) + k;
+        if (R == 16) dft16<INV>(v);
+        const int base = ((j >> lns) << (lns + (R == 16 ? 4 : (R == 8 ? 3 : (R == 4 ? 2 : 1))))) + k;
         // output swizzle only on pass 0 (Ns == 1, base a multiple of R): one
         // XOR term for the whole butterfly
         const int xo = (base >> sout.sh) & sout.mask;
@@ -205,6 +252,7 @@ __device__ __forceinline__ void generic_pass(const double2* __restrict__ src, do
 // The Stockham passes of an N-point plan (radix list `radix`, npass passes)
 // over a table of W_L (N | L); data in a, b is scratch; returns the buffer
 // holding the result.
+template <bool R16 = false>
 __device__ __forceinline__ double2* fft_passes(double2* a, double2* b, int N, int npass, const int16_t* radix,
                                                const double2* tw, int L, int lane) {
     int Ns = 1;
@@ -214,14 +262,15 @@ __device__ __forceinline__ double2* fft_passes(double2* a, double2* b, int N, in
     Swz carry = {0, 0};  // swizzle of the buffer the next pass reads
     for (int p = 0; p < npass; ++p) {
         const int R = radix[p];
-        if (R == 8 || R == 4 || R == 2) {
-            const int lr = (R == 8 ? 3 : (R == 4 ? 2 : 1));
+        if (R == 16 || R == 8 || R == 4 || R == 2) {
+            const int lr = (R == 16 ? 4 : (R == 8 ? 3 : (R == 4 ? 2 : 1)));
             const int tstep = L >> (lns + lr);  // L / (Ns R)
             // swizzle pass 0's output when pass 1 is a power-of-two pass too
-            const bool swz = (p == 0 && R > 2 && npass > 1 && (radix[1] & (radix[1] - 1)) == 0 &&
+            const bool swz = (p == 0 && R > 2 && R < 16 && npass > 1 && (radix[1] & (radix[1] - 1)) == 0 &&
                               (N / radix[1]) % (R * R) == 0);
             const Swz out = swz ? Swz{lr, R - 1} : Swz{0, 0};
-            if (R == 8) stockham_pass<8, false>(src, dst, N, lns, tw, tstep, lane, carry, out);
+            if (R16 && R == 16) stockham_pass<R16 ? 16 : 8, false>(src, dst, N, lns, tw, tstep, lane, carry, out);
+            else if (R == 8) stockham_pass<8, false>(src, dst, N, lns, tw, tstep, lane, carry, out);
             else if (R == 4) stockham_pass<4, false>(src, dst, N, lns, tw, tstep, lane, carry, out);
             else stockham_pass<2, false>(src, dst, N, lns, tw, tstep, lane, carry, out);
             carry = out;
@@ -261,17 +310,17 @@ __device__ __forceinline__ double2* bluestein(double2* a, double2* b, const FftG
 }
 
 // Forward N-point complex FFT per the plan; data in a, b is scratch.
-template <bool BLUE = true>
+template <bool BLUE = true, bool R16 = false>
 __device__ __forceinline__ double2* fft_any(double2* a, double2* b, const FftGeo& g, const double2* tw, int L,
                                             int lane) {
     if (BLUE && g.blue) return bluestein(a, b, g, lane);
-    return fft_passes(a, b, g.N, g.npass, g.radix, tw, L, lane);
+    return fft_passes<R16>(a, b, g.N, g.npass, g.radix, tw, L, lane);
 }
 
 // rfft of the real series x (length L, in buffer xa) -> X[0 .. L/2]
 // (complex, bins = L/2 + 1).  xb is scratch of the same capacity (>= 2L + 2
 // doubles for odd L).  Returns the buffer holding X; the other is free.
-template <bool BLUE = true>
+template <bool BLUE = true, bool R16 = false>
 __device__ __forceinline__ double2* rfft_any(double* xa, double* xb, int L, const FftGeo& g, const double2* tw,
                                             int lane) {
     double2* za = reinterpret_cast<double2*>(xa);
@@ -285,7 +334,7 @@ __device__ __forceinline__ double2* rfft_any(double* xa, double* xb, int L, cons
     }
     double2* s0 = g.packed ? za : zb;
     double2* d0 = g.packed ? zb : za;
-    double2* Z = fft_any<BLUE>(s0, d0, g, tw, L, lane);  // one call site: the FFT is emitted once
+    double2* Z = fft_any<BLUE, R16>(s0, d0, g, tw, L, lane);  // one call site: the FFT is emitted once
     if (!g.packed) {
         if (lane == 0) Z[0].y = 0.0;
         __syncwarp();
@@ -321,7 +370,7 @@ __device__ __forceinline__ bool fin_bad(double v) {  // exponent all ones: inf o
 
 // bad (optional): OR-ed with "some output is non-finite" in the final
 // scaling loop, so callers need no separate pass over the row.
-template <bool BLUE = true>
+template <bool BLUE = true, bool R16 = false>
 __device__ __forceinline__ double* irfft_any(double2* X, double2* other, int L, const FftGeo& g, const double2* tw,
                                             int lane, bool* bad = nullptr) {
     const int M = L >> 1;
@@ -348,7 +397,7 @@ __device__ __forceinline__ double* irfft_any(double2* X, double2* other, int L, 
         }
     }
     __syncwarp();
-    double2* Z = fft_any<BLUE>(other, X, g, tw, L, lane);  // one call site: the FFT is emitted once
+    double2* Z = fft_any<BLUE, R16>(other, X, g, tw, L, lane);  // one call site: the FFT is emitted once
     if (!g.packed) {
         double* out = reinterpret_cast<double*>(Z == X ? other : X);
         const double s = 1.0 / (double)L;
@@ -392,7 +441,7 @@ __device__ __forceinline__ double* dct2_any(double* xa, double* xb, int N, const
                                            const double2* dtw, int lane) {
     for (int n = lane; n < N; n += 32) xb[n] = xa[(2 * n < N) ? 2 * n : 2 * (N - 1 - n) + 1];
     __syncwarp();
-    double2* V = rfft_any(xb, xa, N, g, tw, lane);
+    double2* V = rfft_any<true, true>(xb, xa, N, g, tw, lane);
     double* y = (reinterpret_cast<double*>(V) == xa) ? xb : xa;
     const double g0 = 1.0 / sqrt((double)N), gk = sqrt(2.0 / (double)N);
     for (int k = lane; k < N; k += 32) {
@@ -417,7 +466,7 @@ __device__ __forceinline__ double* dct3_any(double* ya, double* yb, int N, const
         V[k] = cmul(make_double2(sk, -snk), w);
     }
     __syncwarp();
-    double* v = irfft_any(V, reinterpret_cast<double2*>(ya), N, g, tw, lane);
+    double* v = irfft_any<true, true>(V, reinterpret_cast<double2*>(ya), N, g, tw, lane);
     double* x = (v == ya) ? yb : ya;
     for (int n = lane; n < N; n += 32) x[(2 * n < N) ? 2 * n : 2 * (N - 1 - n) + 1] = v[n];
     __syncwarp();

@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(32) rfft_kernel(const __grid_constant__ FftPar
             for (int t = lane; t < p.L; t += 32) A[t] = src[t];
         }
         __syncwarp();
-        double2* X = rfft_any(A, B, p.L, p.fft, p.tw, lane);
+        double2* X = rfft_any<true, true>(A, B, p.L, p.fft, p.tw, lane);
         double* freeb = (reinterpret_cast<double*>(X) == A) ? B : A;
         const int64_t next = row + gridDim.x;
         if (rp.bulk && next < p.n) rp.start(freeb, p.x + next * p.L, lane);
@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(32) irfft_kernel(const __grid_constant__ FftPa
     for (int64_t row = blockIdx.x; row < p.n; row += gridDim.x) {
         for (int k = lane; k < bins; k += 32) X[k] = make_double2(p.re[row * bins + k], p.im[row * bins + k]);
         __syncwarp();
-        double* y = irfft_any(X, O, p.L, p.fft, p.tw, lane);
+        double* y = irfft_any<true, true>(X, O, p.L, p.fft, p.tw, lane);
         for (int t = lane; t < p.L; t += 32) p.xo[row * p.L + t] = y[t];
         __syncwarp();
     }
@@ -709,7 +709,9 @@ int get_twiddles(int dev, int L, const double2** out) {
 // generic pass per remaining prime factor (ascending).
 int env_int(const char* k, int d);
 
-bool make_fft_geo(int64_t L, FftGeo* g) {
+// allow16: the plan may use radix-16 passes (the standalone transform
+// kernels; the chain kernel has no register room for them)
+bool make_fft_geo(int64_t L, FftGeo* g, bool allow16 = false) {
     std::memset(g, 0, sizeof(*g));
     if (L < 1) return false;
     g->packed = (L % 2 == 0) ? 1 : 0;
@@ -719,12 +721,24 @@ bool make_fft_geo(int64_t L, FftGeo* g) {
     int np = 0;
     int64_t p2 = 1;
     while (rem % 2 == 0) { rem /= 2; p2 *= 2; }
-    int64_t left = p2;
+    // power-of-two part: radix-8 passes, except that a final radix-16 pass
+    // replaces two passes when log2 is not a multiple of 3 (1024 = 8*8*16
+    // instead of 8*8*4*4); radix 16 never runs first (its pass-0 stores would
+    // conflict 16 ways in shared memory)
+    int lg2 = 0;
+    while ((1ll << lg2) < p2) ++lg2;
+    const bool use16 = allow16 && env_int("SA_FFT_RADIX16", 1) && lg2 >= 7 && lg2 != 8 && lg2 % 3 != 0;
+    int64_t left = use16 ? p2 / 16 : p2;
     while (left > 1) {
         int r = (left >= 8 && left != 16) ? 8 : (left >= 4 ? 4 : 2);
+        if (use16 && left == 16) r = 16;  // two radix-16 passes for lg2 % 3 == 2
         if (np >= SA_FFT_MAXPASS) return false;
         g->radix[np++] = (int16_t)r;
         left /= r;
+    }
+    if (use16) {
+        if (np >= SA_FFT_MAXPASS) return false;
+        g->radix[np++] = 16;
     }
     for (int64_t f = 3; rem > 1; f += 2) {
         while (rem % f == 0) {
@@ -1380,7 +1394,7 @@ int sa_fft_forward(const double* d_in, int64_t n, int64_t len, double* d_re, dou
     int rc = ensure_device(&dev);
     if (rc) return rc;
     FftParams p{};
-    if (!make_fft_geo(len, &p.fft)) return fail(SA_ERR_UNSUPPORTED, "no FFT plan for this length");
+    if (!make_fft_geo(len, &p.fft, true)) return fail(SA_ERR_UNSUPPORTED, "no FFT plan for this length");
     p.x = d_in; p.reo = d_re; p.imo = d_im; p.n = n; p.L = (int32_t)len;
     rc = get_twiddles(dev, (int)len, &p.tw);
     if (!rc) rc = finish_geo(dev, &p.fft);
@@ -1409,7 +1423,7 @@ int sa_fft_inverse(const double* d_re, const double* d_im, int64_t n, int64_t le
     int rc = ensure_device(&dev);
     if (rc) return rc;
     FftParams p{};
-    if (!make_fft_geo(len, &p.fft)) return fail(SA_ERR_UNSUPPORTED, "no FFT plan for this length");
+    if (!make_fft_geo(len, &p.fft, true)) return fail(SA_ERR_UNSUPPORTED, "no FFT plan for this length");
     p.re = d_re; p.im = d_im; p.xo = d_out; p.n = n; p.L = (int32_t)len;
     rc = get_twiddles(dev, (int)len, &p.tw);
     if (!rc) rc = finish_geo(dev, &p.fft);
@@ -1438,7 +1452,7 @@ static int dct_launch(const double* d_in, int64_t n, int64_t len, double* d_out,
     int rc = ensure_device(&dev);
     if (rc) return rc;
     FftParams p{};
-    if (len < 1 || !make_fft_geo(len, &p.fft)) return fail(SA_ERR_UNSUPPORTED, "no DCT plan for this length");
+    if (len < 1 || !make_fft_geo(len, &p.fft, true)) return fail(SA_ERR_UNSUPPORTED, "no DCT plan for this length");
     p.x = d_in; p.xo = d_out; p.n = n; p.L = (int32_t)len; p.inverse = inverse;
     rc = get_twiddles(dev, (int)len, &p.tw);
     if (rc) return rc;
