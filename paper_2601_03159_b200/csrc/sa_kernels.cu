@@ -67,6 +67,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// Ampere-style async copy of one 8-byte word global -> shared (L2 only);
+// used where the source is not a 16-byte-aligned contiguous row (TMA's
+// requirement), e.g. interleaving separate re / im arrays.
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 // ------------------------------------------------------------ smem layout
 struct Layout {
     uint32_t buf_a, buf_b, win, scache, small, iscr, bar, total;
@@ -417,12 +426,35 @@ __global__ void __launch_bounds__(32) irfft_kernel(const __grid_constant__ FftPa
     double2* X = reinterpret_cast<double2*>(row_bufs<GMEM>(smem, p.gbuf, p.lcap));
     double2* O = X + p.lcap / 2;
     const int bins = p.L / 2 + 1;
+    // shared-memory rows: the next row's re / im land in the free buffer by
+    // cp.async while this row's series is stored
+    auto fetch = [&](double2* dst, int64_t row) {
+        const double* re = p.re + row * bins;
+        const double* im = p.im + row * bins;
+        for (int k = lane; k < bins; k += 32) {
+            cp_async8(&dst[k].x, re + k);
+            cp_async8(&dst[k].y, im + k);
+        }
+        cp_async_commit();
+    };
+    if (!GMEM && blockIdx.x < p.n) fetch(X, blockIdx.x);
     for (int64_t row = blockIdx.x; row < p.n; row += gridDim.x) {
-        for (int k = lane; k < bins; k += 32) X[k] = make_double2(p.re[row * bins + k], p.im[row * bins + k]);
+        if (GMEM) {
+            for (int k = lane; k < bins; k += 32) X[k] = make_double2(p.re[row * bins + k], p.im[row * bins + k]);
+        } else {
+            cp_async_wait_all();
+        }
         __syncwarp();
         double* y = irfft_any<true, true>(X, O, p.L, p.fft, p.tw, lane);
+        double2* freeb = (y == reinterpret_cast<double*>(X)) ? O : X;
+        const int64_t next = row + gridDim.x;
+        if (!GMEM && next < p.n) fetch(freeb, next);
         for (int t = lane; t < p.L; t += 32) p.xo[row * p.L + t] = y[t];
         __syncwarp();
+        if (!GMEM) {
+            O = reinterpret_cast<double2*>(y);
+            X = freeb;
+        }
     }
 }
 

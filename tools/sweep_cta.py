@@ -13,7 +13,7 @@ x = device_walks(n, L, 5, torch.device("cuda"))
 out = torch.empty((n, pipe.projected_length(L)), dtype=torch.float64, device="cuda")
 flags = torch.zeros(1, dtype=torch.int32, device="cuda")
 ref = None
-for warps, sync, sched in [(0, 4, 1), (0, 4, 0), (0, 0, 0), (0, 8, 0), (0, 4, 1)]:
+for warps, sync, sched in [(0, 4, 1), (7, 4, 1), (4, 4, 1), (2, 4, 1), (0, 4, 1)]:
     os.environ['SA_SCHEDULE'] = str(sched)
     os.environ["SA_CTA_WARPS"] = str(warps)
     os.environ["SA_SYNC_EVERY"] = str(sync)
