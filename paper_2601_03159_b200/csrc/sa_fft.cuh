@@ -207,44 +207,72 @@ struct FftGeo {
     const double2* twM;    // exp(-2 pi i k / M), k < M
 };
 
-// Generic radix-R Stockham pass (any R | N): each output is the direct sum
-// V[u] = sum_r src[j + rQ] * W_N^(r * (k*N/(Ns R) + u*N/R)), a geometric
-// progression in r: one table load for its ratio, then one complex multiply
-// per term (rounding grows ~R ulp, far inside the FFT tolerance) instead of
-// a table load per term.  Four outputs u0 + {0,1,2,3}*q of the same input
-// column are accumulated together (shared loads, four independent chains).
-__device__ __forceinline__ void generic_pass(const double2* __restrict__ src, double2* __restrict__ dst, int N, int Ns,
+// Generic radix-R Stockham pass, R an odd prime (R | N).  Output u of column
+// j is the R-point DFT of the twiddled column y_r = src[j + rQ] W_N^(r k a):
+// V[u] = sum_r y_r W_R^(ru).  Folding the pairs r, R - r (s_r = y_r +
+// y_(R-r), d_r = y_r - y_(R-r)) gives, for the output pair u, R - u,
+//   V[u]     = y_0 + sum_m s_m cos(2 pi m u / R) - i sum_m d_m sin(2 pi m u / R)
+//   V[R - u] = y_0 + sum_m s_m cos(2 pi m u / R) + i sum_m d_m sin(2 pi m u / R)
+// (m = 1 .. (R-1)/2): 4 real FMAs per (m, output pair) instead of 16 for the
+// direct complex sums.  Step 1 twiddles and folds each column in place in
+// `src` (this pass's input is scratch afterwards); step 2 accumulates four
+// output pairs per work item over the folded column, cos / sin exact from the
+// W_L table (index m u mod R kept incrementally).
+__device__ __forceinline__ void generic_pass(double2* __restrict__ src, double2* __restrict__ dst, int N, int Ns,
                                              int R, const double2* __restrict__ tw, int L, int lane) {
     const int Q = N / R;
-    const int ts = L / N;               // table stride for W_N
-    const int a = N / (Ns * R), b = N / R;
-    const int q = (R + 3) / 4;          // outputs u0 + c*q, c < 4, share the column j
-    for (int idx = lane; idx < Q * q; idx += 32) {
-        const int j = idx % Q, u0 = idx / Q;
+    const int ts = L / N;  // W_N stride in the W_L table
+    const int tr = L / R;  // W_R stride
+    const int a = N / (Ns * R);
+    const int H = (R - 1) >> 1;
+    for (int idx = lane; idx < Q * H; idx += 32) {
+        const int j = idx % Q, m = 1 + idx / Q;
+        const int ka = (j % Ns) * a;  // < N / R
+        double2 y1 = src[j + m * Q], y2 = src[j + (R - m) * Q];
+        if (ka) {  // exponents r ka < R * (N / R): no reduction
+            y1 = cmul(y1, __ldg(&tw[m * ka * ts]));
+            y2 = cmul(y2, __ldg(&tw[(R - m) * ka * ts]));
+        }
+        src[j + m * Q] = cadd(y1, y2);
+        src[j + (R - m) * Q] = csub(y1, y2);
+    }
+    __syncwarp();
+    const int G = (H + 4) >> 2;  // output pairs u = 0 .. H, four per item
+    for (int idx = lane; idx < Q * G; idx += 32) {
+        const int j = idx % Q, g0 = 4 * (idx / Q);
         const int k = j % Ns;
-        const int ka = k * a;            // < N
-        double2 t[4], st[4], acc[4];
+        const double2 y0 = src[j];
+        double2 A[4], B[4];
+        int id[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-            const int u = u0 + c * q;
-            int e = ka + (u < R ? u : 0) * b;  // both terms < N
-            e = e >= N ? e - N : e;
-            st[c] = __ldg(&tw[e * ts]);
-            t[c] = make_double2(1.0, 0.0);
-            acc[c] = make_double2(0.0, 0.0);
+            A[c] = make_double2(0.0, 0.0);
+            B[c] = make_double2(0.0, 0.0);
+            id[c] = 0;
         }
-        for (int r = 0; r < R; ++r) {
-            const double2 v = src[j + r * Q];
+        for (int m = 1; m <= H; ++m) {
+            const double2 sm = src[j + m * Q], dm = src[j + (R - m) * Q];
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
-                acc[c] = cadd(acc[c], cmul(v, t[c]));
-                t[c] = cmul(t[c], st[c]);
+                id[c] += g0 + c;  // m u mod R, u = g0 + c <= H + 3 < R
+                id[c] = id[c] >= R ? id[c] - R : id[c];
+                const double2 w = __ldg(&tw[id[c] * tr]);  // (cos, -sin)
+                A[c].x = fma(sm.x, w.x, A[c].x);
+                A[c].y = fma(sm.y, w.x, A[c].y);
+                B[c].x = fma(dm.x, w.y, B[c].x);  // B = -sum d sin
+                B[c].y = fma(dm.y, w.y, B[c].y);
             }
         }
         const int o = (j - k) * R + k;
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-            if (u0 + c * q < R) dst[o + (u0 + c * q) * Ns] = acc[c];
+        for (int c = 0; c < 4; ++c) {
+            const int u = g0 + c;
+            if (u > H) break;
+            const double re = y0.x + A[c].x, im = y0.y + A[c].y;
+            // -i * (-B) = (-B.y, B.x) for V[u]; its negation for V[R - u]
+            dst[o + u * Ns] = make_double2(re - B[c].y, im + B[c].x);
+            if (u) dst[o + (R - u) * Ns] = make_double2(re + B[c].y, im - B[c].x);
+        }
     }
     __syncwarp();
 }

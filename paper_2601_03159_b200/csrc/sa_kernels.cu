@@ -799,7 +799,7 @@ bool make_fft_geo(int64_t L, FftGeo* g, bool allow16 = false) {
         int lg = 0;
         while ((1ll << lg) < M) ++lg;
         const double blu = 4.5 * (double)M * (double)lg;
-        if ((double)gen > 1.8 * blu || env_int("SA_BLUESTEIN", 1) == 2) {
+        if ((double)gen > 0.1 * env_int("SA_BLUE_X10", 18) * blu || env_int("SA_BLUESTEIN", 1) == 2) {
             if (M > (1ll << 26)) return false;
             g->blue = 1;
             g->M = (int32_t)M;
@@ -1028,7 +1028,15 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
     p.iscr_words = iscr;
     plan->lay = make_layout(p.lcap, ns, small, iscr);
     DeviceState& ds = dev_state(dev);
-    if (plan->lay.total + 256 * sizeof(ZigEntry) > ds.smem_optin || env_int("SA_FORCE_GLOBAL", 0)) {
+    // Row buffers in shared memory unless (a) they do not fit, or (b) so few
+    // warps fit (<= 3 per SM: long odd lengths, Bluestein buffers) that the
+    // SM's four schedulers starve while there are rows for several waves:
+    // then the buffers move to global memory (L2 resident), which lets 12
+    // warps per SM run (sweep: L = 2369 1.9x, Bluestein 541 / 1707 1.3-2x).
+    const size_t smem_fit = (ds.smem_optin - 256 * sizeof(ZigEntry)) / std::max<size_t>(plan->lay.total, 1);
+    const bool starved = smem_fit >= 1 && smem_fit <= 3 && env_int("SA_AUTO_GLOBAL", 1) &&
+                         p.rows_out > 3 * (int64_t)ds.sms * (int64_t)smem_fit;
+    if (plan->lay.total + 256 * sizeof(ZigEntry) > ds.smem_optin || starved || env_int("SA_FORCE_GLOBAL", 0)) {
         // long series: the two row buffers move to global memory (L2 / HBM
         // resident, same code); shared memory keeps the window and scratch
         plan->global = true;

@@ -335,6 +335,25 @@ def test_config5_sweep_vs_oracle():
     assert excused <= max(2, total // 1000), (excused, total)
 
 
+@pytest.mark.parametrize("ds", [73, 33, 81])
+def test_sweep_low_occupancy_lengths_full_size(ds):
+    """Sweep datasets whose shared-memory plan fits <= 3 warps per SM (L =
+    2369 = 23 * 103 complexified, Bluestein 1707 / 753) at full size: the
+    plan then moves the row buffers to global memory (make_plan's starved
+    rule).  First and last 64 series against the oracle."""
+    import bench_inputs
+
+    i, n, L = next(d for d in bench_inputs.sweep_datasets() if d[0] == ds)
+    pipe = bench_inputs.sweep_pipeline(L, seed=i)
+    x = bench_inputs.synthetic_walks(n, L, seed=i)
+    got = gpu_run(pipe, x)
+    for a in (0, n - 64):
+        want = O.run_pipeline(pipe, x[a:a + 64], series_offset=a)
+        tol = 1e-9 * max(1.0, float(np.abs(want).max()))
+        bad = np.flatnonzero(np.abs(got[a:a + 64] - want).max(axis=1) > tol)
+        assert bad.size <= 1, (ds, a, bad)  # APP's zero-bin ill-conditioning only (test above)
+
+
 def test_pinned_host_batches_roundtrip():
     from paper_2601_03159_b200 import pinned_copy, pinned_empty
 

@@ -27,3 +27,5 @@ for ms, i, n, L in sorted(rows, reverse=True)[:15]:
     Lf = L // 2 if L % 2 == 0 else L
     print(f"{ms:8.3f} ms  ds {i:3d} n={n:6d} L={L:5d}  fft N={Lf} factors={factors(Lf)}  us/series={1e3*ms/n:.2f}")
 print("median ms", np.median([r[0] for r in rows]))
+if len(sys.argv) > 1:
+    import json; json.dump(rows, open(sys.argv[1], "w"))
