@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <initializer_list>
 #include <cmath>
 #include <condition_variable>
 #include <thread>
@@ -32,6 +33,7 @@
 #include "sa_text.cuh"
 #include "sa_dataset.cuh"
 #include "sa_ops.cuh"
+#include "sa_fft_cta.cuh"
 
 namespace sa {
 
@@ -72,6 +74,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // requirement), e.g. interleaving separate re / im arrays.
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
@@ -488,6 +493,216 @@ __global__ void __launch_bounds__(32) dct_kernel(const __grid_constant__ FftPara
     }
 }
 
+// CTA-cooperative transforms (sa_fft_cta.cuh): power-of-two complex length
+// N = 256 .. 2048, T = N / 8 threads per row.  Shared memory: the FFT's
+// exchange buffer (N complex) and a next-row buffer (N + 1 complex) that
+// cp.async fills with row r + gridDim while row r is transformed.
+struct CtaSmem {
+    double2* buf;
+    double2* nb;
+};
+__device__ __forceinline__ CtaSmem cta_smem(unsigned char* smem, int N) {
+    double2* b = reinterpret_cast<double2*>(smem);
+    return {b, b + N};
+}
+
+// rfft (freqtransform.py:101-108): real row (N complex) -> bins 0..N
+template <int LGN>
+__global__ void __launch_bounds__(256) rfft_cta_kernel(const __grid_constant__ FftParams p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int T = CtaPlan<LGN>::T;
+    const int t = threadIdx.x;
+    const int M = p.L >> 1, bins = M + 1;
+    const CtaSmem sm = cta_smem(smem, M);
+    double2 w[8];
+    cta_twiddles<LGN>(w, t, p.tw, LGN + 1);
+    auto fetch = [&](int64_t row) {
+        const double2* xr = reinterpret_cast<const double2*>(p.x + row * p.L);
+        for (int i = t; i < M; i += T) cp_async16(&sm.nb[i], xr + i);
+        cp_async_commit();
+    };
+    double2 ws[8];  // split twiddles W_L^k, k = t + m T
+#pragma unroll
+    for (int m = 0; m < 8; ++m) ws[m] = __ldg(&p.tw[t + m * T]);
+    if (blockIdx.x < p.n) fetch(blockIdx.x);
+    for (int64_t row = blockIdx.x; row < p.n; row += gridDim.x) {
+        double2 v[8];
+        cp_async_wait_all();
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < 8; ++m) v[m] = sm.nb[t + m * T];
+        __syncthreads();
+        if (row + gridDim.x < p.n) fetch(row + gridDim.x);
+        cta_fft<LGN>(v, sm.buf, t, w);
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < 8; ++m) sm.buf[t + m * T] = v[m];
+        __syncthreads();
+        double* re = p.reo + row * bins;
+        double* im = p.imo + row * bins;
+#pragma unroll 4
+        for (int m = 0; m < 8; ++m) {
+            const int k = t + m * T;
+            double2 X = cta_split(sm.buf[k], sm.buf[k == 0 ? 0 : M - k], ws[m]);
+            if (k == 0) X.y = 0.0;
+            __stcs(re + k, X.x);
+            __stcs(im + k, X.y);
+        }
+        if (t == 0) {
+            const double2 X = cta_split(sm.buf[0], sm.buf[0], __ldg(&p.tw[M]));
+            __stcs(re + M, X.x);
+            __stcs(im + M, 0.0);
+        }
+    }
+}
+
+// irfft (freqtransform.py:110-116): bins 0..N (separate re / im rows) -> real row
+template <int LGN>
+__global__ void __launch_bounds__(256) irfft_cta_kernel(const __grid_constant__ FftParams p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int T = CtaPlan<LGN>::T;
+    const int t = threadIdx.x;
+    const int M = p.L >> 1, bins = M + 1;
+    const CtaSmem sm = cta_smem(smem, M);
+    double2 w[8];
+    cta_twiddles<LGN>(w, t, p.tw, LGN + 1);
+    const double s = 1.0 / (double)M;
+    auto fetch = [&](int64_t row) {  // interleave re / im into complex bins
+        const double* re = p.re + row * bins;
+        const double* im = p.im + row * bins;
+        for (int k = t; k < bins; k += T) {
+            cp_async8(&sm.nb[k].x, re + k);
+            cp_async8(&sm.nb[k].y, im + k);
+        }
+        cp_async_commit();
+    };
+    double2 ws[8];  // fold twiddles W_L^k, k = t + m T
+#pragma unroll
+    for (int m = 0; m < 8; ++m) ws[m] = __ldg(&p.tw[t + m * T]);
+    if (blockIdx.x < p.n) fetch(blockIdx.x);
+    for (int64_t row = blockIdx.x; row < p.n; row += gridDim.x) {
+        double2 v[8];
+        cp_async_wait_all();
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const int k = t + m * T;
+            v[m] = cta_fold(sm.nb[k], sm.nb[M - k], ws[m], k == 0);
+        }
+        __syncthreads();
+        if (row + gridDim.x < p.n) fetch(row + gridDim.x);
+        cta_fft<LGN>(v, sm.buf, t, w);
+        double2* xo = reinterpret_cast<double2*>(p.xo + row * p.L);
+#pragma unroll
+        for (int m = 0; m < 8; ++m) __stcs(xo + t + m * T, make_double2(v[m].x * s, -(v[m].y * s)));
+    }
+}
+
+// DCT-II / DCT-III (orthonormal, freqtransform.py:91-98) of length Lr = 2N,
+// dct2_any / dct3_any's formulas; the Makhoul permutation is applied by the
+// row fetch (II: v[i] = x[2i], v[Lr-1-i] = x[2i+1]) or the row store (III).
+template <int LGN>
+__global__ void __launch_bounds__(256) dct2_cta_kernel(const __grid_constant__ FftParams p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int T = CtaPlan<LGN>::T;
+    const int t = threadIdx.x;
+    const int Lr = p.L, N = Lr >> 1;
+    const CtaSmem sm = cta_smem(smem, N);
+    double* nbd = reinterpret_cast<double*>(sm.nb);
+    double2 w[8];
+    cta_twiddles<LGN>(w, t, p.tw, LGN + 1);
+    auto fetch = [&](int64_t row) {
+        const double* xr = p.x + row * Lr;
+        for (int i = t; i < N; i += T) {
+            cp_async8(&nbd[i], xr + 2 * i);
+            cp_async8(&nbd[Lr - 1 - i], xr + 2 * i + 1);
+        }
+        cp_async_commit();
+    };
+    if (blockIdx.x < p.n) fetch(blockIdx.x);
+    const double g0 = 1.0 / sqrt((double)Lr), gk = sqrt(2.0 / (double)Lr);
+    for (int64_t row = blockIdx.x; row < p.n; row += gridDim.x) {
+        double2 v[8];
+        cp_async_wait_all();
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < 8; ++m) v[m] = sm.nb[t + m * T];
+        __syncthreads();
+        if (row + gridDim.x < p.n) fetch(row + gridDim.x);
+        cta_fft<LGN>(v, sm.buf, t, w);
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < 8; ++m) sm.buf[t + m * T] = v[m];
+        __syncthreads();
+        double* y = p.xo + row * Lr;
+#pragma unroll 2
+        for (int m = 0; m < 8; ++m) {
+            const int k = t + m * T;
+            double2 X = cta_split(sm.buf[k], sm.buf[k == 0 ? 0 : N - k], __ldg(&p.tw[k]));
+            if (k == 0) X.y = 0.0;
+            const double2 w = __ldg(&p.dtw[k]);
+            __stcs(y + k, (k == 0 ? g0 : gk) * (X.x * w.x - X.y * w.y));
+            if (k > 0) {
+                const double2 w2 = __ldg(&p.dtw[Lr - k]);  // V[Lr-k] = conj(V[k])
+                __stcs(y + Lr - k, gk * (X.x * w2.x + X.y * w2.y));
+            }
+        }
+        if (t == 0) {
+            double2 X = cta_split(sm.buf[0], sm.buf[0], __ldg(&p.tw[N]));
+            X.y = 0.0;
+            const double2 w = __ldg(&p.dtw[N]);
+            __stcs(y + N, gk * (X.x * w.x - X.y * w.y));
+        }
+    }
+}
+
+template <int LGN>
+__global__ void __launch_bounds__(256) dct3_cta_kernel(const __grid_constant__ FftParams p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int T = CtaPlan<LGN>::T;
+    const int t = threadIdx.x;
+    const int Lr = p.L, N = Lr >> 1;
+    const CtaSmem sm = cta_smem(smem, N);
+    const double* nbd = reinterpret_cast<const double*>(sm.nb);
+    const double* xb = reinterpret_cast<const double*>(sm.buf);
+    double2 w[8];
+    cta_twiddles<LGN>(w, t, p.tw, LGN + 1);
+    auto fetch = [&](int64_t row) {
+        const double2* yr = reinterpret_cast<const double2*>(p.x + row * Lr);
+        for (int i = t; i < N; i += T) cp_async16(&sm.nb[i], yr + i);
+        cp_async_commit();
+    };
+    if (blockIdx.x < p.n) fetch(blockIdx.x);
+    const double i0 = sqrt((double)Lr), ik = sqrt((double)Lr / 2.0);
+    const double s = 1.0 / (double)N;
+    auto V = [&](int q) {  // V[q] = e^{+i pi q / 2Lr} (S[q] - i S[Lr-q]), q <= N
+        const double sk = nbd[q] * (q == 0 ? i0 : ik);
+        const double snk = (q == 0) ? 0.0 : nbd[Lr - q] * ik;
+        double2 w = __ldg(&p.dtw[q]);
+        w.y = -w.y;
+        return cmul(make_double2(sk, -snk), w);
+    };
+    for (int64_t row = blockIdx.x; row < p.n; row += gridDim.x) {
+        double2 v[8];
+        cp_async_wait_all();
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const int k = t + m * T;
+            v[m] = cta_fold(V(k), V(N - k), __ldg(&p.tw[k]), k == 0);
+        }
+        __syncthreads();
+        if (row + gridDim.x < p.n) fetch(row + gridDim.x);
+        cta_fft<LGN>(v, sm.buf, t, w);
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < 8; ++m) sm.buf[t + m * T] = make_double2(v[m].x * s, -(v[m].y * s));
+        __syncthreads();
+        double2* xo = reinterpret_cast<double2*>(p.xo + row * Lr);
+        for (int i = t; i < N; i += T) __stcs(xo + i, make_double2(xb[i], xb[Lr - 1 - i]));
+    }
+}
+
 // DTW (reference dtw.py:40-106) -----------------------
 struct DtwParams {
     const double* a;
@@ -690,6 +905,22 @@ int init_device(int dev) {
     SA_CUDA(cudaFuncSetAttribute(rfft_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(irfft_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(irfft_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(rfft_cta_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(rfft_cta_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(rfft_cta_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(rfft_cta_kernel<11>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(irfft_cta_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(irfft_cta_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(irfft_cta_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(irfft_cta_kernel<11>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(dct2_cta_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(dct2_cta_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(dct2_cta_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(dct2_cta_kernel<11>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(dct3_cta_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(dct3_cta_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(dct3_cta_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(dct3_cta_kernel<11>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(spectrum_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(spectrum_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(dct_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
@@ -1214,6 +1445,48 @@ int fft_plan_smem(int dev, int64_t L, int* lcap, size_t* smem, int* grid, const 
     return SA_OK;
 }
 
+// CTA transform path: even length, power-of-two complex length N = L / 2
+// in [256, 2048] (SA_CTA_FFT=0 disables).  T = N / 8 threads, 16 N bytes.
+bool cta_fft_len(int64_t L, std::initializer_list<const void*> aligned16) {
+    const int64_t N = L / 2;
+    for (const void* q : aligned16)  // 16-byte row accesses (cp.async / double2 stores)
+        if (reinterpret_cast<uintptr_t>(q) & 15) return false;
+    return (L % 2 == 0) && N >= 256 && N <= 2048 && (N & (N - 1)) == 0 && env_int("SA_CTA_FFT", 1) != 0;
+}
+// kernel instantiation for N = L / 2 = 2^lg (8 <= lg <= 11)
+#define SA_CTA_PICK(kern)                                                     \
+    inline const void* pick_##kern(int64_t L) {                               \
+        switch (L / 2) {                                                      \
+            case 256: return (const void*)kern<8>;                            \
+            case 512: return (const void*)kern<9>;                            \
+            case 1024: return (const void*)kern<10>;                          \
+            default: return (const void*)kern<11>;                            \
+        }                                                                     \
+    }
+SA_CTA_PICK(rfft_cta_kernel)
+SA_CTA_PICK(irfft_cta_kernel)
+SA_CTA_PICK(dct2_cta_kernel)
+SA_CTA_PICK(dct3_cta_kernel)
+
+int cta_launch(const void* kern, int grid, int threads, size_t smem, cudaStream_t st, FftParams& p) {
+    void* args[] = {&p};
+    SA_CUDA(cudaLaunchKernel(kern, dim3(grid), dim3(threads), args, smem, st));
+    __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
+    return SA_OK;
+}
+
+int cta_launch_shape(int dev, const void* kern, int64_t L, int64_t n, int* threads, size_t* smem, int* grid) {
+    const int64_t N = L / 2;
+    *threads = (int)(N / 8);
+    *smem = 16 * (size_t)(2 * N + 1);
+    int per_sm = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, *threads, *smem);
+    if (e != cudaSuccess) return cuda_fail(e, "occupancy");
+    const int64_t g = (int64_t)dev_state(dev).sms * std::max(per_sm, 1);
+    *grid = (int)std::max<int64_t>(1, std::min<int64_t>(g, n));
+    return SA_OK;
+}
+
 // global scratch for a transform launch (freed stream-ordered by the caller)
 int alloc_row_bufs(bool global, int lcap, int grid, cudaStream_t st, double** out) {
     *out = nullptr;
@@ -1439,6 +1712,14 @@ int sa_fft_forward(const double* d_in, int64_t n, int64_t len, double* d_re, dou
     rc = get_twiddles(dev, (int)len, &p.tw);
     if (!rc) rc = finish_geo(dev, &p.fft);
     if (rc) return rc;
+    if (cta_fft_len(len, {d_in})) {
+        int threads, grid;
+        size_t smem;
+        const void* kern = pick_rfft_cta_kernel(len);
+        rc = cta_launch_shape(dev, kern, len, n, &threads, &smem, &grid);
+        if (rc || n == 0) return rc;
+        return cta_launch(kern, grid, threads, smem, (cudaStream_t)stream, p);
+    }
     size_t smem;
     int lcap, grid;
     bool global;
@@ -1468,6 +1749,14 @@ int sa_fft_inverse(const double* d_re, const double* d_im, int64_t n, int64_t le
     rc = get_twiddles(dev, (int)len, &p.tw);
     if (!rc) rc = finish_geo(dev, &p.fft);
     if (rc) return rc;
+    if (cta_fft_len(len, {d_out})) {
+        int threads, grid;
+        size_t smem;
+        const void* kern = pick_irfft_cta_kernel(len);
+        rc = cta_launch_shape(dev, kern, len, n, &threads, &smem, &grid);
+        if (rc || n == 0) return rc;
+        return cta_launch(kern, grid, threads, smem, (cudaStream_t)stream, p);
+    }
     size_t smem;
     int lcap, grid;
     bool global;
@@ -1499,6 +1788,14 @@ static int dct_launch(const double* d_in, int64_t n, int64_t len, double* d_out,
     rc = get_dct_twiddles(dev, (int)len, &p.dtw);
     if (!rc) rc = finish_geo(dev, &p.fft);
     if (rc) return rc;
+    if (cta_fft_len(len, {d_in, d_out})) {
+        int threads, grid;
+        size_t smem;
+        const void* kern = inverse ? pick_dct3_cta_kernel(len) : pick_dct2_cta_kernel(len);
+        rc = cta_launch_shape(dev, kern, len, n, &threads, &smem, &grid);
+        if (rc || n == 0) return rc;
+        return cta_launch(kern, grid, threads, smem, (cudaStream_t)stream, p);
+    }
     size_t smem;
     int lcap, grid;
     bool global;
