@@ -703,6 +703,153 @@ __global__ void __launch_bounds__(256) dct3_cta_kernel(const __grid_constant__ F
     }
 }
 
+// Spectral-only chains (every stage FrequencyMask / RandomSinusoid, e.g.
+// BASELINE config 3) on the CTA FFT: one CTA per row, rfft -> the fired
+// stages' perturbations on the bins -> irfft, the row never leaving the SM
+// (freqaugment.py:37-47, 131-170 + BASELINE M6; the warp chain's op_spectral
+// with spectrum residency).  Warp 0 draws each stage's gate and scalars (one
+// lane per stage, SStream); rows none of whose stages fire are copied.
+template <int LGN>
+__global__ void __launch_bounds__(256) spectral_cta_kernel(const __grid_constant__ ChainParams p,
+                                                           const double2* __restrict__ tw) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int T = CtaPlan<LGN>::T, N = 1 << LGN;
+    const int t = threadIdx.x;
+    const int L = 2 * N, bins = N + 1;
+    const CtaSmem sm = cta_smem(smem, N);
+    __shared__ uint64_t s_fire;
+    __shared__ int s_pos[64];        // mask start / sinusoid bin of stage j
+    __shared__ double2 s_add[64];    // sinusoid increment of stage j
+    __shared__ double2 s_nyq;
+    double2 w[8], ws[8];
+    cta_twiddles<LGN>(w, t, tw, LGN + 1);
+#pragma unroll
+    for (int m = 0; m < 8; ++m) ws[m] = __ldg(&tw[t + m * T]);
+    const double2 wn = __ldg(&tw[N]);
+    auto fetch = [&](int64_t row) {
+        const double2* xr = reinterpret_cast<const double2*>(p.in + row * L);
+        for (int i = t; i < N; i += T) cp_async16(&sm.nb[i], xr + i);
+        cp_async_commit();
+    };
+    if (blockIdx.x < p.rows_out) fetch(blockIdx.x);
+    bool bad = false;
+    for (int64_t row = blockIdx.x; row < p.rows_out; row += gridDim.x) {
+        if (t < 32) {  // gates and draws, stage j on lane j % 32
+            uint64_t fire = 0;
+            for (int j0 = 0; j0 < p.ns; j0 += 32) {
+                const int j = j0 + t;
+                bool f = false;
+                if (j < p.ns) {
+                    const DevStage& st = p.st[j];
+                    uint64_t k0, k1;
+                    derive_key(p.seed, (uint64_t)st.index, (uint64_t)(p.offset + row), k0, k1);
+                    SStream s;
+                    s_init(s, k0, k1);
+                    f = s_next_double(s) < st.prob && !spectral_noop(st);
+                    if (f && st.op == SA_OP_FREQ_MASK) {
+                        const int wd = (int)st.i[0];
+                        int start = (int)s_bounded(s, (uint32_t)(bins - 1)) - wd / 2;
+                        if (start < 0) start = 0;
+                        if (start > bins - wd) start = bins - wd;
+                        s_pos[j] = start;
+                    } else if (f) {  // SA_OP_SINUSOID
+                        const int mb = (int)st.i[0];
+                        const int b = mb + (int)s_bounded(s, (uint32_t)(bins - mb - 1));
+                        const double phi = (2.0 * 3.14159265358979323846) * s_next_double(s);
+                        const double A = st.f[0];
+                        s_pos[j] = b;
+                        if (b == 0 || b == bins - 1) {
+                            s_add[j] = make_double2((A * (double)L) * cos(phi), 0.0);
+                        } else {
+                            const double h = (A * (double)L) * 0.5;
+                            s_add[j] = make_double2(h * cos(phi), h * sin(phi));
+                        }
+                    }
+                }
+                fire |= (uint64_t)__ballot_sync(SA_FULL, f) << j0;
+            }
+            if (t == 0) s_fire = fire;
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        double2 v[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            v[m] = sm.nb[t + m * T];
+            bad |= nonfinite(v[m].x) | nonfinite(v[m].y);  // Batch invariant (core.py:104)
+        }
+        const uint64_t fire = s_fire;
+        __syncthreads();
+        if (row + gridDim.x < p.rows_out) fetch(row + gridDim.x);
+        double2* xo = reinterpret_cast<double2*>(p.out + row * L);
+        if (!fire) {
+#pragma unroll
+            for (int m = 0; m < 8; ++m) __stcs(xo + t + m * T, v[m]);
+            continue;
+        }
+        cta_fft<LGN>(v, sm.buf, t, w);
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < 8; ++m) sm.buf[t + m * T] = v[m];
+        __syncthreads();
+        double2 X[8];  // bins t + m T (DC / Nyquist imaginary parts pinned to 0)
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const int k = t + m * T;
+            X[m] = cta_split(sm.buf[k], sm.buf[k == 0 ? 0 : N - k], ws[m]);
+        }
+        double2 nyq = cta_split(sm.buf[0], sm.buf[0], wn);
+        if (t == 0) X[0].y = 0.0;
+        nyq.y = 0.0;
+        for (uint64_t f = fire; f; f &= f - 1) {  // stages in chain order
+            const int j = __ffsll((long long)f) - 1;
+            const DevStage& st = p.st[j];
+            const int pos = s_pos[j];
+            if (st.op == SA_OP_FREQ_MASK) {
+                const int end = pos + (int)st.i[0];
+#pragma unroll
+                for (int m = 0; m < 8; ++m) {
+                    const int k = t + m * T;
+                    if (k >= pos && k < end) X[m] = make_double2(0.0, 0.0);
+                }
+                if (N >= pos && N < end) nyq = make_double2(0.0, 0.0);
+            } else {
+                const double2 a = s_add[j];
+                if (pos == N) {
+                    nyq.x = nyq.x + a.x;
+                } else {
+#pragma unroll
+                    for (int m = 0; m < 8; ++m) {
+                        if (t + m * T == pos) {
+                            X[m].x = X[m].x + a.x;
+                            if (pos != 0) X[m].y = X[m].y + a.y;
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();  // the split's reads of the buffer are done
+#pragma unroll
+        for (int m = 0; m < 8; ++m) sm.buf[t + m * T] = X[m];
+        if (t == 0) s_nyq = nyq;
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const int k = t + m * T;
+            v[m] = cta_fold(sm.buf[k], k == 0 ? s_nyq : sm.buf[N - k], ws[m], k == 0);
+        }
+        cta_fft<LGN>(v, sm.buf, t, w);
+        const double sc = 1.0 / (double)N;
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const double2 o = make_double2(v[m].x * sc, -(v[m].y * sc));
+            bad |= nonfinite(o.x) | nonfinite(o.y);
+            __stcs(xo + t + m * T, o);
+        }
+    }
+    if (__any_sync(SA_FULL, bad) && (t & 31) == 0) atomicOr(p.flags, SA_FLAG_NONFINITE);
+}
+
 // DTW (reference dtw.py:40-106) -----------------------
 struct DtwParams {
     const double* a;
@@ -905,6 +1052,30 @@ int init_device(int dev) {
     SA_CUDA(cudaFuncSetAttribute(rfft_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(irfft_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(irfft_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    {
+        cudaFuncAttributes fa;
+        SA_CUDA(cudaFuncGetAttributes(&fa, spectral_cta_kernel<8>));
+        SA_CUDA(cudaFuncSetAttribute(spectral_cta_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     optin - (int)fa.sharedSizeBytes));
+    }
+    {
+        cudaFuncAttributes fa;
+        SA_CUDA(cudaFuncGetAttributes(&fa, spectral_cta_kernel<9>));
+        SA_CUDA(cudaFuncSetAttribute(spectral_cta_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     optin - (int)fa.sharedSizeBytes));
+    }
+    {
+        cudaFuncAttributes fa;
+        SA_CUDA(cudaFuncGetAttributes(&fa, spectral_cta_kernel<10>));
+        SA_CUDA(cudaFuncSetAttribute(spectral_cta_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     optin - (int)fa.sharedSizeBytes));
+    }
+    {
+        cudaFuncAttributes fa;
+        SA_CUDA(cudaFuncGetAttributes(&fa, spectral_cta_kernel<11>));
+        SA_CUDA(cudaFuncSetAttribute(spectral_cta_kernel<11>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     optin - (int)fa.sharedSizeBytes));
+    }
     SA_CUDA(cudaFuncSetAttribute(rfft_cta_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(rfft_cta_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(rfft_cta_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
@@ -1376,9 +1547,44 @@ struct StreamScratch {
     }
 };
 
+bool cta_fft_len(int64_t L, std::initializer_list<const void*> aligned16);
+int cta_launch_shape(int dev, const void* kern, int64_t L, int64_t n, int* threads, size_t* smem, int* grid);
+
+// Spectral-only chain on the CTA FFT (spectral_cta_kernel): every stage a
+// FrequencyMask / RandomSinusoid, length L = 2N with N = 256 .. 2048 a power
+// of two, no Repeat, rows 16-byte aligned.  Returns the W_L table or null.
+const double2* spectral_cta_table(const Plan* plan) {
+    const ChainParams& p = plan->p;
+    const int64_t L = p.len_in;
+    if (plan->global || p.repeat_r != 1 || p.len_out != L || p.ns < 1 || p.ns > 64 ||
+        env_int("SA_CTA_CHAIN", 1) == 0 || !cta_fft_len(L, {p.in, p.out}))
+        return nullptr;
+    const double2* tw = nullptr;
+    for (int j = 0; j < p.ns; ++j) {
+        if (p.st[j].op != SA_OP_FREQ_MASK && p.st[j].op != SA_OP_SINUSOID) return nullptr;
+        if (p.st[j].tw) tw = p.st[j].tw;
+    }
+    return tw;
+}
+
 int launch_chain(Plan* plan, cudaStream_t stream) {
     ChainParams& p = plan->p;
     if (p.rows_out == 0) return SA_OK;
+    if (const double2* tw = spectral_cta_table(plan)) {
+        const int64_t N = p.len_in / 2;
+        const void* kern = N == 256 ? (const void*)spectral_cta_kernel<8>
+                         : N == 512 ? (const void*)spectral_cta_kernel<9>
+                         : N == 1024 ? (const void*)spectral_cta_kernel<10> : (const void*)spectral_cta_kernel<11>;
+        int threads, grid;
+        size_t smem;
+        int rc = cta_launch_shape(current_device_id(), kern, p.len_in, p.rows_out, &threads, &smem, &grid);
+        if (rc) return rc;
+        p.order = nullptr;
+        void* args[] = {&p, (void*)&tw};
+        SA_CUDA(cudaLaunchKernel(kern, dim3(grid), dim3(threads), args, smem, stream));
+        __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
+        return SA_OK;
+    }
     DeviceState& ds = dev_state(current_device_id());
     StreamScratch scratch(stream);
     p.order = nullptr;

@@ -149,6 +149,54 @@ __device__ __forceinline__ uint32_t next32(WStream& s, int lane) {
 
 __device__ __forceinline__ double next_double(WStream& s, int lane) { return u53(next64(s, lane)); }
 
+// One thread's private stream (the CTA spectral kernel draws each stage's
+// few scalars on one lane): the same numpy semantics as WStream's scalar
+// draws -- block b = philox(key, b + 1), buffered upper 32-bit halves.
+struct SStream {
+    uint64_t k0, k1, wpos, blk;
+    uint64_t w0, w1, w2, w3;
+    uint32_t has32, u32;
+};
+__device__ __forceinline__ void s_init(SStream& s, uint64_t k0, uint64_t k1) {
+    s.k0 = k0; s.k1 = k1; s.wpos = 0; s.blk = ~0ull; s.has32 = 0; s.u32 = 0;
+}
+__device__ __forceinline__ uint64_t s_next64(SStream& s) {
+    const uint64_t b = s.wpos >> 2;
+    if (b != s.blk) {
+        philox(s.k0, s.k1, b + 1, s.w0, s.w1, s.w2, s.w3);
+        s.blk = b;
+    }
+    const uint32_t q = (uint32_t)(s.wpos & 3);
+    s.wpos += 1;
+    return q == 0 ? s.w0 : (q == 1 ? s.w1 : (q == 2 ? s.w2 : s.w3));
+}
+__device__ __forceinline__ uint32_t s_next32(SStream& s) {
+    if (s.has32) {
+        s.has32 = 0;
+        return s.u32;
+    }
+    const uint64_t v = s_next64(s);
+    s.has32 = 1;
+    s.u32 = (uint32_t)(v >> 32);
+    return (uint32_t)v;
+}
+__device__ __forceinline__ double s_next_double(SStream& s) { return u53(s_next64(s)); }
+__device__ __forceinline__ uint32_t s_bounded(SStream& s, uint32_t rng) {  // = bounded()
+    if (rng == 0) return 0;
+    if (rng == 0xFFFFFFFFu) return s_next32(s);
+    const uint32_t ex = rng + 1u;
+    uint64_t m = (uint64_t)s_next32(s) * ex;
+    uint32_t left = (uint32_t)m;
+    if (left < ex) {
+        const uint32_t th = (0u - ex) % ex;
+        while (left < th) {
+            m = (uint64_t)s_next32(s) * ex;
+            left = (uint32_t)m;
+        }
+    }
+    return (uint32_t)(m >> 32);
+}
+
 // Generator.integers(0, rng + 1): numpy random_bounded_uint64, 32-bit Lemire.
 __device__ __forceinline__ uint32_t bounded(WStream& s, int lane, uint32_t rng) {
     if (rng == 0) return 0;

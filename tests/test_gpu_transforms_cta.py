@@ -58,3 +58,58 @@ def test_cta_matches_warp_kernels(L, monkeypatch):
     b = run()
     for u, v in zip(a, b):
         assert np.abs(u - v).max() <= 1e-12 * max(1.0, np.abs(v).max())
+
+
+# ---------------------------------------------------------------- spectral-only chains
+def _spectral_chains(L):
+    from paper_2601_03159_b200 import FrequencyMask, Pipeline, RandomSinusoid
+
+    bins = L // 2 + 1
+    return [
+        Pipeline(stages=(FrequencyMask(L // 20, probability=0.5), RandomSinusoid(0.5, probability=0.5)),
+                 master_seed=3),  # BASELINE config 3's shape
+        Pipeline(stages=(RandomSinusoid(1.0, min_bin=0), FrequencyMask(0), RandomSinusoid(0.3, min_bin=bins - 2),
+                         FrequencyMask(bins, probability=0.3), RandomSinusoid(2.0, probability=0.7)),
+                 master_seed=11),  # DC / Nyquist bins, a no-op mask, a mask over every bin
+        Pipeline(stages=(FrequencyMask(7),), master_seed=5),
+    ]
+
+
+@pytest.mark.parametrize("L", [512, 1024, 2048, 4096])
+def test_cta_spectral_chain_vs_oracle(L):
+    import torch
+
+    from oracle import oracle as O
+
+    x = walks(300, L, L)
+    for pipe in _spectral_chains(L):
+        got = pipe.run_device(torch.from_numpy(x).cuda(), series_offset=17).cpu().numpy()
+        want = O.run_pipeline(pipe, x[:64], series_offset=17)
+        assert np.abs(got[:64] - want).max() <= spectral_tol(want), pipe.stages
+        # rows whose stages all stay off are copied bitwise
+        same = np.flatnonzero(np.all(want == x[:64], axis=1))
+        assert np.array_equal(got[same], x[same])
+
+
+@pytest.mark.parametrize("L", [512, 2048])
+def test_cta_spectral_chain_matches_warp_chain(L, monkeypatch):
+    import torch
+
+    x = torch.from_numpy(walks(500, L, 3)).cuda()
+    for pipe in _spectral_chains(L):
+        a = pipe.run_device(x).cpu().numpy()
+        monkeypatch.setenv("SA_CTA_CHAIN", "0")
+        b = pipe.run_device(x).cpu().numpy()
+        monkeypatch.delenv("SA_CTA_CHAIN")
+        assert np.abs(a - b).max() <= 1e-11 * max(1.0, np.abs(b).max())
+
+
+def test_cta_spectral_chain_nonfinite_input():
+    import torch
+
+    from paper_2601_03159_b200 import InvalidInputError
+
+    x = walks(40, 1024, 1)
+    x[13, 100] = np.nan
+    with pytest.raises(InvalidInputError):
+        _spectral_chains(1024)[0].run_device(torch.from_numpy(x).cuda())
