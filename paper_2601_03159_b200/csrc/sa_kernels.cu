@@ -710,7 +710,7 @@ __global__ void __launch_bounds__(256) dct3_cta_kernel(const __grid_constant__ F
 // with spectrum residency).  Warp 0 draws each stage's gate and scalars (one
 // lane per stage, SStream); rows none of whose stages fire are copied.
 template <int LGN>
-__global__ void __launch_bounds__(256) spectral_cta_kernel(const __grid_constant__ ChainParams p,
+__global__ void __launch_bounds__(CtaPlan<LGN>::T, 512 / CtaPlan<LGN>::T) spectral_cta_kernel(const __grid_constant__ ChainParams p,
                                                            const double2* __restrict__ tw) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int T = CtaPlan<LGN>::T, N = 1 << LGN;
@@ -721,10 +721,16 @@ __global__ void __launch_bounds__(256) spectral_cta_kernel(const __grid_constant
     __shared__ int s_pos[64];        // mask start / sinusoid bin of stage j
     __shared__ double2 s_add[64];    // sinusoid increment of stage j
     __shared__ double2 s_nyq;
-    double2 w[8], ws[8];
+    double2 w[8];
     cta_twiddles<LGN>(w, t, tw, LGN + 1);
+#ifndef SA_SPEC_WS
+#define SA_SPEC_WS 1
+#endif
+    double2 ws[8];
+    if (SA_SPEC_WS) {
 #pragma unroll
-    for (int m = 0; m < 8; ++m) ws[m] = __ldg(&tw[t + m * T]);
+        for (int m = 0; m < 8; ++m) ws[m] = __ldg(&tw[t + m * T]);
+    }
     const double2 wn = __ldg(&tw[N]);
     auto fetch = [&](int64_t row) {
         const double2* xr = reinterpret_cast<const double2*>(p.in + row * L);
@@ -796,7 +802,7 @@ __global__ void __launch_bounds__(256) spectral_cta_kernel(const __grid_constant
 #pragma unroll
         for (int m = 0; m < 8; ++m) {
             const int k = t + m * T;
-            X[m] = cta_split(sm.buf[k], sm.buf[k == 0 ? 0 : N - k], ws[m]);
+            X[m] = cta_split(sm.buf[k], sm.buf[k == 0 ? 0 : N - k], SA_SPEC_WS ? ws[m] : __ldg(&tw[k]));
         }
         double2 nyq = cta_split(sm.buf[0], sm.buf[0], wn);
         if (t == 0) X[0].y = 0.0;
@@ -836,7 +842,7 @@ __global__ void __launch_bounds__(256) spectral_cta_kernel(const __grid_constant
 #pragma unroll
         for (int m = 0; m < 8; ++m) {
             const int k = t + m * T;
-            v[m] = cta_fold(sm.buf[k], k == 0 ? s_nyq : sm.buf[N - k], ws[m], k == 0);
+            v[m] = cta_fold(sm.buf[k], k == 0 ? s_nyq : sm.buf[N - k], SA_SPEC_WS ? ws[m] : __ldg(&tw[k]), k == 0);
         }
         cta_fft<LGN>(v, sm.buf, t, w);
         const double sc = 1.0 / (double)N;
