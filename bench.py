@@ -126,7 +126,7 @@ def ncu_traffic(cfg):
     if os.path.exists(p):
         with open(p) as fh:
             d = json.load(fh)
-        v = d.get(f"config{cfg}")
+        v = d.get(cfg if isinstance(cfg, str) else f"config{cfg}")
         if v:
             return v
     return None
@@ -669,8 +669,8 @@ def run_transforms(args, rank):
         "config": {"workload": TR_WORKLOAD, "n_series": n, "len": L, "round_trip_max_err": err,
                    "l2": "inputs larger than L2 (no flush needed)"},
         "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                     "traffic": None, "peak_source": src, "algorithmic_bytes_per_step": byts,
-                     "scope": "rfft_kernel + irfft_kernel + 2 x dct_kernel"},
+                     "traffic": ncu_traffic("transforms"), "peak_source": src, "algorithmic_bytes_per_step": byts,
+                     "scope": "rfft_cta_kernel + irfft_cta_kernel + dct2_cta_kernel + dct3_cta_kernel (L = 2048: CTA-cooperative register FFT)"},
         "e2e": {"value": pts / e2e_s, "unit": "points/s", "h2d_bytes_per_step": 8 * n * L * 3 + 16 * n * B,
                 "d2h_bytes_per_step": 8 * n * L * 3 + 16 * n * B},
         "gpu_launches": int(launches), "clocks": clocks,

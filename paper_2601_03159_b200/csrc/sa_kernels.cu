@@ -506,9 +506,13 @@ __device__ __forceinline__ CtaSmem cta_smem(unsigned char* smem, int N) {
     return {b, b + N};
 }
 
+#ifndef SA_CTA_MINB
+#define SA_CTA_MINB 512  // min CTAs per SM x T: a register cap of 65536 / SA_CTA_MINB
+#endif
+
 // rfft (freqtransform.py:101-108): real row (N complex) -> bins 0..N
 template <int LGN>
-__global__ void __launch_bounds__(256) rfft_cta_kernel(const __grid_constant__ FftParams p) {
+__global__ void __launch_bounds__(CtaPlan<LGN>::T, SA_CTA_MINB / CtaPlan<LGN>::T) rfft_cta_kernel(const __grid_constant__ FftParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int T = CtaPlan<LGN>::T;
     const int t = threadIdx.x;
@@ -558,7 +562,7 @@ __global__ void __launch_bounds__(256) rfft_cta_kernel(const __grid_constant__ F
 
 // irfft (freqtransform.py:110-116): bins 0..N (separate re / im rows) -> real row
 template <int LGN>
-__global__ void __launch_bounds__(256) irfft_cta_kernel(const __grid_constant__ FftParams p) {
+__global__ void __launch_bounds__(CtaPlan<LGN>::T, SA_CTA_MINB / CtaPlan<LGN>::T) irfft_cta_kernel(const __grid_constant__ FftParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int T = CtaPlan<LGN>::T;
     const int t = threadIdx.x;
@@ -602,7 +606,7 @@ __global__ void __launch_bounds__(256) irfft_cta_kernel(const __grid_constant__ 
 // dct2_any / dct3_any's formulas; the Makhoul permutation is applied by the
 // row fetch (II: v[i] = x[2i], v[Lr-1-i] = x[2i+1]) or the row store (III).
 template <int LGN>
-__global__ void __launch_bounds__(256) dct2_cta_kernel(const __grid_constant__ FftParams p) {
+__global__ void __launch_bounds__(CtaPlan<LGN>::T, SA_CTA_MINB / CtaPlan<LGN>::T) dct2_cta_kernel(const __grid_constant__ FftParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int T = CtaPlan<LGN>::T;
     const int t = threadIdx.x;
@@ -657,7 +661,7 @@ __global__ void __launch_bounds__(256) dct2_cta_kernel(const __grid_constant__ F
 }
 
 template <int LGN>
-__global__ void __launch_bounds__(256) dct3_cta_kernel(const __grid_constant__ FftParams p) {
+__global__ void __launch_bounds__(CtaPlan<LGN>::T, SA_CTA_MINB / CtaPlan<LGN>::T) dct3_cta_kernel(const __grid_constant__ FftParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int T = CtaPlan<LGN>::T;
     const int t = threadIdx.x;
