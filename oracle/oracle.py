@@ -40,6 +40,7 @@ def lib():
         L.sao_raw.argtypes = [u64, u64, u64, i64, vp]
         L.sao_normals.argtypes = [u64, u64, u64, i64, ctypes.c_double, ctypes.c_double, vp]
         L.sao_doubles.argtypes = [u64, u64, u64, i64, vp]
+        L.sao_normals_words.argtypes = [vp, i64, i64, i64, vp, vp]
         L.sao_script.argtypes = [u64, u64, u64, i64, vp, vp, vp]
         L.sao_permutation.argtypes = [u64, u64, u64, i64, vp]
         L.sao_choice.argtypes = [u64, u64, u64, i64, i64, vp]
@@ -128,6 +129,15 @@ def normals(seed, j, i, n, loc=0.0, scale=1.0):
     out = np.empty(n)
     lib().sao_normals(seed, j, i, n, loc, scale, _p(out))
     return out
+
+
+def normals_words(words: np.ndarray, n: int, skip: int = 0):
+    """numpy's ziggurat on a crafted word stream: (n normals, position after)."""
+    w = np.ascontiguousarray(words, dtype=np.uint64)
+    out = np.empty(n)
+    pos = ctypes.c_int64(0)
+    lib().sao_normals_words(_p(w), w.size, skip, n, _p(out), ctypes.byref(pos))
+    return out, pos.value
 
 
 def doubles(seed, j, i, n):

@@ -14,11 +14,12 @@
 //     upper half: a 64-bit word serves two 32-bit draws, low half first, and
 //     the buffered half survives intervening 64-bit draws.
 //   * The ziggurat normal consumes a data-dependent number of words (one on
-//     the fast path, 99.3%; more on the wedge / tail paths).  normals() walks
-//     a window with a warp-wide min-reduction to find the next slow word:
-//     the run of fast words before it becomes normals in parallel (output
-//     index = position offset), the slow word is resolved uniformly by all
-//     lanes with the reference's exact arithmetic, and the walk continues.
+//     the fast path, 99.3%; more on the wedge / tail paths).  normals()
+//     parses a whole window in one pass: which words head a draw follows
+//     from the parity of the slow-word run before them, wedge tests run in
+//     parallel, and a warp scan of the accepted heads gives each normal its
+//     output index; tails (log1p loop) are resolved uniformly by all lanes
+//     with the reference's exact arithmetic.
 //
 // Every lane of the warp holds an identical copy of the stream state (all
 // control flow on it is warp-uniform); only emitted values are lane-private.
@@ -90,6 +91,13 @@ __device__ __forceinline__ void philox(uint64_t k0, uint64_t k1, uint64_t ctr0, 
     o0 = c0; o1 = c1; o2 = c2; o3 = c3;
 }
 
+// Words 4b..4b+3 of a stream = Philox block counter b + 1.  Test builds
+// (tests/csrc/rng_probe.cu) substitute a word array here to drive the window
+// walks through crafted streams (wedge / tail runs the generator makes rare).
+#ifndef SA_WINDOW_BLOCK
+#define SA_WINDOW_BLOCK(k0, k1, b, o0, o1, o2, o3) philox(k0, k1, (b) + 1, o0, o1, o2, o3)
+#endif
+
 __device__ __forceinline__ double u53(uint64_t w) {  // Generator.random()
     return (double)(w >> 11) * (1.0 / 9007199254740992.0);
 }
@@ -112,7 +120,7 @@ struct WStream {
 // caller's stream state stays in registers.
 __device__ __noinline__ void fill_window(uint64_t k0, uint64_t k1, uint64_t blk0, uint64_t* winbuf, int lane) {
     uint64_t o0, o1, o2, o3;
-    philox(k0, k1, blk0 + (uint64_t)lane + 1, o0, o1, o2, o3);
+    SA_WINDOW_BLOCK(k0, k1, blk0 + (uint64_t)lane, o0, o1, o2, o3);
     __syncwarp();  // every lane is done reading the previous window
     ulonglong2* w2 = reinterpret_cast<ulonglong2*>(winbuf) + 2 * lane;
     w2[0] = make_ulonglong2(o0, o1);
@@ -292,7 +300,7 @@ __device__ __forceinline__ double std_normal(WStream& s, int lane) {
 __device__ __forceinline__ void refill_inline(WStream& s, int lane) {
     const uint64_t blk0 = s.wpos >> 2;
     uint64_t o0, o1, o2, o3;
-    philox(s.k0, s.k1, blk0 + (uint64_t)lane + 1, o0, o1, o2, o3);
+    SA_WINDOW_BLOCK(s.k0, s.k1, blk0 + (uint64_t)lane, o0, o1, o2, o3);
     __syncwarp();
     ulonglong2* w2 = reinterpret_cast<ulonglong2*>(s.winbuf) + 2 * lane;
     w2[0] = make_ulonglong2(o0, o1);
@@ -303,98 +311,159 @@ __device__ __forceinline__ void refill_inline(WStream& s, int lane) {
     s.wn = SA_WIN;
 }
 
+// numpy's wedge test for slow word w (idx != 0, x its signed value) with
+// uniform word uw: accept iff fi[idx] + (fi[idx-1] - fi[idx]) * u < exp(-x^2/2).
+// float pre-test: __expf is within ~1e-6 relative of exp(e2); only near-ties
+// fall back to the double exp the reference compares with.
+__device__ __forceinline__ bool zig_wedge_accept(uint64_t w, double x, uint64_t uw) {
+    const int idx = (int)(w & 0xff);
+    const double u = u53(uw);
+    const double fi0 = __ldg(&g_fi[idx - 1]), fi1 = __ldg(&g_fi[idx]);
+    const double lhs = (fi0 - fi1) * u + fi1;
+    const double e2 = -0.5 * x * x;  // |x| < 3.66 on the wedge: e2 > -6.7
+    const double ef = (double)__expf((float)e2);
+    const double d = lhs - ef;
+    return (fabs(d) > 1e-5 * ef) ? (d < 0.0) : (lhs < exp(e2));
+}
+
 // `count` standard normals in stream order; emit(k, z) is called exactly
 // once per k by exactly one lane (k = normal index 0..count-1).
 // zig: the fast-path table (shared memory copy of g_zig).
+//
+// One pass per window parses numpy's sequential word consumption in
+// parallel: a fast word is one normal; a wedge word (slow, idx != 0) takes
+// the next word as its uniform and yields a normal or nothing; so a word is
+// the HEAD of a draw iff the run of slow words right before it (within the
+// parse) has even length.  Every lane classifies its 4 words, gets the run
+// entering it from its left neighbour, evaluates its wedge heads, and a warp
+// scan of accepted heads gives each normal its output index.  The parse stops
+// (sequential resolution, then a new pass) at a tail head (idx 0, log1p
+// loop), a wedge head whose uniform lies past the window, or in a lane whose
+// 4 words are all slow (the entering run would need more than one neighbour).
+// Head bits of a lane's 4 words from its slow bits and the parity of the
+// slow run entering it: word r heads a draw iff the run before it is even.
+__host__ __device__ constexpr uint64_t zig_head_table(int pin) {
+    uint64_t t = 0;
+    for (int sl = 0; sl < 16; ++sl) {
+        int h = !pin, bits = h;
+        for (int r = 1; r < 4; ++r) {
+            h = ((sl >> (r - 1)) & 1) ? !h : 1;
+            bits |= h << r;
+        }
+        t |= (uint64_t)bits << (4 * sl);
+    }
+    return t;
+}
+
 template <class Emit>
 __device__ __forceinline__ void normals(WStream& s, int lane, int count, const ZigEntry* __restrict__ zig,
                                         Emit&& emit) {
+    constexpr uint64_t kHead0 = zig_head_table(0), kHead1 = zig_head_table(1);
+    const uint32_t lt = (1u << lane) - 1u;
     int k = 0;
     while (k < count) {
         if (s.wpos >= s.wb + s.wn) refill_inline(s, lane);
         const uint32_t wn = s.wn;
-        uint32_t sp = (uint32_t)(s.wpos - s.wb);
-        // classify this lane's words (window positions 4*lane + r)
-        double z[4];
-        uint32_t slowbits = 0;
-        {
-            uint64_t wv[4];
-            if (4u * lane < wn) {
-                const ulonglong2* w2 = reinterpret_cast<const ulonglong2*>(s.win) + 2 * lane;
-                ulonglong2 a = w2[0], b = w2[1];
-                wv[0] = a.x; wv[1] = a.y; wv[2] = b.x; wv[3] = b.y;
-            } else {
-                wv[0] = wv[1] = wv[2] = wv[3] = 0;
-            }
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const uint64_t w = wv[r];
-                const uint64_t rr = w >> 8;
-                const uint64_t rabs = (rr >> 1) & 0x000fffffffffffffULL;
-                const ZigEntry ze = zig[w & 0xff];
-                const double x = (double)rabs * ze.wi;
-                z[r] = (rr & 1) ? -x : x;
-                if (!(rabs < ze.ki)) slowbits |= 1u << r;
-            }
-            if (4u * lane >= wn) slowbits = 0;
+        const uint32_t sp = (uint32_t)(s.wpos - s.wb);
+        const uint32_t p0 = 4u * lane;
+        uint64_t wv[4];
+        if (p0 < wn) {
+            const ulonglong2* w2 = reinterpret_cast<const ulonglong2*>(s.win) + 2 * lane;
+            ulonglong2 a = w2[0], b = w2[1];
+            wv[0] = a.x; wv[1] = a.y; wv[2] = b.x; wv[3] = b.y;
+        } else {
+            wv[0] = wv[1] = wv[2] = wv[3] = 0;
         }
-        for (;;) {
-            // first slow word at or after sp
-            uint32_t mine = 0xffffffffu;
+        const uint64_t nx = __shfl_down_sync(SA_FULL, wv[0], 1);  // word p0 + 4
+        double z[4];
+        uint32_t pres = 0, slow = 0, tail = 0;
 #pragma unroll
-            for (int r = 3; r >= 0; --r) {
-                const uint32_t p = 4u * lane + r;
-                if (((slowbits >> r) & 1u) && p >= sp) mine = p;
-            }
-            uint32_t t = __reduce_min_sync(SA_FULL, mine);
-            t = t > wn ? wn : t;
-            uint32_t nf = t - sp;
-            if (nf > (uint32_t)(count - k)) nf = (uint32_t)(count - k);
+        for (int r = 0; r < 4; ++r) {
+            const uint64_t w = wv[r];
+            const uint64_t rr = w >> 8;
+            const uint64_t rabs = (rr >> 1) & 0x000fffffffffffffULL;
+            const ZigEntry ze = zig[w & 0xff];
+            const double x = (double)rabs * ze.wi;
+            z[r] = (rr & 1) ? -x : x;
+            const uint32_t pb = (p0 + r - sp < wn - sp) ? 1u : 0u;  // sp <= p < wn
+            const uint32_t sb = pb & (rabs < ze.ki ? 0u : 1u);
+            pres |= pb << r;
+            slow |= sb << r;
+            tail |= (sb & ((w & 0xff) == 0 ? 1u : 0u)) << r;
+        }
+        const uint32_t wedge = slow & ~tail;
+        // parity of the slow run entering this lane (trailing run of the left one)
+        const uint32_t inv = ~slow & 0xfu;
+        const uint32_t trail = inv ? (uint32_t)(__clz(inv) - 28) : 4u;
+        uint32_t pin = __shfl_up_sync(SA_FULL, trail, 1) & 1u;
+        if (lane == 0) pin = 0;
+        const uint32_t head = (uint32_t)(((pin ? kHead1 : kHead0) >> (4 * slow)) & 0xfu) & pres;
+        uint32_t stop = head & tail;
+        if (slow == 0xfu) stop |= head;
+        const uint32_t last = wn - 1u - p0;  // the window's last word, if in this lane
+        if (last < 4u) stop |= head & wedge & (1u << last);
+        const uint32_t mine = stop ? p0 + (uint32_t)(__ffs(stop) - 1) : 0xffffffffu;
+        uint32_t t = __reduce_min_sync(SA_FULL, mine);
+        t = t > wn ? wn : t;
+        // heads before t: fast heads are normals, wedge heads pass the test
+        const uint32_t below = t <= p0 ? 0u : (t - p0 >= 4u ? 0xfu : (1u << (t - p0)) - 1u);
+        uint32_t acc = head & below & ~slow;
+        uint32_t wh = head & below & wedge;
+        while (wh) {
+            const int r = __ffs(wh) - 1;
+            wh &= wh - 1;
+            const uint64_t uw = r == 0 ? wv[1] : (r == 1 ? wv[2] : (r == 2 ? wv[3] : nx));
+            const uint64_t w = r == 0 ? wv[0] : (r == 1 ? wv[1] : (r == 2 ? wv[2] : wv[3]));
+            const double x = r == 0 ? z[0] : (r == 1 ? z[1] : (r == 2 ? z[2] : z[3]));
+            if (zig_wedge_accept(w, x, uw)) acc |= 1u << r;
+        }
+        // output index of each accepted head: exclusive warp prefix of popc(acc)
+        // from three ballots of its bits (c <= 4)
+        const uint32_t c = (uint32_t)__popc(acc);
+        const uint32_t b0 = __ballot_sync(SA_FULL, c & 1u), b1 = __ballot_sync(SA_FULL, c & 2u),
+                       b2 = __ballot_sync(SA_FULL, c & 4u);
+        const uint32_t excl = __popc(b0 & lt) + 2 * __popc(b1 & lt) + 4 * __popc(b2 & lt);
+        const uint32_t tot = __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
+        const uint32_t need = (uint32_t)(count - k);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const uint32_t e = excl + (uint32_t)__popc(acc & ((1u << r) - 1u));
+            if (((acc >> r) & 1u) && e < need) emit(k + (int)e, z[r]);
+        }
+        if (tot >= need) {  // the last normal ends inside this pass
+            uint32_t endp = 0;
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
-                const uint32_t off = 4u * lane + r - sp;  // wraps when p < sp
-                if (off < nf) emit(k + (int)off, z[r]);
+                const uint32_t e = excl + (uint32_t)__popc(acc & ((1u << r) - 1u));
+                if (((acc >> r) & 1u) && e == need - 1) endp = p0 + r + ((slow >> r) & 1u) + 1u;
             }
-            k += (int)nf;
-            sp += nf;
-            if (k >= count || sp >= wn) {
-                s.wpos = s.wb + sp;
-                break;
-            }
-            // slow word at sp (numpy's wedge / tail paths), resolved uniformly
-            const uint64_t r0 = s.win[sp];
-            s.wpos = s.wb + sp + 1;
-            const int idx = (int)(r0 & 0xff);
-            const uint64_t old_wb = s.wb;
-            bool ok;
-            double v;
-            if (idx != 0) {  // wedge: one uniform, then the density test
-                const uint64_t rr = r0 >> 8;
-                const uint64_t rabs = (rr >> 1) & 0x000fffffffffffffULL;
-                double x = (double)rabs * zig[idx].wi;
-                if (rr & 1) x = -x;
-                if (s.wpos >= s.wb + s.wn) refill(s, lane);
-                const double u = u53(s.win[s.wpos - s.wb]);
-                s.wpos += 1;
-                const double fi0 = __ldg(&g_fi[idx - 1]), fi1 = __ldg(&g_fi[idx]);
-                const double lhs = (fi0 - fi1) * u + fi1;
-                const double e2 = -0.5 * x * x;  // |x| < 3.66 on the wedge: e2 > -6.7
-                // float pre-test: __expf is within ~1e-6 relative of exp(e2); only
-                // near-ties fall back to the double exp the reference compares with
-                const double ef = (double)__expf((float)e2);
-                const double d = lhs - ef;
-                ok = (fabs(d) > 1e-5 * ef) ? (d < 0.0) : (lhs < exp(e2));
-                v = x;
-            } else {
-                ok = zig_slow(s, lane, r0, v);  // tail: out of line, ~3e-4 of words
-            }
-            if (ok) {
-                if (lane == 0) emit(k, v);
-                k += 1;
-            }
-            if (k >= count || s.wb != old_wb) break;
-            sp = (uint32_t)(s.wpos - s.wb);
-            if (sp >= wn) break;
+            s.wpos = s.wb + __reduce_max_sync(SA_FULL, endp);
+            return;
+        }
+        k += (int)tot;
+        s.wpos = s.wb + t;
+        if (t >= wn) continue;
+        // stop head at t, resolved uniformly with the reference's arithmetic
+        const uint64_t r0 = s.win[t];
+        s.wpos += 1;
+        bool ok;
+        double v;
+        if (r0 & 0xff) {  // wedge (its uniform may start the next window)
+            const uint64_t rr = r0 >> 8;
+            const uint64_t rabs = (rr >> 1) & 0x000fffffffffffffULL;
+            double x = (double)rabs * zig[r0 & 0xff].wi;
+            if (rr & 1) x = -x;
+            if (s.wpos >= s.wb + s.wn) refill(s, lane);
+            const uint64_t uw = s.win[s.wpos - s.wb];
+            s.wpos += 1;
+            ok = zig_wedge_accept(r0, x, uw);
+            v = x;
+        } else {
+            ok = zig_slow(s, lane, r0, v);  // tail: out of line, ~3e-4 of words
+        }
+        if (ok) {
+            if (lane == 0) emit(k, v);
+            k += 1;
         }
     }
 }

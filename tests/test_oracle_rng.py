@@ -119,3 +119,24 @@ def test_ziggurat_tables_match_numpy():
     r = subprocess.run([sys.executable, os.path.join(here, "tools", "gen_ziggurat_tables.py"), "--check"],
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("ctx", CTX)
+def test_normals_on_word_stream_hook(ctx):
+    # the crafted-stream hook (tests/test_gpu_rng_probe.py) reads words from an
+    # array: on the Philox words of a stream it must give that stream's normals
+    raw = O.raw(*ctx, 50_000)
+    z, pos = O.normals_words(raw, 40_000)
+    assert np.array_equal(z, O.normals(*ctx, 40_000)) and pos < raw.size
+
+
+def test_crafted_stream_classes():
+    from zig_streams import crafted, ki_table
+
+    ki = ki_table()
+    assert ki.size == 256 and ki[1] == 0
+    w = crafted(4000, 0.5, 0.2, seed=1)
+    idx = (w & np.uint64(0xFF)).astype(np.int64)
+    rabs = (w >> np.uint64(9)) & np.uint64((1 << 52) - 1)
+    slow = rabs >= ki[idx]
+    assert 0.45 < slow.mean() < 0.55 and (slow & (idx == 0)).sum() > 200
