@@ -19,7 +19,9 @@ from .errors import (
     UnsupportedPlatformError,
 )
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libseriesaug_b200.so")
+# SA_LIB_PATH: an alternative build of the same backend (A/B timing, tools/ab_timing.py)
+LIB_PATH = os.environ.get("SA_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
+                                                         "libseriesaug_b200.so")
 
 _lock = threading.Lock()
 _lib = None

@@ -908,6 +908,64 @@ __device__ __forceinline__ bool spectral_noop(const DevStage& st) {
     return st.f[0] == 0.0;  // SINUSOID
 }
 
+// sin and cos of a phase perturbation: Taylor series to x^17 / x^18 (Horner
+// in x^2, explicit FMA; truncation < 1e-19 for |x| <= pi/4).  APP phases are
+// sigma_phase * N(0, 1); larger ones take CUDA's sincos (app_bin_slow).
+__device__ __forceinline__ void sincos_small(double x, double* sn, double* cs) {  // |x| <= pi/4
+    const double x2 = x * x;
+    double ps = 1.0 / 355687428096000.0;
+    ps = fma(ps, x2, -1.0 / 1307674368000.0);
+    ps = fma(ps, x2, 1.0 / 6227020800.0);
+    ps = fma(ps, x2, -1.0 / 39916800.0);
+    ps = fma(ps, x2, 1.0 / 362880.0);
+    ps = fma(ps, x2, -1.0 / 5040.0);
+    ps = fma(ps, x2, 1.0 / 120.0);
+    ps = fma(ps, x2, -1.0 / 6.0);
+    *sn = fma(x * x2, ps, x);
+    double pc = -1.0 / 6402373705728000.0;
+    pc = fma(pc, x2, 1.0 / 20922789888000.0);
+    pc = fma(pc, x2, -1.0 / 87178291200.0);
+    pc = fma(pc, x2, 1.0 / 479001600.0);
+    pc = fma(pc, x2, -1.0 / 3628800.0);
+    pc = fma(pc, x2, 1.0 / 40320.0);
+    pc = fma(pc, x2, -1.0 / 720.0);
+    pc = fma(pc, x2, 1.0 / 24.0);
+    pc = fma(pc, x2, -0.5);
+    *cs = fma(x2, pc, 1.0);
+}
+
+// One interior APP bin (freqaugment.py:117-122): r' = max(|X| + amp, 0) at
+// angle atan2(im, re) + ph, evaluated as a rotation of X by ph scaled by
+// r'/|X| (the same quantity up to rounding; spectral results are compared to
+// tolerance).  Common case: |X| and 1/|X| from one rsqrt (|X|^2 comfortably
+// normal) and the series sincos (|ph| <= pi/4); otherwise the reference's form.
+__device__ __noinline__ double2 app_bin_slow(double2 v, double a, double p) {
+    const double r = hypot(v.x, v.y);
+    double rn = r + a;
+    rn = (rn >= 0.0) ? rn : ((rn != rn) ? rn : 0.0);
+    double sn, cs;
+    if (r > 0.0) {
+        sincos(p, &sn, &cs);
+        const double f = rn / r;
+        return make_double2(f * (v.x * cs - v.y * sn), f * (v.x * sn + v.y * cs));
+    }
+    sincos(atan2(v.y, v.x) + p, &sn, &cs);
+    return make_double2(rn * cs, rn * sn);
+}
+__device__ __forceinline__ double2 app_bin(double2 v, double a, double p) {
+    const double q = fma(v.x, v.x, v.y * v.y);
+    const bool fast = q > 1e-290 && q < 1e290 && fabs(p) <= 0.78539816339744828;
+    const double inv_r = rsqrt(q);
+    const double r = q * inv_r;
+    double rn = r + a;
+    rn = (rn >= 0.0) ? rn : ((rn != rn) ? rn : 0.0);
+    double sn, cs;
+    sincos_small(p, &sn, &cs);
+    const double f = rn * inv_r;
+    const double2 y = make_double2(f * (v.x * cs - v.y * sn), f * (v.x * sn + v.y * cs));
+    return fast ? y : app_bin_slow(v, a, p);
+}
+
 // freqaugment.py:106-170 (+ BASELINE M6): perturb the half spectrum X[0..bins)
 // (interleaved complex, smem); scratch holds >= 2 * bins doubles.
 __device__ __forceinline__ void perturb_spectrum(const DevStage& st, WStream& s, double2* X, int L, double* scratch, Warp& w) {
@@ -928,21 +986,7 @@ __device__ __forceinline__ void perturb_spectrum(const DevStage& st, WStream& s,
         // same quantity without atan2 and full-range sin/cos (differs from
         // the reference's formula in rounding only; spectral results are
         // compared to tolerance).  |X| == 0 keeps the reference's form.
-        for (int b = 1 + w.lane; b < hi; b += 32) {
-            const double2 v = X[b];
-            const double r = hypot(v.x, v.y);
-            double rn = r + amp[b];
-            rn = (rn >= 0.0) ? rn : ((rn != rn) ? rn : 0.0);
-            double sn, cs;
-            if (r > 0.0) {
-                sincos(ph[b], &sn, &cs);
-                const double f = rn / r;
-                X[b] = make_double2(f * (v.x * cs - v.y * sn), f * (v.x * sn + v.y * cs));
-            } else {
-                sincos(atan2(v.y, v.x) + ph[b], &sn, &cs);
-                X[b] = make_double2(rn * cs, rn * sn);
-            }
-        }
+        for (int b = 1 + w.lane; b < hi; b += 32) X[b] = app_bin(X[b], amp[b], ph[b]);
         __syncwarp();
         if (w.lane == 0) {
             for (int q = 0; q < (even ? 2 : 1); ++q) {
