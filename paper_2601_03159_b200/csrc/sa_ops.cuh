@@ -246,9 +246,52 @@ __device__ __noinline__ double pairwise_combine(int n, const double* leafsum) {
     }
 }
 
+// n a power of two >= 128: the recursion's leaves are the 128-blocks and
+// its combine tree is perfect, so no leaf list / post-order walk is needed.
+// 8 lanes per leaf (numpy's 8 strided accumulators), a shfl_xor butterfly
+// for ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), two shfl_down levels join the
+// 4 leaves of a pass, and a perfect tree over the passes' sums (scratch).
+template <class F>
+__device__ __forceinline__ double pairwise_warp_pow2(int n, F f, double* scratch, int lane) {
+    const int nl = n >> 7;
+    const int passes = (nl + 3) >> 2;
+    const int g = lane >> 3, q = lane & 7;
+    double res = 0.0;
+    for (int ps = 0; ps < passes; ++ps) {
+        const int l = 4 * ps + g;
+        double acc = 0.0;
+        if (l < nl) {
+            const int base = 128 * l + q;
+            acc = f(base);
+#pragma unroll
+            for (int k = 1; k < 16; ++k) acc += f(base + 8 * k);
+        }
+        acc = acc + __shfl_xor_sync(SA_FULL, acc, 1);
+        acc = acc + __shfl_xor_sync(SA_FULL, acc, 2);
+        acc = acc + __shfl_xor_sync(SA_FULL, acc, 4);
+        double o = __shfl_down_sync(SA_FULL, acc, 8);
+        if (nl >= 2) acc = acc + o;
+        o = __shfl_down_sync(SA_FULL, acc, 16);
+        if (nl >= 4) acc = acc + o;
+        if (passes == 1) res = acc;
+        else if (lane == 0) scratch[ps] = acc;
+    }
+    if (passes > 1) {
+        __syncwarp();
+        for (int h = 1; h < passes; h *= 2) {
+            for (int i = lane; 2 * h * i < passes; i += 32) scratch[2 * h * i] = scratch[2 * h * i] + scratch[2 * h * i + h];
+            __syncwarp();
+        }
+        res = scratch[0];
+        __syncwarp();
+    }
+    return __shfl_sync(SA_FULL, res, 0);
+}
+
 // Pairwise sum of f(t), t < n.  scratch: >= 2 * (n / 64 + 2) doubles.
 template <class F>
 __device__ double pairwise_warp(int n, F f, double* scratch, int lane) {
+    if (n >= 128 && (n & (n - 1)) == 0) return pairwise_warp_pow2(n, f, scratch, lane);
     if (n < 8) {
         double r = 0.0;
         for (int k = 0; k < n; ++k) r += f(k);
