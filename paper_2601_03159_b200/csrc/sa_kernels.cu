@@ -1496,7 +1496,7 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
             if (stages[j].probability > 0.0 && stages[j].probability < 1.0 && stages[j].op != SA_OP_REPEAT)
                 cand.push_back({-op_cost(stages[j].op), j});
         std::stable_sort(cand.begin(), cand.end());
-        int kb = (int)std::min<size_t>(16, cand.size());
+        int kb = (int)std::min<size_t>((size_t)std::max(0, std::min(24, env_int("SA_SCHEDULE_BITS", 16))), cand.size());
         // sorted keys put similar fire patterns next to each other even when
         // buckets are sparse; only keep the histogram proportionate
         while (kb > 0 && ((int64_t)1 << kb) > 4 * p.rows_out) --kb;

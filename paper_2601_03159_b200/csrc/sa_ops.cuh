@@ -36,7 +36,7 @@ struct ChainParams {
     int32_t sync_every, key_bits;  // sync_every != 0: barriers on; fire-pattern key width
     uint64_t sync_mask;            // bit j: CTA barrier before stage j
     const int32_t* order;          // row schedule (nullptr: identity)
-    int8_t key_stage[16];          // stages whose gates form the key, most expensive first
+    int8_t key_stage[24];          // stages whose gates form the key, most expensive first
     uint64_t seed;
     int64_t offset;
     int64_t rows_out;

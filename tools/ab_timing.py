@@ -18,14 +18,22 @@ if len(sys.argv) > 1 and sys.argv[1] == "--child":
            "drift": Drift(0.5, 5), "time_warp": TimeWarp(5, 0.5), "speed_warp": SpeedWarp(3, 3.0),
            "fmask": FrequencyMask(51), "sinusoid": RandomSinusoid(0.5), "uniform": InjectNoise(UniformNoise(0.1)),
            "dropout": Dropout(0.05), "quantize": Quantize(16), "copy": Rotate(probability=0.0),
-           "window_warp": WindowWarp(128, 4, 0.5), "convolve": Convolve("hann", 7), "pool": Pool(4)}
+           "window_warp": WindowWarp(128, 4, 0.5), "convolve": Convolve("hann", 7), "pool": Pool(4),
+           "scale": Scale(0.1), "rotate": Rotate(), "reverse": Reverse(), "permute": PermuteSegments(4),
+           "gauss": InjectNoise(GaussianNoise(0.1)), "slope": InjectNoise(SlopeTrendNoise(0.5))}
     L = 1024
     x = device_walks(n, L, 5, torch.device("cuda"))
     flags = torch.zeros(1, dtype=torch.int32, device="cuda")
     res = {}
     for name in names:
-        pipe = bench_inputs.pipeline(int(name[6:])) if name.startswith("CONFIG") else \
-            Pipeline(stages=(OPS[name],), master_seed=1)
+        if name == "CONFIG5P1":  # config 5's chain with every stage firing
+            import dataclasses
+            c5 = bench_inputs.pipeline(5)
+            pipe = Pipeline(stages=tuple(dataclasses.replace(st, probability=1.0) for st in c5.stages), master_seed=5)
+        elif name.startswith("CONFIG"):
+            pipe = bench_inputs.pipeline(int(name[6:]))
+        else:
+            pipe = Pipeline(stages=(OPS[name],), master_seed=1)
         out = torch.empty((n, pipe.projected_length(L)), dtype=torch.float64, device="cuda")
         low = _engine._lower(pipe.stages, 0, True)
         for _ in range(3):
