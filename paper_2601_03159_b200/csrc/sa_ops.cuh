@@ -887,32 +887,41 @@ __device__ __forceinline__ bool op_speed_warp(const DevStage& st, WStream& s, do
     for (int m = w.lane; m <= K; m += 32) sbt[m] = (int)(((int64_t)m * L + K) / segs);
     __syncwarp();
     // segment of t: m = #{q in 1..K : sb[q] <= t}; a lane's t only grows, so
-    // m is tracked incrementally (usually no step per element)
-    auto seg_of = [&](int t, int m) {
-        while (m < K && t >= sbt[m + 1]) ++m;
-        return m;
-    };
-    auto tau_at = [&](int t, int m) { return base[m] + speeds[m] * (double)(t - sbt[m]); };
-    const double f = ((double)L - 1.0) / tau_at(L - 1, seg_of(L - 1, 0));
+    // m is tracked incrementally, with the segment's start, base and speed and
+    // the next boundary cached in registers (usually one compare per element)
+    const double f = ((double)L - 1.0) / ([&] {
+        int mm = 0;
+        while (mm < K && L - 1 >= sbt[mm + 1]) ++mm;
+        return base[mm] + speeds[mm] * (double)(L - 1 - sbt[mm]);
+    }());
     const bool cubic = st.i[1] != 0;
-    // four elements per lane per step: their segment indices first (a short
+    // four elements per lane per step: their warped positions first (a short
     // serial walk), then four independent interpolations (ILP for the long
     // tau -> floor -> gather -> cubic chain)
-    int m = 0;
+    int m = 0, sbm = sbt[0];
+    int nb = K > 0 ? sbt[1] : 0x7fffffff;
+    double bm = base[0], spm = speeds[0];
     for (int t0 = w.lane; t0 < L; t0 += 128) {
-        int ms[4];
+        double taus[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int t = t0 + 32 * q;
-            if (t < L) m = seg_of(t, m);
-            ms[q] = m;
+            if (t < L) {
+                while (t >= nb) {
+                    ++m;
+                    sbm = nb;
+                    bm = base[m];
+                    spm = speeds[m];
+                    nb = m < K ? sbt[m + 1] : 0x7fffffff;
+                }
+            }
+            const int tt = t < L ? t : L - 1;
+            taus[q] = (tt == L - 1) ? (double)L - 1.0 : (bm + spm * (double)(tt - sbm)) * f;
         }
         double ys[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            const int t = t0 + 32 * q;
-            const int tt = t < L ? t : L - 1;
-            const double tau = (tt == L - 1) ? (double)L - 1.0 : tau_at(tt, ms[q]) * f;
+            const double tau = taus[q];
             int j = (int)floor(tau);
             j = j < 0 ? 0 : (j > L - 2 ? L - 2 : j);
             const double fr = tau - (double)j;
