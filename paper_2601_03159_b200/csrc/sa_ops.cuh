@@ -121,6 +121,34 @@ __device__ __forceinline__ double interp_slopes(double x, const double* __restri
     return r;
 }
 
+// np.interp(t, xp, fp) for every integer t in [0, L), xp non-decreasing,
+// with numpy's precomputed slopes sl: segment by segment, so the bracketing
+// interval ("largest j with xp[j] <= t") is warp-uniform and held in
+// registers -- no per-element search or table loads.  f(t, value) is called
+// exactly once per t, by one lane.  Same arithmetic as interp_slopes.
+template <class F>
+__device__ __forceinline__ void interp_arange(const double* __restrict__ xp, const double* __restrict__ fp,
+                                              const double* __restrict__ sl, int n, int L, int lane, F&& f) {
+    int t = (int)ceil(xp[0]);  // t < xp[0]: fp[0]
+    t = t < 0 ? 0 : (t > L ? L : t);
+    for (int u = lane; u < t; u += 32) f(u, fp[0]);
+    for (int j = 0; j < n - 1 && t < L; ++j) {
+        const double xj = xp[j], fj = fp[j], sj = sl[j];
+        int te = (int)ceil(xp[j + 1]);  // first t of the next segment
+        te = te > L ? L : te;
+#pragma unroll 4
+        for (int u = t + lane; u < te; u += 32) {
+            const double x = (double)u;
+            double r = sj * (x - xj) + fj;
+            r = (xj == x) ? fj : r;
+            f(u, r);
+        }
+        t = te > t ? te : t;
+    }
+    const double fl = fp[n - 1];  // t >= xp[n-1]
+    for (int u = t + lane; u < L; u += 32) f(u, fl);
+}
+
 // np.interp(x, xp, fp) with xp increasing (binary search, exact-hit rule).
 __device__ __forceinline__ double interp1(double x, const double* xp, const double* fp, int n) {
     if (x > xp[n - 1]) return fp[n - 1];
@@ -510,17 +538,15 @@ __device__ __forceinline__ bool op_drift(const DevStage& st, WStream& s, double*
     __syncwarp();
     for (int k = w.lane; k < np_ - 1; k += 32) sl[k] = (anchors[k + 1] - anchors[k]) / (pos[k + 1] - pos[k]);
     __syncwarp();
-    const double inv = ls.step > 0.0 ? 1.0 / ls.step : 0.0;
     const double c0 = interp_slopes(0.0, pos, anchors, sl, np_, 0);
     double* curve = oth;  // pass 1: curve - c0 and its peak
     double peak = 0.0;
-#pragma unroll 4
-    for (int t = w.lane; t < L; t += 32) {
-        const double c = interp_slopes((double)t, pos, anchors, sl, np_, (int)((double)t * inv)) - c0;
+    interp_arange(pos, anchors, sl, np_, L, w.lane, [&](int t, double v) {
+        const double c = v - c0;
         curve[t] = c;
         const double a = fabs(c);
         peak = (a > peak || a != a) ? a : peak;
-    }
+    });
     peak = warp_max(peak);
     if (peak == 0.0) return false;
 #pragma unroll 4
@@ -732,13 +758,11 @@ __device__ __forceinline__ bool op_time_warp(const DevStage& st, WStream& s, dou
     const double* knots = w.small;
     const double* warped = w.small + nk;
     const double* sl = w.small + 2 * nk;
-    const double inv = (double)(nk - 1) / ((double)L - 1.0);
-#pragma unroll 4
-    for (int t = w.lane; t < L; t += 32) {
-        const double v = interp_grid_fast(interp_slopes((double)t, knots, warped, sl, nk, (int)((double)t * inv)), cur, L);
+    interp_arange(knots, warped, sl, nk, L, w.lane, [&](int t, double pos) {
+        const double v = interp_grid_fast(pos, cur, L);
         oth[t] = v;
         bad |= nonfinite(v);
-    }
+    });
     __syncwarp();
     swapbuf(cur, oth);
     return false;
