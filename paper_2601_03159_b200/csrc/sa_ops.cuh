@@ -786,16 +786,16 @@ __device__ __forceinline__ bool op_window_warp(const DevStage& st, WStream& s, d
     const double* warped = w.small + nk;
     const double* sl = w.small + 2 * nk;
     const double* win = cur + start;
-    const double inv = (double)(nk - 1) / ((double)wsz - 1.0);
-#pragma unroll 4
-    for (int t = w.lane; t < L; t += 32) {
-        int u = t - start;
-        const double v = (u >= 0 && u < wsz)
-                             ? interp_grid_fast(interp_slopes((double)u, knots, warped, sl, nk, (int)((double)u * inv)), win, wsz)
-                             : cur[t];
-        oth[t] = v;
+    double* wout = oth + start;
+    interp_arange(knots, warped, sl, nk, wsz, w.lane, [&](int u, double pos) {
+        const double v = interp_grid_fast(pos, win, wsz);
+        wout[u] = v;
         bad |= nonfinite(v);
-    }
+    });
+    // the complement is untouched (warp.py:108-118)
+#pragma unroll 4
+    for (int t = w.lane; t < L; t += 32)
+        if (t < start || t >= start + wsz) oth[t] = cur[t];
     __syncwarp();
     swapbuf(cur, oth);
     return false;
