@@ -376,6 +376,21 @@ def run_suite(args):
         byt = 8 * (x.numel() + pts)
         res[f"config{cfg}"] = {"ms": ms, "gpts_s": pts / ms / 1e6, "hbm_gbs": byt / ms / 1e6,
                                "hbm_frac": byt / ms / 1e6 / measured_peak()[0]}
+        if cfg in (1, 2):  # launch-bound sizes: the same chain replayed from a CUDA graph
+            run = bench_inputs.pipeline(cfg).capture_device(x.contiguous())
+            for _ in range(3):
+                run.replay()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(20):
+                run.replay()
+            b.record()
+            torch.cuda.synchronize()
+            run.check()
+            gms = a.elapsed_time(b) / 20
+            res[f"config{cfg}_graph"] = {"ms": gms, "gpts_s": pts / gms / 1e6, "hbm_gbs": byt / gms / 1e6,
+                                         "hbm_frac": byt / gms / 1e6 / measured_peak()[0]}
         del x
     tot_ms, tot_pts = 0.0, 0
     for i, n, L in bench_inputs.sweep_datasets():

@@ -15,6 +15,7 @@ import os
 import numpy as np
 
 from . import _abi, _native
+from .errors import InvalidInputError
 from .pipeline import lower_stages
 
 
@@ -143,6 +144,63 @@ def launch_device(stages, values, out, flags, seed: int, series_offset: int = 0,
         values.data_ptr(), n, L, out.data_ptr(), out.shape[1], flags.data_ptr(), st,
     )
     _native.check(rc, "sa_pipeline_launch")
+
+
+class GraphedRun:
+    """A fused-chain launch captured in a CUDA graph (launch-bound small
+    batches: one graph launch instead of a host-planned kernel launch per
+    step).  ``values`` is the captured input buffer -- refill it in place
+    between replays; ``out`` receives every replay's result.  ``check()``
+    reads the device flags (one sync) and raises like ``run_device``."""
+
+    def __init__(self, graph, values, out, flags):
+        self.graph, self.values, self.out, self.flags = graph, values, out, flags
+
+    def replay(self):
+        self.graph.replay()
+        return self.out
+
+    def check(self):
+        f = int(self.flags.item())
+        if f & _abi.SA_FLAG_NONFINITE:
+            raise InvalidInputError("batch contains non-finite values (NaN or Inf)")
+        if f & _abi.SA_FLAG_WARP_MONOTONE:
+            raise RuntimeError("warp map failed to stay strictly increasing")
+        return self.out
+
+
+def capture_device(stages, values, seed: int, series_offset: int = 0, len_out: int | None = None,
+                   first_index: int = 0) -> GraphedRun:
+    """Capture one fused-chain launch over the CUDA tensor ``values`` in a
+    CUDA graph.  The first launch runs eagerly (device tables, plan and
+    stream-ordered scratch pool are set up outside the capture) and is
+    checked; the captured graph is the same sa_pipeline_launch."""
+    import torch
+
+    if not (values.is_cuda and values.dtype == torch.float64 and values.dim() == 2 and values.is_contiguous()):
+        raise TypeError("capture_device expects a contiguous 2-D float64 CUDA tensor")
+    dev = values.device
+    n, L = values.shape
+    with torch.cuda.device(dev):
+        _native.ensure_device(dev.index)
+        low = _lower(stages, first_index, True)
+        out = torch.empty((n * _row_factor(stages, True), L if len_out is None else int(len_out)),
+                          dtype=torch.float64, device=dev)
+        flags = torch.zeros(1, dtype=torch.int32, device=dev)
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            launch_device(stages, values, out, flags, seed, series_offset, first_index, side.cuda_stream, low)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        run = GraphedRun(None, values, out, flags)
+        run.check()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            flags.zero_()
+            launch_device(stages, values, out, flags, seed, series_offset, first_index,
+                          torch.cuda.current_stream(dev).cuda_stream, low)
+        run.graph = graph
+    return run
 
 
 def fft_forward_host(values: np.ndarray):
