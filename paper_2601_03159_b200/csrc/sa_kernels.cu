@@ -713,17 +713,69 @@ __global__ void __launch_bounds__(CtaPlan<LGN>::T, SA_CTA_MINB / CtaPlan<LGN>::T
 // (freqaugment.py:37-47, 131-170 + BASELINE M6; the warp chain's op_spectral
 // with spectrum residency).  Warp 0 draws each stage's gate and scalars (one
 // lane per stage, SStream); rows none of whose stages fire are copied.
+// Gates and scalar draws of a spectral-only chain, one thread per (row,
+// stage): the stage's stream (core.py:77-82), its gate (core.py:235), the
+// mask start (freqaugment.py:162-170) or the sinusoid bin / phase increment
+// (BASELINE M6).  A parallel pre-pass, so the CTA kernel's rows never wait
+// on a serial draw section; each row's entries are cp.async-prefetched with
+// the row itself.
+struct SpecDraw {
+    double2 add;  // sinusoid increment
+    int32_t pos;  // mask start / sinusoid bin
+    int32_t fire;
+    int64_t pad;
+};
+__global__ void __launch_bounds__(256) spectral_draw_kernel(const __grid_constant__ ChainParams p,
+                                                            SpecDraw* __restrict__ out) {
+    const int L = (int)p.len_in, bins = L / 2 + 1;
+    const int64_t total = p.rows_out * (int64_t)p.ns;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = i / p.ns;
+        const int j = (int)(i - row * p.ns);
+        const DevStage& st = p.st[j];
+        uint64_t k0, k1;
+        derive_key(p.seed, (uint64_t)st.index, (uint64_t)(p.offset + row), k0, k1);
+        SStream s;
+        s_init(s, k0, k1);
+        SpecDraw d;
+        d.add = make_double2(0.0, 0.0);
+        d.pos = 0;
+        d.pad = 0;
+        const bool f = s_next_double(s) < st.prob && !spectral_noop(st);
+        d.fire = f ? 1 : 0;
+        if (f && st.op == SA_OP_FREQ_MASK) {
+            const int wd = (int)st.i[0];
+            int start = (int)s_bounded(s, (uint32_t)(bins - 1)) - wd / 2;
+            if (start < 0) start = 0;
+            if (start > bins - wd) start = bins - wd;
+            d.pos = start;
+        } else if (f) {  // SA_OP_SINUSOID
+            const int mb = (int)st.i[0];
+            const int b = mb + (int)s_bounded(s, (uint32_t)(bins - mb - 1));
+            const double phi = (2.0 * 3.14159265358979323846) * s_next_double(s);
+            const double A = st.f[0];
+            d.pos = b;
+            if (b == 0 || b == bins - 1) {
+                d.add = make_double2((A * (double)L) * cos(phi), 0.0);
+            } else {
+                const double h = (A * (double)L) * 0.5;
+                d.add = make_double2(h * cos(phi), h * sin(phi));
+            }
+        }
+        out[i] = d;
+    }
+}
+
 template <int LGN>
 __global__ void __launch_bounds__(CtaPlan<LGN>::T, 512 / CtaPlan<LGN>::T) spectral_cta_kernel(const __grid_constant__ ChainParams p,
-                                                           const double2* __restrict__ tw) {
+                                                           const double2* __restrict__ tw,
+                                                           const SpecDraw* __restrict__ draws) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int T = CtaPlan<LGN>::T, N = 1 << LGN;
     const int t = threadIdx.x;
     const int L = 2 * N, bins = N + 1;
     const CtaSmem sm = cta_smem(smem, N);
-    __shared__ uint64_t s_fire;
-    __shared__ int s_pos[64];        // mask start / sinusoid bin of stage j
-    __shared__ double2 s_add[64];    // sinusoid increment of stage j
+    __shared__ __align__(16) SpecDraw s_tab[2][64];  // this / next row's draws, stage j
     __shared__ double2 s_nyq;
     double2 w[8];
     cta_twiddles<LGN>(w, t, tw, LGN + 1);
@@ -736,50 +788,18 @@ __global__ void __launch_bounds__(CtaPlan<LGN>::T, 512 / CtaPlan<LGN>::T) spectr
         for (int m = 0; m < 8; ++m) ws[m] = __ldg(&tw[t + m * T]);
     }
     const double2 wn = __ldg(&tw[N]);
-    auto fetch = [&](int64_t row) {
+    auto fetch = [&](int64_t row, int b) {
         const double2* xr = reinterpret_cast<const double2*>(p.in + row * L);
         for (int i = t; i < N; i += T) cp_async16(&sm.nb[i], xr + i);
+        const char* dr = reinterpret_cast<const char*>(draws + row * p.ns);
+        char* ds = reinterpret_cast<char*>(&s_tab[b][0]);
+        for (int i = t; i < 2 * p.ns; i += T) cp_async16(ds + 16 * i, dr + 16 * i);
         cp_async_commit();
     };
-    if (blockIdx.x < p.rows_out) fetch(blockIdx.x);
+    if (blockIdx.x < p.rows_out) fetch(blockIdx.x, 0);
     bool bad = false;
-    for (int64_t row = blockIdx.x; row < p.rows_out; row += gridDim.x) {
-        if (t < 32) {  // gates and draws, stage j on lane j % 32
-            uint64_t fire = 0;
-            for (int j0 = 0; j0 < p.ns; j0 += 32) {
-                const int j = j0 + t;
-                bool f = false;
-                if (j < p.ns) {
-                    const DevStage& st = p.st[j];
-                    uint64_t k0, k1;
-                    derive_key(p.seed, (uint64_t)st.index, (uint64_t)(p.offset + row), k0, k1);
-                    SStream s;
-                    s_init(s, k0, k1);
-                    f = s_next_double(s) < st.prob && !spectral_noop(st);
-                    if (f && st.op == SA_OP_FREQ_MASK) {
-                        const int wd = (int)st.i[0];
-                        int start = (int)s_bounded(s, (uint32_t)(bins - 1)) - wd / 2;
-                        if (start < 0) start = 0;
-                        if (start > bins - wd) start = bins - wd;
-                        s_pos[j] = start;
-                    } else if (f) {  // SA_OP_SINUSOID
-                        const int mb = (int)st.i[0];
-                        const int b = mb + (int)s_bounded(s, (uint32_t)(bins - mb - 1));
-                        const double phi = (2.0 * 3.14159265358979323846) * s_next_double(s);
-                        const double A = st.f[0];
-                        s_pos[j] = b;
-                        if (b == 0 || b == bins - 1) {
-                            s_add[j] = make_double2((A * (double)L) * cos(phi), 0.0);
-                        } else {
-                            const double h = (A * (double)L) * 0.5;
-                            s_add[j] = make_double2(h * cos(phi), h * sin(phi));
-                        }
-                    }
-                }
-                fire |= (uint64_t)__ballot_sync(SA_FULL, f) << j0;
-            }
-            if (t == 0) s_fire = fire;
-        }
+    int cb = 0;  // s_tab buffer of the current row
+    for (int64_t row = blockIdx.x; row < p.rows_out; row += gridDim.x, cb ^= 1) {
         cp_async_wait_all();
         __syncthreads();
         double2 v[8];
@@ -788,9 +808,10 @@ __global__ void __launch_bounds__(CtaPlan<LGN>::T, 512 / CtaPlan<LGN>::T) spectr
             v[m] = sm.nb[t + m * T];
             bad |= nonfinite(v[m].x) | nonfinite(v[m].y);  // Batch invariant (core.py:104)
         }
-        const uint64_t fire = s_fire;
+        uint64_t fire = 0;
+        for (int j = 0; j < p.ns; ++j) fire |= (uint64_t)(s_tab[cb][j].fire != 0) << j;
         __syncthreads();
-        if (row + gridDim.x < p.rows_out) fetch(row + gridDim.x);
+        if (row + gridDim.x < p.rows_out) fetch(row + gridDim.x, cb ^ 1);
         double2* xo = reinterpret_cast<double2*>(p.out + row * L);
         if (!fire) {
 #pragma unroll
@@ -814,7 +835,7 @@ __global__ void __launch_bounds__(CtaPlan<LGN>::T, 512 / CtaPlan<LGN>::T) spectr
         for (uint64_t f = fire; f; f &= f - 1) {  // stages in chain order
             const int j = __ffsll((long long)f) - 1;
             const DevStage& st = p.st[j];
-            const int pos = s_pos[j];
+            const int pos = s_tab[cb][j].pos;
             if (st.op == SA_OP_FREQ_MASK) {
                 const int end = pos + (int)st.i[0];
 #pragma unroll
@@ -824,7 +845,7 @@ __global__ void __launch_bounds__(CtaPlan<LGN>::T, 512 / CtaPlan<LGN>::T) spectr
                 }
                 if (N >= pos && N < end) nyq = make_double2(0.0, 0.0);
             } else {
-                const double2 a = s_add[j];
+                const double2 a = s_tab[cb][j].add;
                 if (pos == N) {
                     nyq.x = nyq.x + a.x;
                 } else {
@@ -1590,9 +1611,15 @@ int launch_chain(Plan* plan, cudaStream_t stream) {
         int rc = cta_launch_shape(current_device_id(), kern, p.len_in, p.rows_out, &threads, &smem, &grid);
         if (rc) return rc;
         p.order = nullptr;
-        void* args[] = {&p, (void*)&tw};
+        DeviceState& dsc = dev_state(current_device_id());
+        StreamScratch scr(stream);
+        SpecDraw* draws;
+        SA_CUDA(scr.alloc(&draws, sizeof(SpecDraw) * (size_t)(p.rows_out * p.ns)));
+        const int gd = (int)std::min<int64_t>((int64_t)dsc.sms * 8, (p.rows_out * p.ns + 255) / 256);
+        spectral_draw_kernel<<<gd, 256, 0, stream>>>(p, draws);
+        void* args[] = {&p, (void*)&tw, (void*)&draws};
         SA_CUDA(cudaLaunchKernel(kern, dim3(grid), dim3(threads), args, smem, stream));
-        __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
+        __atomic_add_fetch(&g_launches, 2, __ATOMIC_RELAXED);
         return SA_OK;
     }
     DeviceState& ds = dev_state(current_device_id());
