@@ -370,14 +370,24 @@ __device__ __forceinline__ double2* rfft_any(double* xa, double* xb, int L, cons
     }
     const int M = L >> 1;
     double2* X = (Z == za) ? zb : za;
-    for (int k = lane; k <= M; k += 32) {
-        double2 zk = Z[k == M ? 0 : k];
-        double2 zc = Z[k == 0 ? 0 : M - k];
-        double er = 0.5 * (zk.x + zc.x), ei = 0.5 * (zk.y - zc.y);
-        double orr = 0.5 * (zk.y + zc.y), oi = -0.5 * (zk.x - zc.x);
-        double2 w = __ldg(&tw[k]);
-        double2 o = cmul(make_double2(orr, oi), w);
-        X[k] = make_double2(er + o.x, ei + o.y);
+    // four bins per lane step, all loads first: independent latency chains
+    for (int k0 = lane; k0 <= M; k0 += 128) {
+        double2 zk[4], zc[4], wq[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int k = k0 + 32 * q <= M ? k0 + 32 * q : M;
+            zk[q] = Z[k == M ? 0 : k];
+            zc[q] = Z[k == 0 ? 0 : M - k];
+            wq[q] = __ldg(&tw[k]);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int k = k0 + 32 * q;
+            double er = 0.5 * (zk[q].x + zc[q].x), ei = 0.5 * (zk[q].y - zc[q].y);
+            double orr = 0.5 * (zk[q].y + zc[q].y), oi = -0.5 * (zk[q].x - zc[q].x);
+            double2 o = cmul(make_double2(orr, oi), wq[q]);
+            if (k <= M) X[k] = make_double2(er + o.x, ei + o.y);
+        }
     }
     __syncwarp();
     if (lane == 0) {
@@ -410,18 +420,28 @@ __device__ __forceinline__ double* irfft_any(double2* X, double2* other, int L, 
             other[k] = make_double2(v.x, -v.y);
             if (k > 0) other[L - k] = v;
         }
-    } else {  // even L: fold the half spectrum into M complex points
-        for (int k = lane; k < M; k += 32) {
-            double2 xk = X[k];
-            double2 xc = X[M - k];
-            if (k == 0) { xk.y = 0.0; xc.y = 0.0; }
-            xc.y = -xc.y;
-            double er = 0.5 * (xk.x + xc.x), ei = 0.5 * (xk.y + xc.y);
-            double dr = 0.5 * (xk.x - xc.x), di = 0.5 * (xk.y - xc.y);
-            double2 w = __ldg(&tw[k]);
-            w.y = -w.y;
-            double2 o = cmul(make_double2(dr, di), w);
-            other[k] = make_double2(er - o.y, -(ei + o.x));
+    } else {  // even L: fold the half spectrum into M complex points (4 per lane step)
+        for (int k0 = lane; k0 < M; k0 += 128) {
+            double2 xk[4], xc[4], wq[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int k = k0 + 32 * q < M ? k0 + 32 * q : M - 1;
+                xk[q] = X[k];
+                xc[q] = X[M - k];
+                wq[q] = __ldg(&tw[k]);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int k = k0 + 32 * q;
+                if (k == 0) { xk[q].y = 0.0; xc[q].y = 0.0; }
+                xc[q].y = -xc[q].y;
+                double er = 0.5 * (xk[q].x + xc[q].x), ei = 0.5 * (xk[q].y + xc[q].y);
+                double dr = 0.5 * (xk[q].x - xc[q].x), di = 0.5 * (xk[q].y - xc[q].y);
+                double2 w = wq[q];
+                w.y = -w.y;
+                double2 o = cmul(make_double2(dr, di), w);
+                if (k < M) other[k] = make_double2(er - o.y, -(ei + o.x));
+            }
         }
     }
     __syncwarp();
@@ -441,6 +461,7 @@ __device__ __forceinline__ double* irfft_any(double2* X, double2* other, int L, 
     }
     const double s = 1.0 / (double)M;
     bool b = false;
+#pragma unroll 4
     for (int k = lane; k < M; k += 32) {
         double2 z = Z[k];
         const double2 v = make_double2(z.x * s, -(z.y * s));

@@ -9,7 +9,8 @@ OPS = {"jitter": Jitter(0.05), "app": AmplitudePhasePerturb(0.1, 0.1), "spike": 
        "drift": Drift(0.5, 5), "resize": Resize(1500), "fmask": FrequencyMask(51), "time_warp": TimeWarp(5, 0.5),
        "copy": Rotate(probability=0.0), "uniform": InjectNoise(UniformNoise(0.1))}
 name = sys.argv[1]; n = int(sys.argv[2]) if len(sys.argv) > 2 else 20000
-pipe = Pipeline(stages=(OPS[name],), master_seed=1)
+pipe = Pipeline(stages=(Rotate(probability=0.0), OPS[name[:-6]]), master_seed=1) if name.endswith("_chain") \
+    else Pipeline(stages=(OPS[name],), master_seed=1)
 x = device_walks(n, 1024, 5, torch.device("cuda"))
 out = torch.empty((n, pipe.projected_length(1024)), dtype=torch.float64, device="cuda")
 flags = torch.zeros(1, dtype=torch.int32, device="cuda")
