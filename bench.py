@@ -316,6 +316,9 @@ def run_b200(args, rank, world, local_rank):
                      "algorithmic_bytes_per_launch": bytes_launch, "kernel_ms": kern_ms},
         "gpu_launches": int(launches_all),
         "clocks": clk.summary(),
+        "device": {"name": torch.cuda.get_device_name(dev),
+                   "sms": torch.cuda.get_device_properties(dev).multi_processor_count,
+                   "numpy": __import__("numpy").__version__, "torch": torch.__version__},
     }
     # the kernel is issue bound (numpy-exact RNG and FP64 arithmetic per element):
     # warp-instructions per launch (ncu capture of this build) over the live
