@@ -337,11 +337,25 @@ __device__ __forceinline__ double2* bluestein(double2* a, double2* b, const FftG
     return Z;
 }
 
+// N = 512 (L = 1024, the configs' length) as compile-time constants: the
+// same radix-8 x 3 Stockham plan and pass-0 swizzle fft_passes runs for it,
+// with every size, stride, twiddle step and swizzle folded into the code
+// (no runtime pass loop or index arithmetic).  Same arithmetic, same result.
+__device__ __forceinline__ double2* fft_512(double2* a, double2* b, const double2* tw, int lane) {
+    constexpr int N = 512, L = 1024;
+    stockham_pass<8, false>(a, b, N, 0, tw, L >> 3, lane, Swz{0, 0}, Swz{3, 7});
+    stockham_pass<8, false>(b, a, N, 3, tw, L >> 6, lane, Swz{3, 7}, Swz{0, 0});
+    stockham_pass<8, false>(a, b, N, 6, tw, L >> 9, lane, Swz{0, 0}, Swz{0, 0});
+    return b;
+}
+
 // Forward N-point complex FFT per the plan; data in a, b is scratch.
 template <bool BLUE = true, bool R16 = false>
 __device__ __forceinline__ double2* fft_any(double2* a, double2* b, const FftGeo& g, const double2* tw, int L,
                                             int lane) {
     if (BLUE && g.blue) return bluestein(a, b, g, lane);
+    if (L == 1024 && g.N == 512 && g.npass == 3 && g.radix[0] == 8 && g.radix[1] == 8 && g.radix[2] == 8)
+        return fft_512(a, b, tw, lane);
     return fft_passes<R16>(a, b, g.N, g.npass, g.radix, tw, L, lane);
 }
 
