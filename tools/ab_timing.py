@@ -30,6 +30,9 @@ if len(sys.argv) > 1 and sys.argv[1] == "--child":
             import dataclasses
             c5 = bench_inputs.pipeline(5)
             pipe = Pipeline(stages=tuple(dataclasses.replace(st, probability=1.0) for st in c5.stages), master_seed=5)
+        elif name.startswith("REP"):  # REP<k>_<op>: k copies of one op (composition experiments)
+            kk, op = name[3:].split("_", 1)
+            pipe = Pipeline(stages=tuple(OPS[op] for _ in range(int(kk))), master_seed=1)
         elif name.endswith("_chain"):  # the op inside a mixed chain (warp path, not a CTA kernel)
             pipe = Pipeline(stages=(Rotate(probability=0.0), OPS[name[:-6]]), master_seed=1)
         elif name.startswith("CONFIG"):
