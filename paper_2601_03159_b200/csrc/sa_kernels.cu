@@ -102,6 +102,10 @@ __host__ __device__ inline Layout make_layout(int lcap, int ns, int small_words,
     return l;
 }
 
+// Dynamic shared memory shared by the CTA after the warps' slices: numpy's
+// ziggurat fast-path table and the adaptive-lockstep key slots (2 x OR, AND).
+constexpr size_t kCtaShared = 256 * sizeof(ZigEntry) + 4 * sizeof(unsigned long long);
+
 // ------------------------------------------------------------ the kernel
 // GMEM: the row buffers live in p.gbuf (long series); the shared-memory
 // instantiation keeps them provably in shared memory (LDS/STS, not generic
@@ -134,6 +138,16 @@ __global__ void __launch_bounds__(384) chain_kernel(const __grid_constant__ Chai
 
     if (lane == 0) mbar_init(bar, 1);
     __syncwarp();
+    // adaptive lockstep: OR / AND of the rows' gate keys per row iteration
+    // (double-buffered by iteration parity)
+    unsigned long long* s_kor = reinterpret_cast<unsigned long long*>(zs + 256);
+    unsigned long long* s_kand = s_kor + 2;
+    if (threadIdx.x < 2) {
+        s_kor[threadIdx.x] = 0ull;
+        s_kand[threadIdx.x] = ~0ull;
+    }
+    __syncthreads();
+    int it = 0;
     uint32_t phase = 0;
     uint32_t flags = 0;
     const int r = p.repeat_r;
@@ -189,14 +203,32 @@ __global__ void __launch_bounds__(384) chain_kernel(const __grid_constant__ Chai
             if (__any_sync(SA_FULL, bad)) flags |= SA_FLAG_NONFINITE;
         }
         }
-        // 3. the chain (stage-major across the CTA when sync_every > 0)
+        // 3. the chain (stage-major across the CTA when sync_every > 0).  When
+        // every row of the CTA fires the same gated stages (uni_mask bits) the
+        // warps do the same work and stay together without the in-row
+        // barriers; one barrier per row iteration re-aligns them.
+        bool uniform = false;
+        if (p.sync_every) {
+            const int b = it & 1;
+            if (lane == 0 && active) {
+                atomicOr(&s_kor[b], (unsigned long long)(fire_lo & p.uni_mask));
+                atomicAnd(&s_kand[b], (unsigned long long)(fire_lo & p.uni_mask));
+            }
+            if (threadIdx.x == 0) {  // reset the other parity's slots for the next iteration
+                s_kor[b ^ 1] = 0ull;
+                s_kand[b ^ 1] = ~0ull;
+            }
+            __syncthreads();
+            uniform = p.uni_mask != ~0ull && (s_kor[b] & ~s_kand[b]) == 0ull;
+            ++it;
+        }
         bool bad = false;  // per-lane: some stage output was non-finite
         double* cur = A;
         double* oth = B;
         int L = p.len_in;
         double2* held = nullptr;  // the row's half spectrum between fused spectral stages
         for (int j = 0; j < p.ns; ++j) {
-            if ((p.sync_mask >> j) & 1ull) __syncthreads();
+            if (!uniform && j && ((p.sync_mask >> j) & 1ull)) __syncthreads();  // j = 0: the check above
             if (!active || !((fire_lo >> j) & 1ull)) continue;
             const DevStage& st = p.st[j];
             const uint64_t* c = scache + 6 * j;
@@ -1466,15 +1498,15 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
     // SM's four schedulers starve while there are rows for several waves:
     // then the buffers move to global memory (L2 resident), which lets 12
     // warps per SM run (sweep: L = 2369 1.9x, Bluestein 541 / 1707 1.3-2x).
-    const size_t smem_fit = (ds.smem_optin - 256 * sizeof(ZigEntry)) / std::max<size_t>(plan->lay.total, 1);
+    const size_t smem_fit = (ds.smem_optin - kCtaShared) / std::max<size_t>(plan->lay.total, 1);
     const bool starved = smem_fit >= 1 && smem_fit <= 3 && env_int("SA_AUTO_GLOBAL", 1) &&
                          p.rows_out > 3 * (int64_t)ds.sms * (int64_t)smem_fit;
-    if (plan->lay.total + 256 * sizeof(ZigEntry) > ds.smem_optin || starved || env_int("SA_FORCE_GLOBAL", 0)) {
+    if (plan->lay.total + kCtaShared > ds.smem_optin || starved || env_int("SA_FORCE_GLOBAL", 0)) {
         // long series: the two row buffers move to global memory (L2 / HBM
         // resident, same code); shared memory keeps the window and scratch
         plan->global = true;
         plan->lay = make_layout(0, ns, small, iscr);
-        if (plan->lay.total + 256 * sizeof(ZigEntry) > ds.smem_optin)
+        if (plan->lay.total + kCtaShared > ds.smem_optin)
             return fail(SA_ERR_UNSUPPORTED, "stage scratch too large for shared memory");
     }
     // Stage-major CTAs: `warps` series per CTA walk the chain in lockstep
@@ -1482,12 +1514,12 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
     // operator's code at a time (the fused kernel is
     // instruction-fetch bound when warps drift apart).
     const int per_warp = (int)plan->lay.total;
-    int fit = (int)((ds.smem_optin - 256 * sizeof(ZigEntry)) / (size_t)per_warp);
+    int fit = (int)((ds.smem_optin - kCtaShared) / (size_t)per_warp);
     int warps = env_int("SA_CTA_WARPS", 0);
     if (warps <= 0) warps = std::min(12, std::max(1, fit));
     warps = std::max(1, std::min(warps, std::min(12, fit)));
     plan->warps = warps;
-    plan->smem = (size_t)per_warp * warps + 256 * sizeof(ZigEntry);
+    plan->smem = (size_t)per_warp * warps + kCtaShared;
     p.sync_every = ns > 1 ? env_int("SA_SYNC_EVERY", 4) : 0;
     // barrier placement (bit j: barrier before stage j).  Policy 0: every
     // `sync_every` stages; policy 1: before every stage whose operator is
@@ -1526,6 +1558,12 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
         if (env_int("SA_SCHEDULE", 1) == 0 || p.rows_out > INT32_MAX) kb = 0;
         p.key_bits = kb;
         for (int q = 0; q < kb; ++q) p.key_stage[q] = (int8_t)cand[q].second;
+        // adaptive lockstep compares EVERY gated stage: rows that differ only
+        // in cheap stages still drift apart over a row (measured: comparing
+        // only the sorted gates costs 3% at 1e6 rows); ~0: always barrier
+        p.uni_mask = 0;
+        for (size_t q = 0; q < cand.size(); ++q) p.uni_mask |= 1ull << cand[q].second;
+        if (!env_int("SA_ADAPTIVE_SYNC", 1)) p.uni_mask = ~0ull;
     }
     int per_sm = 0;
     {
@@ -1552,7 +1590,7 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
         want = std::min<int64_t>(want, std::max<int64_t>(1, slots / warps));
         if (slots < warps) {
             plan->warps = warps = (int)slots;
-            plan->smem = (size_t)per_warp * warps + 256 * sizeof(ZigEntry);
+            plan->smem = (size_t)per_warp * warps + kCtaShared;
             ctas_needed = (p.rows_out + warps - 1) / warps;
         }
     }

@@ -35,6 +35,7 @@ struct ChainParams {
     int32_t lcap, small_words, iscr_words, bulk_in;
     int32_t sync_every, key_bits;  // sync_every != 0: barriers on; fire-pattern key width
     uint64_t sync_mask;            // bit j: CTA barrier before stage j
+    uint64_t uni_mask;             // gates compared across the CTA's rows; all equal -> no in-row barriers
     const int32_t* order;          // row schedule (nullptr: identity)
     int8_t key_stage[24];          // stages whose gates form the key, most expensive first
     uint64_t seed;
