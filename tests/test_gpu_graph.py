@@ -21,11 +21,12 @@ def _pipe():
                             Pool(4, probability=0.5), Reverse(probability=0.5)), master_seed=11)
 
 
-def test_graph_replay_matches_eager():
+@pytest.mark.parametrize("rows", [700, 6000])  # 6000: the fire-pattern sort kernels are captured too
+def test_graph_replay_matches_eager(rows):
     pipe = _pipe()
-    rng = np.random.default_rng(0)
-    a = torch.from_numpy(np.cumsum(rng.normal(size=(700, 256)), axis=1)).cuda()
-    b = torch.from_numpy(np.cumsum(rng.normal(size=(700, 256)), axis=1)).cuda()
+    rng = np.random.default_rng(rows)
+    a = torch.from_numpy(np.cumsum(rng.normal(size=(rows, 256)), axis=1)).cuda()
+    b = torch.from_numpy(np.cumsum(rng.normal(size=(rows, 256)), axis=1)).cuda()
     want_a = pipe.run_device(a).clone()
     want_b = pipe.run_device(b).clone()
     buf = a.clone()
