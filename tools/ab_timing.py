@@ -21,7 +21,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "--child":
            "window_warp": WindowWarp(128, 4, 0.5), "convolve": Convolve("hann", 7), "pool": Pool(4),
            "scale": Scale(0.1), "rotate": Rotate(), "reverse": Reverse(), "permute": PermuteSegments(4),
            "gauss": InjectNoise(GaussianNoise(0.1)), "slope": InjectNoise(SlopeTrendNoise(0.5))}
-    L = 1024
+    L = int(os.environ.get("AB_L", "1024"))
     x = device_walks(n, L, 5, torch.device("cuda"))
     flags = torch.zeros(1, dtype=torch.int32, device="cuda")
     res = {}
