@@ -1541,6 +1541,7 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
             }
             if (b) p.sync_mask |= 1ull << j;
         }
+        if (const char* m = getenv("SA_SYNC_MASK")) p.sync_mask = strtoull(m, nullptr, 16) | 1ull;  // experiments
     }
     // scheduling key: gated (0 < p < 1) stages, most expensive first
     {
