@@ -1055,22 +1055,23 @@ __device__ __forceinline__ void perturb_spectrum(const DevStage& st, WStream& s,
         double* ph = scratch + bins;  // scratch holds >= 2 * bins doubles
         // `bins` magnitude normals then `bins` phase normals (freqaugment.py:
         // 113-114): consecutive draws of one stream, taken in one walk;
-        // ph = amp + bins, so draw k lands at scratch[k] scaled by its sigma
-        normals(s, w.lane, 2 * bins, w.zig, [&](int k, double z) { amp[k] = 0.0 + (k < bins ? sa : sp) * z; });
+        // ph = amp + bins, so draw k lands at scratch[k]; numpy's scaling
+        // loc + scale * z (0.0 + sigma * z) is applied where the draws are used
+        normals(s, w.lane, 2 * bins, w.zig, [&](int k, double z) { amp[k] = z; });
         __syncwarp();
         // r' = max(|X| + amp, 0) at angle atan2(im, re) + ph (freqaugment.py:
         // 117-122), evaluated as a rotation of X by ph scaled by r'/|X|: the
         // same quantity without atan2 and full-range sin/cos (differs from
         // the reference's formula in rounding only; spectral results are
         // compared to tolerance).  |X| == 0 keeps the reference's form.
-        for (int b = 1 + w.lane; b < hi; b += 32) X[b] = app_bin(X[b], amp[b], ph[b]);
+        for (int b = 1 + w.lane; b < hi; b += 32) X[b] = app_bin(X[b], 0.0 + sa * amp[b], 0.0 + sp * ph[b]);
         __syncwarp();
         if (w.lane == 0) {
             for (int q = 0; q < (even ? 2 : 1); ++q) {
                 int b = q == 0 ? 0 : bins - 1;
                 double re = X[b].x;
                 double sign = re >= 0 ? 1.0 : -1.0;
-                double v = fabs(re) + amp[b];
+                double v = fabs(re) + (0.0 + sa * amp[b]);
                 double mv = (v >= 0.0) ? v : 0.0;
                 X[b] = make_double2(sign * mv, 0.0);
             }
