@@ -126,10 +126,14 @@ struct Swz {
     __device__ __forceinline__ int operator()(int i) const { return i ^ ((i >> sh) & mask); }
 };
 
-template <int R, bool INV>
+// FIN (irfft's last pass): outputs are stored as conj(v) * fin_s and OR-ed
+// into *fin_bad when non-finite (the irfft scaling loop, fused).
+__device__ __forceinline__ bool fin_bad(double v);
+template <int R, bool INV, bool FIN = false>
 __device__ __forceinline__ void stockham_pass(const double2* __restrict__ src, double2* __restrict__ dst,
                                               int M, int lns, const double2* __restrict__ tw, int tstep,
-                                              int lane, Swz sin = {0, 0}, Swz sout = {0, 0}) {
+                                              int lane, Swz sin = {0, 0}, Swz sout = {0, 0}, double fin_s = 1.0,
+                                              bool* fin_bad_out = nullptr) {
     const int Q = M / R;
     const int Ns = 1 << lns;
 #pragma unroll 2
@@ -182,7 +186,15 @@ __device__ __forceinline__ void stockham_pass(const double2* __restrict__ src, d
         // XOR term for the whole butterfly
         const int xo = (base >> sout.sh) & sout.mask;
 #pragma unroll
-        for (int r = 0; r < R; ++r) dst[(base + r * Ns) ^ xo] = v[r];
+        for (int r = 0; r < R; ++r) {
+            if (FIN) {
+                const double2 o = make_double2(v[r].x * fin_s, -(v[r].y * fin_s));
+                *fin_bad_out |= fin_bad(o.x) | fin_bad(o.y);
+                dst[(base + r * Ns) ^ xo] = o;
+            } else {
+                dst[(base + r * Ns) ^ xo] = v[r];
+            }
+        }
     }
     __syncwarp();
 }
@@ -341,21 +353,27 @@ __device__ __forceinline__ double2* bluestein(double2* a, double2* b, const FftG
 // same radix-8 x 3 Stockham plan and pass-0 swizzle fft_passes runs for it,
 // with every size, stride, twiddle step and swizzle folded into the code
 // (no runtime pass loop or index arithmetic).  Same arithmetic, same result.
-__device__ __forceinline__ double2* fft_512(double2* a, double2* b, const double2* tw, int lane) {
+// FIN: irfft's conj / 1/N scaling and finiteness check fused into the last pass.
+template <bool FIN = false>
+__device__ __forceinline__ double2* fft_512(double2* a, double2* b, const double2* tw, int lane, bool* bad = nullptr) {
     constexpr int N = 512, L = 1024;
     stockham_pass<8, false>(a, b, N, 0, tw, L >> 3, lane, Swz{0, 0}, Swz{3, 7});
     stockham_pass<8, false>(b, a, N, 3, tw, L >> 6, lane, Swz{3, 7}, Swz{0, 0});
-    stockham_pass<8, false>(a, b, N, 6, tw, L >> 9, lane, Swz{0, 0}, Swz{0, 0});
+    stockham_pass<8, false, FIN>(a, b, N, 6, tw, L >> 9, lane, Swz{0, 0}, Swz{0, 0}, 1.0 / (double)N, bad);
     return b;
 }
 
 // Forward N-point complex FFT per the plan; data in a, b is scratch.
-template <bool BLUE = true, bool R16 = false>
+__device__ __forceinline__ bool is_fft_512(const FftGeo& g, int L) {
+    return L == 1024 && !g.blue && g.N == 512 && g.npass == 3 && g.radix[0] == 8 && g.radix[1] == 8 && g.radix[2] == 8;
+}
+
+// FIN (irfft of the fft_512 plan only): see fft_512.
+template <bool BLUE = true, bool R16 = false, bool FIN = false>
 __device__ __forceinline__ double2* fft_any(double2* a, double2* b, const FftGeo& g, const double2* tw, int L,
-                                            int lane) {
+                                            int lane, bool* fin_bad_out = nullptr) {
     if (BLUE && g.blue) return bluestein(a, b, g, lane);
-    if (L == 1024 && g.N == 512 && g.npass == 3 && g.radix[0] == 8 && g.radix[1] == 8 && g.radix[2] == 8)
-        return fft_512(a, b, tw, lane);
+    if (is_fft_512(g, L)) return fft_512<FIN>(a, b, tw, lane, fin_bad_out);
     return fft_passes<R16>(a, b, g.N, g.npass, g.radix, tw, L, lane);
 }
 
@@ -459,7 +477,13 @@ __device__ __forceinline__ double* irfft_any(double2* X, double2* other, int L, 
         }
     }
     __syncwarp();
-    double2* Z = fft_any<BLUE, R16>(other, X, g, tw, L, lane);  // one call site: the FFT is emitted once
+    bool fb = false;
+    double2* Z = fft_any<BLUE, R16, true>(other, X, g, tw, L, lane, &fb);  // one call site: the FFT is emitted once
+    if (g.packed && is_fft_512(g, L)) {  // scaled and checked by the last pass
+        if (bad) *bad |= fb;
+        __syncwarp();
+        return reinterpret_cast<double*>(Z);
+    }
     if (!g.packed) {
         double* out = reinterpret_cast<double*>(Z == X ? other : X);
         const double s = 1.0 / (double)L;
