@@ -102,7 +102,7 @@ def pipeline(cfg: int):
                   Dropout(0.05, probability=0.5), Pool(4, probability=0.5), Reverse(probability=0.5))
         seed = 1
     elif cfg == 3:
-        stages = (FrequencyMask(205), RandomSinusoid(1.0))  # 10% of 2,049 bins
+        stages = (FrequencyMask(102), RandomSinusoid(1.0))  # 10% of the 1,025 bins of L = 2,048
         seed = 2
     elif cfg == 4:
         stages = (SpeedWarp(3, 3.0, "cubic"), Resize(1500), Convolve("hann", 7))

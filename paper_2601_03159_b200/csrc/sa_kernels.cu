@@ -1065,6 +1065,36 @@ std::mutex g_host_mu[kMaxDevices];
 
 DeviceState& dev_state(int dev) { return g_dev_state[dev < 0 ? 0 : (dev >= kMaxDevices ? kMaxDevices - 1 : dev)]; }
 
+// Stream-ordered scratch (scheduling buffers, global row buffers, dataset
+// intermediates) comes from a private memory pool per device, so the host
+// application's default pool keeps its own release policy.  Up to 1 GiB stays
+// mapped between calls (the default threshold of 0 unmaps at every
+// synchronisation and the next allocation pays a remap: 20-60 ms host stalls
+// were measured); larger transient buffers are returned at synchronisation.
+cudaMemPool_t g_pool[kMaxDevices];
+std::once_flag g_pool_once[kMaxDevices];
+cudaError_t g_pool_err[kMaxDevices];
+
+cudaError_t sa_malloc_async(void** p, size_t bytes, cudaStream_t st) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const int d = dev < 0 ? 0 : (dev >= kMaxDevices ? kMaxDevices - 1 : dev);
+    std::call_once(g_pool_once[d], [&] {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        g_pool_err[d] = cudaMemPoolCreate(&g_pool[d], &props);
+        if (g_pool_err[d] == cudaSuccess) {
+            uint64_t keep = 1ull << 30;
+            g_pool_err[d] = cudaMemPoolSetAttribute(g_pool[d], cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    });
+    if (g_pool_err[d] != cudaSuccess) return g_pool_err[d];
+    return cudaMallocFromPoolAsync(p, bytes, g_pool[d], st);
+}
+
 int current_device_id() {
     int d = 0;
     cudaGetDevice(&d);
@@ -1101,16 +1131,6 @@ int init_device(int dev) {
     ds.smem_optin = (size_t)optin;
     SA_CUDA(cudaFuncSetAttribute(chain_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(chain_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
-    // The scheduling buffers come from the stream-ordered allocator; keep the
-    // pool's memory mapped between calls (the default release threshold of 0
-    // unmaps it at every synchronisation and the next cudaMallocAsync pays a
-    // remap -- seen as 20-60 ms host stalls inside sa_pipeline_launch).
-    {
-        cudaMemPool_t pool;
-        SA_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
-        uint64_t keep = UINT64_MAX;
-        SA_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-    }
     SA_CUDA(cudaFuncSetAttribute(rfft_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(rfft_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(irfft_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
@@ -1608,7 +1628,7 @@ struct StreamScratch {
     explicit StreamScratch(cudaStream_t s) : st(s) {}
     template <class T>
     cudaError_t alloc(T** p, size_t bytes) {
-        cudaError_t e = cudaMallocAsync((void**)p, bytes, st);
+        cudaError_t e = sa_malloc_async((void**)p, bytes, st);
         if (e == cudaSuccess) ptrs.push_back(*p);
         return e;
     }
@@ -1773,7 +1793,7 @@ int cta_launch_shape(int dev, const void* kern, int64_t L, int64_t n, int* threa
 int alloc_row_bufs(bool global, int lcap, int grid, cudaStream_t st, double** out) {
     *out = nullptr;
     if (!global) return SA_OK;
-    SA_CUDA(cudaMallocAsync(out, sizeof(double) * 2 * (size_t)lcap * (size_t)grid, st));
+    SA_CUDA(sa_malloc_async((void**)out, sizeof(double) * 2 * (size_t)lcap * (size_t)grid, st));
     return SA_OK;
 }
 
@@ -1852,7 +1872,7 @@ int sa_pipeline_run(const sa_stage* stages, int32_t n_stages, const double* aux,
     rc = make_plan(dev, stages, n_stages, aux, n_aux, master_seed, series_offset, n, len_in, len_out, &plan);
     if (rc) return rc;
     uint32_t* dflag = nullptr;
-    SA_CUDA(cudaMallocAsync(&dflag, sizeof(uint32_t), (cudaStream_t)stream));
+    SA_CUDA(sa_malloc_async((void**)&dflag, sizeof(uint32_t), (cudaStream_t)stream));
     rc = launch_plan(&plan, d_in, d_out, dflag, (cudaStream_t)stream);
     if (rc) return rc;
     uint32_t h = 0;
@@ -1904,6 +1924,10 @@ int sa_pipeline_run_host(const sa_stage* stages, int32_t n_stages, const double*
                            return launch_chain(&pl, st);
                        });
     if (rc) return rc;
+    // every slot's flag reset (and kernels) must be complete before the read:
+    // run_rows_host only waits on the slots that received rows, and the slot
+    // streams are non-blocking (not ordered with the legacy stream)
+    for (int k = 0; k < DeviceState::NS; ++k) SA_CUDA(cudaStreamSynchronize(ds.hs[k]));
     uint32_t hflags[DeviceState::NS] = {0, 0, 0};
     SA_CUDA(cudaMemcpy(hflags, ds.dflags, DeviceState::NS * sizeof(uint32_t), cudaMemcpyDeviceToHost));
     uint32_t f = 0;
@@ -2122,7 +2146,7 @@ int sa_dtw_batch(const double* d_a, const double* d_b, int64_t n_pairs, int64_t 
     int per_sm = 0;
     SA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dtw_batch_kernel<false>, 32, smem));
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ds.sms * std::max(per_sm, 1), n_pairs));
-    if (global) SA_CUDA(cudaMallocAsync(&p.gprow, sizeof(double) * (size_t)len_b * grid, (cudaStream_t)stream));
+    if (global) SA_CUDA(sa_malloc_async((void**)&p.gprow, sizeof(double) * (size_t)len_b * grid, (cudaStream_t)stream));
     if (global) dtw_batch_kernel<true><<<grid, 32, smem, (cudaStream_t)stream>>>(p);
     else dtw_batch_kernel<false><<<grid, 32, smem, (cudaStream_t)stream>>>(p);
     SA_CUDA(cudaGetLastError());
@@ -2148,7 +2172,7 @@ int sa_dtw_path(const double* d_a, int64_t len_a, const double* d_b, int64_t len
     p.path = d_path; p.path_len = d_path_len;
     p.stage_b = 0;
     p.pairs = 1; p.n = (int32_t)len_a; p.m = (int32_t)len_b;
-    if (global) SA_CUDA(cudaMallocAsync(&p.gprow, sizeof(double) * (size_t)len_b, (cudaStream_t)stream));
+    if (global) SA_CUDA(sa_malloc_async((void**)&p.gprow, sizeof(double) * (size_t)len_b, (cudaStream_t)stream));
     if (global) dtw_path_kernel<true><<<1, 32, smem, (cudaStream_t)stream>>>(p);
     else dtw_path_kernel<false><<<1, 32, smem, (cudaStream_t)stream>>>(p);
     SA_CUDA(cudaGetLastError());

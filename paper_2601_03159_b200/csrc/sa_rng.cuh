@@ -25,11 +25,15 @@
 // control flow on it is warp-uniform); only emitted values are lane-private.
 // FP expressions are written in the reference's evaluation order and the
 // translation unit is compiled with -fmad=false (no FMA contraction).
-// Known deviation: the ziggurat TAIL (idx 0 and rabs >= ki[0], 2.6e-4 of
-// normals) evaluates log1p; CUDA's log1p and glibc's may differ by 1 ulp, so
-// those samples match the reference to <= 1 ulp rather than bitwise.
+// The ziggurat TAIL (idx 0 and rabs >= ki[0], 2.6e-4 of normals) evaluates
+// log1p: sa_log1p (sa_log1p.h) restates the reference libm's log1p bit for
+// bit, so tail normals are bitwise too.  The wedge test compares against exp();
+// CUDA's exp and glibc's may differ by an ulp, which changes the decision only
+// when the left side equals one of the two candidates exactly (~2^-52 per
+// wedge test).
 #pragma once
 #include <stdint.h>
+#include "sa_log1p.h"
 #include "zig_tables.h"
 
 #define SA_FULL 0xffffffffu
@@ -253,8 +257,8 @@ __device__ __noinline__ void zig_slow_impl(WStream s, int lane, uint64_t r0, Zig
     res->ok = false;
     if (idx == 0) {
         for (;;) {
-            double xx = -kZigInvR * log1p(-next_double(s, lane));
-            double yy = -log1p(-next_double(s, lane));
+            double xx = -kZigInvR * sa_log1p(-next_double(s, lane));
+            double yy = -sa_log1p(-next_double(s, lane));
             if (yy + yy > xx * xx) {
                 res->v = ((rabs >> 8) & 1) ? -(kZigR + xx) : kZigR + xx;
                 res->ok = true;

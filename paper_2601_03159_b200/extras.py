@@ -13,7 +13,8 @@ C oracle (oracle/sa_oracle.c); parity for them is oracle-vs-device only
 Draw order per series (after the gate draw):
   dropout          L doubles u_t; y_t = fill if u_t < rate else x_t
   pool             no draws; block reducer over consecutive `size` samples
-  convolve         no draws; edge-replicated, normalised window taps
+  convolve         no draws; edge-replicated, scipy get_window(fftbins=False)
+                   taps normalised by their sum
   speed_warp       n_speed_change + 1 uniforms in [1, max_speed_ratio]
   random_sinusoid  bin = integers(min_bin, L//2 + 1), then phase = 2*pi*random()
 """
@@ -84,16 +85,13 @@ class Pool(Augmenter):
 
 
 def window_taps(window: str, size: int) -> np.ndarray:
-    """Normalised symmetric window of `size` taps, sampled at the interior
-    points theta_k = 2*pi*(k+1)/(size+1) so no tap is zero."""
-    k = np.arange(size, dtype=np.float64)
-    if window == "flat":
-        w = np.ones(size)
-    elif window == "triang":
-        w = 1.0 - np.abs(2.0 * (k + 1.0) / (size + 1.0) - 1.0)
-    else:
-        c = np.cos(2.0 * np.pi * (k + 1.0) / (size + 1.0))
-        w = 0.5 - 0.5 * c if window == "hann" else 0.54 - 0.46 * c
+    """The smoothing kernel: scipy.signal.get_window(window, size,
+    fftbins=False) -- the symmetric window of filter design ("flat" is
+    scipy's "boxcar") -- normalised by its sum.  Computed on the host once per
+    stage and uploaded with the stage table."""
+    from scipy.signal import get_window
+
+    w = get_window("boxcar" if window == "flat" else window, size, fftbins=False)
     return w / w.sum()
 
 
@@ -115,6 +113,12 @@ class Convolve(Augmenter):
         if not 1 <= self.size <= MAX_CONVOLVE_TAPS:
             raise InvalidParameterError(
                 f"{self.kind}: size must lie in [1, {MAX_CONVOLVE_TAPS}], got {self.size}"
+            )
+        from scipy.signal import get_window
+
+        if not get_window("boxcar" if self.window == "flat" else self.window, self.size, fftbins=False).sum() > 0:
+            raise InvalidParameterError(
+                f"{self.kind}: the {self.window} window of size {self.size} is all zeros"
             )
 
     def taps(self) -> np.ndarray:

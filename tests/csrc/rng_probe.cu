@@ -88,3 +88,23 @@ extern "C" int rngprobe_normals(const uint64_t* h_words, int64_t nwords, const i
     cudaFree(dw); cudaFree(dc); cudaFree(dout); cudaFree(dpos);
     return rc;
 }
+
+// sa_log1p (the restatement of the reference libm's log1p) evaluated on the
+// device, for tests/test_log1p_pin.py.
+__global__ void probe_log1p_kernel(const double* x, double* y, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = sa_log1p(x[i]);
+}
+
+extern "C" int rngprobe_log1p(const double* h_x, double* h_y, int64_t n) {
+    double *dx = nullptr, *dy = nullptr;
+    int rc = -2;
+    if (cudaMalloc(&dx, 8 * (n + 1)) == cudaSuccess && cudaMalloc(&dy, 8 * (n + 1)) == cudaSuccess &&
+        cudaMemcpy(dx, h_x, 8 * n, cudaMemcpyHostToDevice) == cudaSuccess) {
+        probe_log1p_kernel<<<592, 256>>>(dx, dy, n);
+        if (cudaDeviceSynchronize() == cudaSuccess && cudaMemcpy(h_y, dy, 8 * n, cudaMemcpyDeviceToHost) == cudaSuccess)
+            rc = 0;
+    }
+    cudaFree(dx); cudaFree(dy);
+    return rc;
+}

@@ -6,7 +6,9 @@ Run in the build container (where /root/reference exists):
 
 Every case is a seriesaug pipeline config (the reference's own JSON schema,
 pipeline.py:159-201) or a transform call, run through the reference's public
-API on a small seeded input; inputs and outputs are stored so the tests can
+API on a small seeded input (the BASELINE-only kinds -- dropout, pool,
+convolve, speed_warp, random_sinusoid -- as the reference plugins of
+oracle/extras_ref.py); inputs and outputs are stored so the tests can
 replay them against the C oracle (CPU) and the CUDA backend (GPU) without the
 reference present.  numpy / scipy versions are recorded in the JSON.
 """
@@ -42,9 +44,14 @@ def sinusoids(n, L, seed):
 
 
 def main() -> None:
-    sys.path.insert(0, REF)
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
     import scipy
-    import seriesaug as ref
+    from scipy.signal import lfilter
+
+    from oracle.refpkg import import_reference
+
+    ref = import_reference()
+    import oracle.extras_ref  # noqa: F401  (registers the BASELINE-only kinds as reference plugins)
 
     arrays: dict[str, np.ndarray] = {}
     cases: list[dict] = []
@@ -68,6 +75,7 @@ def main() -> None:
         "sin512": inp("sin512", sinusoids(6, 512, seed=0)),
         "w1500": inp("w1500", np.cumsum(rng.normal(0, 1, (2, 1500)), axis=1)
                      + 3 * np.sin(2 * np.pi * np.arange(1500) / 200.0)),
+        "ar2048": inp("ar2048", lfilter([1.0], [1.0, -0.6, 0.2], rng.normal(0, 1, (3, 2048)), axis=1)),
     }
 
     def case(name, stages, inkey, seed=7, mode="standard", exact=True, index=None):
@@ -162,6 +170,51 @@ def main() -> None:
     case("cfg5_full", cfg5[:11] + [st("amplitude_phase_perturb", .5, sigma_amp=0.1, sigma_phase=0.1),
                                     st("frequency_mask", .5, width=51)] + cfg5[11:],
          I["w1024"], seed=5, exact=False)
+    cfg5_all = (cfg5[:11] + [st("amplitude_phase_perturb", .5, sigma_amp=0.1, sigma_phase=0.1),
+                             st("frequency_mask", .5, width=51)] + cfg5[11:]
+                + [st("dropout", .5, rate=0.05), st("pool", .5, size=4), st("convolve", .5, window="hann", size=7),
+                   st("random_sinusoid", .5, amplitude=0.5), st("speed_warp", .5, n_speed_change=3,
+                                                                max_speed_ratio=3.0)])
+    case("cfg5_all20", cfg5_all, I["w1024"], seed=5, exact=False)
+    case("cfg5_all20_per_sample", cfg5_all, I["w128"], seed=6, mode="per-sample", exact=False)
+
+    # --- BASELINE-only operators (M2-M6) as reference plugins (oracle/extras_ref.py),
+    #     run by the reference's own Pipeline
+    case("dropout", [st("dropout", rate=0.05)], I["w1024"])
+    case("dropout_half_fill", [st("dropout", 0.5, rate=0.5, fill=-1.0)], I["w100"], seed=4)
+    case("dropout_zero", [st("dropout", rate=0.0)], I["w15"])
+    case("dropout_all", [st("dropout", rate=1.0, fill=2.5)], I["w7"])
+    case("pool_mean4", [st("pool", size=4)], I["w1024"])
+    case("pool_mean4_partial", [st("pool", 0.5, size=4)], I["w15"], seed=2)
+    case("pool_max5", [st("pool", size=5, reducer="max")], I["w64"])
+    case("pool_min3", [st("pool", size=3, reducer="min")], I["w7"])
+    case("pool_big", [st("pool", size=40)], I["w15"])
+    case("pool_one", [st("pool", size=1)], I["w15"])
+    case("convolve_hann7", [st("convolve", window="hann", size=7)], I["w1024"])
+    case("convolve_flat4", [st("convolve", window="flat", size=4)], I["w64"])
+    case("convolve_triang31", [st("convolve", window="triang", size=31)], I["w100"])
+    case("convolve_hamming6", [st("convolve", 0.5, window="hamming", size=6)], I["w15"], seed=3)
+    case("convolve_wide", [st("convolve", window="hann", size=25)], I["w7"])
+    case("convolve_one", [st("convolve", window="flat", size=1)], I["w15"])
+    case("speed_warp", [st("speed_warp", n_speed_change=3, max_speed_ratio=3.0)], I["w1500"])
+    case("speed_warp_1024", [st("speed_warp", 0.5, n_speed_change=3, max_speed_ratio=3.0)], I["w1024"])
+    case("speed_warp_linear", [st("speed_warp", n_speed_change=7, max_speed_ratio=1.5,
+                                  interpolation="linear")], I["w100"])
+    case("speed_warp_len2", [st("speed_warp", n_speed_change=3, max_speed_ratio=2.0)], I["w2"])
+    case("speed_warp_many", [st("speed_warp", n_speed_change=10, max_speed_ratio=4.0)], I["w7"])
+    case("speed_warp_noop", [st("speed_warp", n_speed_change=0)], I["w15"])
+    case("sinusoid", [st("random_sinusoid", amplitude=1.0)], I["w1024"], exact=False)
+    case("sinusoid_bin0", [st("random_sinusoid", amplitude=0.5, min_bin=0)], I["w64"], exact=False)
+    case("sinusoid_odd", [st("random_sinusoid", amplitude=2.0)], I["w15"], exact=False)
+    case("sinusoid_zero", [st("random_sinusoid", amplitude=0.0)], I["w64"])
+    # --- BASELINE configs 2-5 in full (every stage), through the reference's Pipeline
+    case("cfg2_full", [st("crop", size=819), st("drift", 0.5, max_drift=0.5, n_points=5),
+                       st("quantize", 0.5, n_levels=16), st("dropout", 0.5, rate=0.05),
+                       st("pool", 0.5, size=4), st("reverse", 0.5)], I["w1024"], seed=1)
+    case("cfg3_full", [st("frequency_mask", width=102), st("random_sinusoid", amplitude=1.0)], I["ar2048"],
+         seed=2, exact=False)
+    case("cfg4_full", [st("speed_warp", n_speed_change=3, max_speed_ratio=3.0), st("resize", target_len=1500),
+                       st("convolve", window="hann", size=7)], I["w1500"], seed=3)
 
     # --- transforms (F5)
     for key in ("w1", "w2", "w15", "w64", "w100", "w128", "w1024"):
@@ -224,6 +277,7 @@ def main() -> None:
         "numpy": np.__version__,
         "scipy": scipy.__version__,
         "reference": "seriesaug " + ref.__version__,
+        "plugins": "oracle/extras_ref.py (BASELINE-only kinds as reference Augmenter subclasses)",
         "gate_pin": {"seed": 12345, "sigma": 0.5, "probability": 0.5, "shape": [10000, 8], "fired": fired},
         "cases": cases,
     }

@@ -12,8 +12,8 @@ def spectral_tol(expected: np.ndarray) -> float:
 
 def assert_matches(got: np.ndarray, want: np.ndarray, exact: bool, what: str = ""):
     assert got.shape == want.shape, (what, got.shape, want.shape)
-    if exact:
-        bad = np.flatnonzero(~((got == want) | (np.isnan(got) & np.isnan(want))))
+    if exact:  # bitwise: identical float64 bit patterns, sign of zero included
+        bad = np.flatnonzero(np.ascontiguousarray(got).view(np.uint64) != np.ascontiguousarray(want).view(np.uint64))
         assert bad.size == 0, f"{what}: {bad.size} mismatches, first {bad[:5]}"
     else:
         err = float(np.abs(got - want).max()) if got.size else 0.0

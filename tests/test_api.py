@@ -159,6 +159,11 @@ def test_extras_validation():
         sa.Pipeline(stages=(sa.RandomSinusoid(1.0, min_bin=9),)).projected_length(8)
     taps = sa.Convolve("triang", 7).taps()
     assert np.isclose(taps.sum(), 1.0) and (taps > 0).all() and np.allclose(taps, taps[::-1])
+    # hann: scipy's symmetric window (zero end taps), normalised by its sum
+    hann = sa.Convolve("hann", 7).taps()
+    assert hann[0] == 0.0 == hann[-1] and np.allclose(hann, np.array([0, 1, 3, 4, 3, 1, 0]) / 12.0, rtol=0, atol=1e-15)
+    with pytest.raises(sa.InvalidParameterError):
+        sa.Convolve("hann", 2)
 
 
 def test_custom_augmenter_without_kernel_fails_loudly():
