@@ -170,10 +170,44 @@ def test_custom_augmenter_without_kernel_fails_loudly():
     from dataclasses import dataclass
     from typing import ClassVar
 
+    import numpy as np
+
     @dataclass(frozen=True)
     class Mine(sa.Augmenter):
         probability: float = 1.0
         kind: ClassVar[str] = "mine_test"
 
-    with pytest.raises(sa.InvalidConfigError, match="no B200 kernel"):
-        lower_stages((Mine(),))
+        def _apply(self, series, rng):
+            return series + 1.0
+
+    @dataclass(frozen=True)
+    class MySpectral(sa.SpectralAugmenter):
+        probability: float = 1.0
+        kind: ClassVar[str] = "my_spectral_test"
+
+        def _perturb_row(self, re, im, original_len, rng):
+            return re, im
+
+    @dataclass(frozen=True)
+    class MyJitter(sa.Jitter):  # overriding a built-in's hook drops its kernel
+        def _apply(self, series, rng):
+            return series
+
+    @dataclass(frozen=True)
+    class NoHook(sa.Augmenter):
+        probability: float = 1.0
+        kind: ClassVar[str] = "no_hook_test"
+
+    # the reference refuses to instantiate an operator without _apply (ABC)
+    with pytest.raises(TypeError):
+        NoHook()
+    # kernel-less operators are rejected when the pipeline is built
+    for op in (Mine(), MySpectral(), MyJitter(0.1)):
+        with pytest.raises(sa.InvalidConfigError, match="no B200 kernel"):
+            sa.Pipeline(stages=(sa.Jitter(0.1), op))
+        with pytest.raises(sa.InvalidConfigError, match="no B200 kernel"):
+            lower_stages((op,))
+    # built-ins run on the device only: their Python hook refuses
+    with pytest.raises(sa.InvalidConfigError, match="not available"):
+        sa.Jitter(0.1)._apply(np.zeros(4), None)
+    assert sa.Pipeline(stages=(sa.Jitter(0.1), sa.FrequencyMask(3), sa.Dropout(0.1))).stages
