@@ -2,32 +2,41 @@
 """Benchmark of the fused B200 augmentation pipeline (driver contract).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl b200|reference]
+                    [--workload pipeline|sweep|transforms|dtw|datafiles]
 
 One "step" = one pass of the whole augmentation chain over the batch of the
-chosen BASELINE config (default: config 5, the full pipeline of every
-augmenter at p=0.5 on 1,000,000 x 1,024 float64 series, the configuration the
-metric "pipeline at 1/2/4/8 B200" is quoted on).  The batch is sharded by
-contiguous series ranges across ranks (no data-path collective; torch.distributed
-is used only for the barrier and the max-over-ranks of the timings), so total
-work is fixed as N grows ("strong" scaling).
+chosen BASELINE config (default: config 5, all 20 length-preserving augmenters
+at p=0.5 on 1,000,000 x 1,024 float64 series, the configuration the metric
+"pipeline at 1/2/4/8 B200" is quoted on).  With --gpus N the batch is sharded
+by contiguous series ranges over N ranks, one process per GPU (torchrun's
+RANK / WORLD_SIZE / LOCAL_RANK; without them bench.py launches the N ranks
+itself); there is no data-path collective -- torch.distributed carries only
+the barrier and the max-over-ranks of the timings -- and total work is fixed
+as N grows ("strong" scaling).
 
 value  = output points (all ranks) / max-over-ranks device time, inputs resident
          in HBM, CUDA events on the launching stream.
 e2e    = same metric through the host-buffer C ABI call (sa_pipeline_run_host)
          from pinned host memory: H2D + kernels + D2H inside the timed region.
+e2e_pageable = the drop-in user's call, Pipeline.run(Batch(numpy)) on ordinary
+         (pageable) numpy arrays in and out.
 roofline.achieved = algorithmic bytes 8*(n*L_in + n_out*L_out) per launch /
          mean kernel duration (per GPU); peak = MEASURED_PEAKS.json hbm_gbs.
-cpu_baseline = the C oracle (a restatement of the reference's algorithm) on a
-         bounded sample of the same workload, all host cores, rank 0 at N=1.
---impl reference times that CPU implementation alone (rank 0) on the same
+cpu_baseline = the GENUINE reference (seriesaug from oracle/_ref, the
+         BASELINE-only kinds as its plugins) on a bounded sample of the same
+         workload: a process pool over all host cores running its per-sample
+         loop, rank 0 at N=1; cpu_port = the C oracle (a restatement) likewise.
+--impl reference times that reference CPU path alone (rank 0) on the same
          config and prints the same line with "impl": "reference".
 """
 
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -41,13 +50,16 @@ import numpy as np  # noqa: E402
 
 METRIC = "augmented points/sec"
 UNIT = "points/s"
+LIB_PATH = os.path.join(ROOT, "paper_2601_03159_b200", "_lib", "libseriesaug_b200.so")
 
 WORKLOADS = {
     1: "config1: AddNoise/Jitter(sigma=0.05) on 1,000 x 512 sum-of-sinusoids",
     2: "config2: Crop(819)->Drift->Quantize(16)->Dropout(0.05)->Pool(4)->Reverse (p=0.5) on 10,000 x 1,024 walks",
-    3: "config3: rfft->FrequencyMask(10% bins)->random-phase sinusoid->irfft on 50,000 x 2,048 AR(2)",
+    3: "config3: rfft->FrequencyMask(102 = 10% of 1,025 bins)->random-phase sinusoid->irfft on 50,000 x 2,048 AR(2)",
     4: "config4: SpeedWarp(3, 3.0, cubic)->Resize(1500)->Convolve(hann,7) on 100,000 x 1,500 walk+sine",
     5: "config5: all 20 length-preserving augmenters at p=0.5 on 1,000,000 x 1,024 walks (8.2 GB)",
+    "sweep": ("config5 sweep: the 20-augmenter chain (length-scaled parameters) over 100 synthetic datasets, "
+              "series counts log-uniform in [20, 24,000], lengths log-uniform in [24, 2,900] (random walks)"),
 }
 
 
@@ -121,97 +133,172 @@ def measured_peak():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def _profile_json(name):
+    p = os.path.join(ROOT, "profiles", name)
+    if os.path.exists(p):
+        with open(p) as fh:
+            return json.load(fh)
+    return {}
+
+
 def ncu_traffic(cfg):
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(p):
-        with open(p) as fh:
-            d = json.load(fh)
-        v = d.get(cfg if isinstance(cfg, str) else f"config{cfg}")
-        if v:
-            return v
-    return None
+    return _profile_json("ncu_traffic.json").get(cfg if isinstance(cfg, str) else f"config{cfg}")
 
 
-def ncu_instructions(cfg):
-    p = os.path.join(ROOT, "profiles", "ncu_instructions.json")
-    if os.path.exists(p):
-        with open(p) as fh:
-            return json.load(fh).get(f"config{cfg}")
-    return None
+def build_sha16() -> str | None:
+    """Identity of the library under test (the ncu instruction counts carry
+    the hash of the build they were captured on)."""
+    try:
+        with open(LIB_PATH, "rb") as fh:
+            return hashlib.sha256(fh.read()).hexdigest()[:16]
+    except OSError:
+        return None
 
 
-def cpu_baseline(cfg: int, pipe, L_in: int, target_s: float = 8.0, threads: int | None = None):
-    """The C oracle (reference algorithm restated, oracle/sa_oracle.c) on a
-    bounded sample of the workload, all host threads."""
-    from bench_inputs import host_input
+def config_dict(cfg, N, L, L_out, world, pipe_cfg):
+    """The line's `config`: identical for the device and the reference arm."""
+    return {"workload": WORKLOADS[cfg], "n_series": N, "len_in": L, "len_out": L_out,
+            "stages": [s["kind"] for s in pipe_cfg["stages"]], "master_seed": pipe_cfg["master_seed"],
+            "parallelism": f"series-range shards x{world}, no collective",
+            "l2": "inputs larger than L2 (no flush needed)" if 8 * N * L / world > 256e6 else
+                  "input smaller than L2: repeated steps may hit L2"}
+
+
+def reduce_timings(t, k: int, dev):
+    """Max over ranks of t[:k] (times), sum of t[k:] (counts).  NCCL reduces
+    device tensors only; the gloo test backend reduces host tensors."""
+    import torch
+    import torch.distributed as dist
+
+    where = dev if dist.get_backend() == "nccl" else torch.device("cpu")
+    tm = t[:k].clone().to(where)
+    dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    lt = t[k:].clone().to(where)
+    dist.all_reduce(lt, op=dist.ReduceOp.SUM)
+    return torch.cat([tm, lt]).cpu()
+
+
+# ------------------------------------------------------------------ CPU legs
+def reference_cpu(pipe_cfg: dict, L: int, target_s: float, cores: int | None = None, steps: int = 1,
+                  warmup: int = 1, first: int = 0):
+    """The genuine reference on all host cores (oracle/ref_runner.py: one
+    process per core, each running the reference's per-sample loop over its
+    own contiguous block of series), sized so one pass takes ~target_s.
+    Returns (points per pass, seconds per pass, cores, rows per core)."""
+    from oracle import ref_runner as R
+
+    pool = R.ProcessPool(cores)
+    try:
+        rows = 4
+        pool.assign(R.config_tasks(pipe_cfg, L, rows, pool.cores, first=first))
+        pool.run()  # first-call costs (lazy imports inside numpy / scipy)
+        pts, dt = pool.run()
+        rows = int(min(max(rows, rows * target_s / max(dt, 1e-6)), 200_000))
+        pool.assign(R.config_tasks(pipe_cfg, L, rows, pool.cores, first=first))
+        for _ in range(warmup):
+            pool.run()
+        runs = [pool.run() for _ in range(steps)]
+    finally:
+        pool.close()
+    pts = runs[-1][0]
+    return pts, sum(dt for _, dt in runs) / len(runs), pool.cores, rows
+
+
+def reference_baseline(pipe_cfg: dict, L: int, label: str, target_s: float = 8.0) -> dict:
+    pts, dt, cores, rows = reference_cpu(pipe_cfg, L, target_s)
+    return {"value": pts / dt, "unit": UNIT, "cores": cores, "kind": "reference",
+            "sample": f"{cores} x {rows} series of {label} through the unmodified reference "
+                      f"(seriesaug, per-sample loop, one process per core): {pts} output points in {dt:.2f} s"}
+
+
+def port_baseline(pipe_cfg: dict, L: int, label: str, target_s: float = 5.0):
+    """The C oracle (oracle/sa_oracle.c, a restatement of the reference's
+    algorithm) on all host threads, same workload: the strongest CPU
+    implementation of the path at hand."""
     from oracle import oracle as O
+    from oracle import ref_runner as R
 
-    threads = threads or os.cpu_count() or 1
-    probe = host_input(cfg, n=max(64, 8 * threads))
+    threads = os.cpu_count() or 1
+    probe = R.walks(max(64, 8 * threads), L, 1)
     t0 = time.perf_counter()
-    O.run_pipeline(pipe, probe, threads=threads)
+    O.run_config(pipe_cfg, probe, threads=threads)
     per_row = (time.perf_counter() - t0) / probe.shape[0]
     n = int(min(max(256, target_s / max(per_row, 1e-9)), 200_000))
-    x = host_input(cfg, n=n)
+    x = R.walks(n, L, 2)
     t0 = time.perf_counter()
-    out = O.run_pipeline(pipe, x, threads=threads)
+    out = O.run_config(pipe_cfg, x, threads=threads)
     dt = time.perf_counter() - t0
     return {"value": out.size / dt, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"first {n} series of {WORKLOADS[cfg].split(':')[0]} ({out.size} output points, {dt:.2f} s)"}
+            "sample": f"{n} series of {label} through the C oracle ({out.size} output points, {dt:.2f} s)"}
 
 
 def run_reference(args, rank, world):
-    from bench_inputs import CONFIG_SHAPES, host_input, pipeline
-    from oracle import oracle as O
+    """--impl reference: the unmodified reference's CPU pipeline on this box's
+    host cores, on the same workload, config and metric as the device arm."""
+    import bench_inputs as B
 
     if rank != 0:
         return
+    if args.workload == "sweep":
+        return run_sweep_reference(args)
     cfg = args.config
-    pipe = pipeline(cfg)
-    N, L = CONFIG_SHAPES[cfg]
-    threads = os.cpu_count() or 1
-    probe = host_input(cfg, n=max(64, 8 * threads))
-    t0 = time.perf_counter()
-    O.run_pipeline(pipe, probe, threads=threads)
-    per_row = (time.perf_counter() - t0) / probe.shape[0]
-    n = int(min(N, max(256, 4.0 / max(per_row, 1e-9))))
-    x = host_input(cfg, n=n)
-    for _ in range(args.warmup):
-        O.run_pipeline(pipe, x, threads=threads)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        out = O.run_pipeline(pipe, x, threads=threads)
-    dt = (time.perf_counter() - t0) / args.steps
-    v = out.size / dt
+    N, L = B.CONFIG_SHAPES[cfg]
+    if args.n_series:
+        N = args.n_series
+    pipe_cfg = B.pipeline_config(cfg)
+    L_out = L
+    for s in pipe_cfg["stages"]:
+        if s["kind"] == "crop" and s["probability"] == 1.0:
+            L_out = s["params"]["size"]
+    label = WORKLOADS[cfg].split(":")[0]
+    pts, dt, cores, rows = reference_cpu(pipe_cfg, L, args.ref_step_s, steps=args.steps,
+                                         warmup=max(1, min(args.warmup, 2)))
+    v = pts / dt
+    # the reference's other two modes, once each (SURVEY.md §8(d)): its own
+    # Pipeline.run serially and with parallel=True (its GIL-bound thread pool)
+    from oracle import ref_runner as R
+
+    modes = {"processes": {"value": v, "cores": cores}}
+    for name, par in (("serial", False), ("threads", True)):
+        n = max(8, int(v / cores * (2.0 if par else 1.0) / L))
+        p2, d2 = R.time_pipeline(pipe_cfg, n, L, par)
+        modes[name] = {"value": p2 / d2, "cores": 1 if not par else (os.cpu_count() or 1), "series": n}
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded; BASELINE config shapes)",
-        "config": {"workload": WORKLOADS[cfg], "sample_series": n, "len": L},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"first {n} of {N} series per step"},
+        "data": "synthetic (seeded random walks; BASELINE config shapes)",
+        "config": config_dict(cfg, N, L, L_out, world, pipe_cfg),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"per step: {cores} processes x {rows} series of {label} ({pts} output "
+                                   f"points) through the unmodified reference, per-sample loop"},
+        "reference_modes": modes,
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def run_b200(args, rank, world, local_rank):
+# ------------------------------------------------------------------ device arm
+def run_b200(args, rank, world, local_rank, dist_ok):
+    import ctypes
+
     import torch
     import torch.distributed as dist
 
-    from bench_inputs import CONFIG_SHAPES, device_walks, host_input, pipeline
-    from paper_2601_03159_b200 import _engine, _native
+    from bench_inputs import CONFIG_SHAPES, device_walks, host_input, pipeline_config
+    from paper_2601_03159_b200 import Batch, Pipeline, _engine, _native
     from paper_2601_03159_b200.sharding import shard_range
 
     cfg = args.config
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
-    _native.ensure_device(local_rank)
+    dev_index = env_int("SA_BENCH_DEVICE", local_rank)
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
+    _native.ensure_device(dev_index)
     N, L = CONFIG_SHAPES[cfg]
     if args.n_series:
         N = args.n_series
-    pipe = pipeline(cfg)
+    pipe_cfg = pipeline_config(cfg)
+    pipe = Pipeline.parse(pipe_cfg)
     L_out = pipe.projected_length(L)
     r0, r1 = shard_range(N, rank, world)
     n = r1 - r0
@@ -243,7 +330,7 @@ def run_b200(args, rank, world, local_rank):
     launches0 = _native.launch_count()
     barrier()
     torch.cuda.synchronize()
-    with Clocks(local_rank) as clk:
+    with Clocks(dev_index) as clk:
         with torch.cuda.stream(stream):
             for k in range(args.steps):
                 ev[2 * k].record(stream)
@@ -256,16 +343,18 @@ def run_b200(args, rank, world, local_rank):
     total_ms = ev[0].elapsed_time(ev[-1])
     if int(flags.item()):
         raise RuntimeError(f"kernel flagged {int(flags.item())}")
+    if args.check_out:
+        os.makedirs(args.check_out, exist_ok=True)
+        np.save(os.path.join(args.check_out, f"rank{rank}_of{world}.npy"), out.cpu().numpy())
 
     # e2e: host-buffer C ABI from pinned memory (H2D + kernel + D2H timed)
-    e2e_s = None
+    e2e_s = e2e_pg_s = None
     h2d = 8 * n * L
     d2h = 8 * rows_out * L_out
     if not args.no_e2e:
         hin = x.cpu().pin_memory()
         hout = torch.empty((rows_out, L_out), dtype=torch.float64).pin_memory()
         arr, aux = lowered
-        import ctypes
 
         def e2e_step():
             rc = _native.lib().sa_pipeline_run_host(
@@ -281,18 +370,35 @@ def run_b200(args, rank, world, local_rank):
             e2e_step()
         e2e_s = (time.perf_counter() - t0) / args.steps
         barrier()
-        # the e2e result must equal the device result
         if not torch.equal(hout[: min(64, rows_out)].to(dev), out[: min(64, rows_out)]):
             raise RuntimeError("e2e output differs from the device-resident output")
+        del hin, hout
+        # the drop-in user's call: Pipeline.run(Batch(numpy)) on pageable arrays
+        # (rank shards: the same call on the rank's rows with its global offset)
+        hx = x.cpu().numpy()
+        k_pg = max(1, min(args.steps, 3))
 
-    t = torch.tensor([total_ms / args.steps, sum(step_ms) / len(step_ms), e2e_s or 0.0, float(launches)],
-                     dtype=torch.float64, device=dev)
+        def pageable_step():
+            if world == 1:
+                return pipe.run(Batch(hx)).values
+            return _engine.run_host(pipe.stages, hx, pipe.master_seed, series_offset=r0, len_out=L_out)
+
+        res = pageable_step()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(k_pg):
+            res = pageable_step()
+        e2e_pg_s = (time.perf_counter() - t0) / k_pg
+        barrier()
+        if not torch.equal(torch.from_numpy(res[: min(64, rows_out)]).to(dev), out[: min(64, rows_out)]):
+            raise RuntimeError("pageable e2e output differs from the device-resident output")
+        del res, hx
+
+    t = torch.tensor([total_ms / args.steps, sum(step_ms) / len(step_ms), e2e_s or 0.0, e2e_pg_s or 0.0,
+                      float(launches)], dtype=torch.float64)
     if world > 1:
-        dist.all_reduce(t[:3], op=dist.ReduceOp.MAX)
-        lt = t[3:].clone()
-        dist.all_reduce(lt, op=dist.ReduceOp.SUM)
-        t[3] = lt[0]
-    ms_per_step, kern_ms, e2e_max, launches_all = [float(v) for v in t.tolist()]
+        t = reduce_timings(t, 4, dev)
+    ms_per_step, kern_ms, e2e_max, e2e_pg_max, launches_all = [float(v) for v in t.tolist()]
     if rank != 0:
         return
     pts = N * pipe.row_factor() * L_out
@@ -300,44 +406,203 @@ def run_b200(args, rank, world, local_rank):
     peak, peak_src = measured_peak()
     bytes_launch = 8 * (n * L + rows_out * L_out)
     achieved = bytes_launch / (kern_ms / 1e3) / 1e9
+    props = torch.cuda.get_device_properties(dev)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded random walks / BASELINE config distributions; no corpus available)",
-        "config": {"workload": WORKLOADS[cfg], "n_series": N, "len_in": L, "len_out": L_out,
-                   "stages": [s.kind for s in pipe.stages], "master_seed": pipe.master_seed,
-                   "parallelism": f"series-range shards x{world}, no collective",
-                   "l2": "inputs larger than L2 (no flush needed)" if 8 * n * L > 256e6 else
-                         "input smaller than L2: repeated steps may hit L2"},
+        "config": config_dict(cfg, N, L, L_out, world, pipe_cfg),
         "hbm_gbs": achieved,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": ncu_traffic(cfg), "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": bytes_launch, "kernel_ms": kern_ms},
         "gpu_launches": int(launches_all),
         "clocks": clk.summary(),
-        "device": {"name": torch.cuda.get_device_name(dev),
-                   "sms": torch.cuda.get_device_properties(dev).multi_processor_count,
-                   "numpy": __import__("numpy").__version__, "torch": torch.__version__},
+        "device": {"name": torch.cuda.get_device_name(dev), "sms": props.multi_processor_count,
+                   "numpy": np.__version__, "torch": torch.__version__, "build_sha16": build_sha16()},
     }
     # the kernel is issue bound (numpy-exact RNG and FP64 arithmetic per element):
-    # warp-instructions per launch (ncu capture of this build) over the live
-    # kernel time, against 4 issue slots x SMs x the sampled SM clock
-    instr = ncu_instructions(cfg)
-    if instr and cfg == 5 and N == CONFIG_SHAPES[5][0]:
+    # warp-instructions per launch (ncu capture; valid only for the build it
+    # was captured on) over the live kernel time, against 4 issue slots x SMs
+    # x the sampled SM clock
+    ins = _profile_json("ncu_instructions.json").get(f"config{cfg}")
+    if isinstance(ins, dict) and N == CONFIG_SHAPES[cfg][0]:
         sm_mhz = line["clocks"].get("sm_mhz") or 1965.0
-        sms = torch.cuda.get_device_properties(dev).multi_processor_count
-        peak_issue = 4.0 * sms * sm_mhz * 1e6
-        ach_issue = instr / world / (kern_ms / 1e3)
+        peak_issue = 4.0 * props.multi_processor_count * sm_mhz * 1e6
+        ach_issue = ins["instructions"] / world / (kern_ms / 1e3)
         line["issue_roofline"] = {"achieved": ach_issue, "peak": peak_issue, "unit": "warp-instructions/s",
                                   "frac": ach_issue / peak_issue,
-                                  "instructions_per_launch": instr / world,
+                                  "instructions_per_launch": ins["instructions"] / world,
+                                  "captured_build_sha16": ins.get("build_sha16"),
+                                  "stale": ins.get("build_sha16") != build_sha16(),
                                   "source": "profiles/ncu_instructions.json (ncu smsp__inst_executed.sum)"}
     if e2e_s is not None:
         line["e2e"] = {"value": pts / e2e_max, "unit": UNIT, "h2d_bytes_per_step": h2d * world,
-                       "d2h_bytes_per_step": d2h * world}
+                       "d2h_bytes_per_step": d2h * world,
+                       "path": "sa_pipeline_run_host (C ABI) from page-locked host buffers"}
+        line["e2e_pageable"] = {"value": pts / e2e_pg_max, "unit": UNIT, "h2d_bytes_per_step": h2d * world,
+                                "d2h_bytes_per_step": d2h * world, "steps": max(1, min(args.steps, 3)),
+                                "path": "Pipeline.run(Batch(numpy)) on pageable numpy arrays (the drop-in call)"}
     if world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline(cfg, pipe, L)
+        label = WORKLOADS[cfg].split(":")[0]
+        line["cpu_baseline"] = reference_baseline(pipe_cfg, L, label)
+        line["cpu_port"] = port_baseline(pipe_cfg, L, label)
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ sweep
+def run_sweep(args, rank, world, local_rank, dist_ok):
+    """BASELINE config 5's sweep: one step = the 20-augmenter chain over all
+    100 datasets (one fused launch each), datasets dealt to ranks round-robin
+    by size; inputs resident in HBM.  e2e = Pipeline.run(Batch(numpy)) per
+    dataset (host numpy in and out, the drop-in call)."""
+    import torch
+    import torch.distributed as dist
+
+    import bench_inputs as B
+    from paper_2601_03159_b200 import Batch, _engine, _native
+
+    dev_index = env_int("SA_BENCH_DEVICE", local_rank)
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
+    _native.ensure_device(dev_index)
+    ds = sorted(B.sweep_datasets(), key=lambda d: -d[1] * d[2])
+    mine = ds[rank::world]
+    work = []
+    for i, n, L in mine:
+        pipe = B.sweep_pipeline(L, i)
+        hx = B.synthetic_walks(n, L, i)
+        x = torch.from_numpy(hx).to(dev)
+        out = torch.empty((n, L), dtype=torch.float64, device=dev)
+        work.append((pipe, hx, x, out, _engine._lower(pipe.stages, 0, True)))
+    flags = torch.zeros(1, dtype=torch.int32, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+
+    def step():
+        for pipe, hx, x, out, low in work:
+            _engine.launch_device(pipe.stages, x, out, flags, pipe.master_seed, stream=stream.cuda_stream,
+                                  lowered=low)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+    torch.cuda.synchronize()
+    assert int(flags.item()) == 0
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    launches0 = _native.launch_count()
+    if world > 1:
+        dist.barrier()
+    with Clocks(dev_index) as clk:
+        with torch.cuda.stream(stream):
+            ev[0].record(stream)
+            for k in range(args.steps):
+                step()
+                ev[k + 1].record(stream)
+        torch.cuda.synchronize()
+    launches = _native.launch_count() - launches0
+    ms = ev[0].elapsed_time(ev[-1]) / args.steps
+    # e2e through the public call on host numpy arrays
+    for pipe, hx, x, out, low in work[:3]:
+        pipe.run(Batch(hx))
+    t0 = time.perf_counter()
+    k_e2e = max(1, min(args.steps, 3))
+    for _ in range(k_e2e):
+        for pipe, hx, x, out, low in work:
+            res = pipe.run(Batch(hx)).values
+    e2e_s = (time.perf_counter() - t0) / k_e2e
+    pipe, hx, x, out, low = work[-1]
+    if not np.array_equal(res.view(np.uint64), out.cpu().numpy().view(np.uint64)):
+        raise RuntimeError("sweep e2e output differs from the device-resident output")
+    t = torch.tensor([ms, e2e_s, float(launches)], dtype=torch.float64)
+    if world > 1:
+        t = reduce_timings(t, 2, dev)
+    ms, e2e_s, launches = [float(v) for v in t.tolist()]
+    if rank != 0:
+        return
+    pts = sum(n * L for _, n, L in ds)
+    peak, src = measured_peak()
+    line = {
+        "metric": METRIC, "value": pts / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded random walks, seed = dataset id)",
+        "config": sweep_config_dict(ds, world),
+        "roofline": {"bound": "hbm", "achieved": 16 * pts / world / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                     "frac": 16 * pts / world / (ms / 1e3) / 1e9 / peak, "traffic": None, "peak_source": src,
+                     "note": "100 launches of 0.06-4 ms: mostly latency / tail bound, not HBM"},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "e2e": {"value": pts / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * pts, "d2h_bytes_per_step": 8 * pts,
+                "path": "Pipeline.run(Batch(numpy)) per dataset, pageable numpy arrays"},
+        "device": {"name": torch.cuda.get_device_name(dev), "build_sha16": build_sha16()},
+    }
+    if world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = sweep_reference_baseline(ds, target_s=10.0)
+    print(json.dumps(line), flush=True)
+
+
+def sweep_config_dict(ds, world):
+    return {"workload": WORKLOADS["sweep"], "datasets": len(ds), "points": sum(n * L for _, n, L in ds),
+            "n_range": [min(d[1] for d in ds), max(d[1] for d in ds)],
+            "len_range": [min(d[2] for d in ds), max(d[2] for d in ds)],
+            "parallelism": f"datasets dealt to {world} rank(s), no collective",
+            "l2": "datasets of 4 KB - 0.5 GB; consecutive launches touch different data"}
+
+
+def sweep_reference_baseline(ds, target_s: float) -> dict:
+    """The genuine reference on every dataset of the sweep, a bounded sample
+    of series per dataset (same fraction everywhere), all host cores: a pool
+    task per (dataset, block of series)."""
+    import bench_inputs as B
+    from oracle import ref_runner as R
+
+    cores = os.cpu_count() or 1
+    pool = R.ProcessPool(cores)
+    try:
+        def tasks_for(frac):
+            """Worker w gets slice w of every dataset's sampled series (the
+            same number of series of each dataset per worker: balanced)."""
+            per = [[] for _ in range(cores)]
+            pts = 0
+            for i, n, L in ds:
+                rows = max(1, int(round(n * frac / cores)))
+                cfgj = json.dumps(B.sweep_config(L, i), sort_keys=True)
+                for w in range(cores):
+                    per[w].append((cfgj, L, w * rows, rows, i * 1_000_003 + w))
+                pts += cores * rows * L
+            return per, pts
+
+        def run(frac):
+            tasks, pts = tasks_for(frac)
+            pool.assign(tasks)
+            pool.run()
+            return pts, pool.run()[1]
+
+        total = sum(n * L for _, n, L in ds)
+        p, dt = run(0.001)
+        frac = min(1.0, target_s * (p / dt) / total)
+        p, dt = run(frac)
+    finally:
+        pool.close()
+    return {"value": p / dt, "unit": UNIT, "cores": cores, "kind": "reference",
+            "sample": f"{frac:.4f} of the series of every dataset (at least one per process) through the "
+                      f"unmodified reference (per-sample loop, each of {cores} processes a slice of every "
+                      f"dataset): {p} output points in {dt:.2f} s"}
+
+
+def run_sweep_reference(args):
+    import bench_inputs as B
+
+    ds = sorted(B.sweep_datasets(), key=lambda d: -d[1] * d[2])
+    base = sweep_reference_baseline(ds, target_s=args.ref_step_s * 4)
+    v = base["value"]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": env_int("WORLD_SIZE", 1),
+        "steps": 1, "warmup": 1, "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded random walks, seed = dataset id)",
+        "config": sweep_config_dict(ds, env_int("WORLD_SIZE", 1)), "cpu_baseline": base,
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
     print(json.dumps(line), flush=True)
 
 
@@ -403,6 +668,8 @@ def run_suite(args):
         tot_pts += pts
     res["sweep100"] = {"ms": tot_ms, "gpts_s": tot_pts / tot_ms / 1e6, "datasets": 100, "points": tot_pts}
     print(json.dumps(res), flush=True)
+
+
 
 
 DS_SHAPE = (100_000, 1024)
@@ -806,6 +1073,26 @@ def dtw_cpu(a, b, pairs=None):
             "sample": f"{pairs} pairs through the C oracle ({dt:.2f} s)"}
 
 
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn_ranks(n: int) -> int:
+    """No torchrun environment but --gpus N > 1: launch the N ranks here, one
+    process per GPU, with the variables torchrun would set."""
+    port = _free_port()
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n), LOCAL_WORLD_SIZE=str(n),
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:], env=env))
+    return max(abs(p.wait()) for p in procs)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -817,10 +1104,22 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--suite", action="store_true", help="configs 1-5 + sweep, device-resident, one JSON")
-    ap.add_argument("--workload", default="pipeline", choices=["pipeline", "datafiles", "transforms", "dtw"],
-                    help="datafiles / transforms / dtw: the SURVEY.md §8(f) next rows")
+    ap.add_argument("--workload", default="pipeline",
+                    choices=["pipeline", "sweep", "datafiles", "transforms", "dtw"],
+                    help="sweep: BASELINE config 5's 100-dataset sweep; datafiles / transforms / dtw: the "
+                         "SURVEY.md §8(f) next rows")
+    ap.add_argument("--check-out", default="", help="directory: each rank saves its output shard (tests)")
+    ap.add_argument("--ref-step-s", type=float, default=3.0,
+                    help="reference arm: seconds of host-core work per timed step")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        if args.impl == "reference":  # rank 0 alone runs the CPU reference
+            os.environ["WORLD_SIZE"] = str(args.gpus)
+        else:
+            sys.exit(spawn_ranks(args.gpus))
     rank, world, local_rank = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if args.workload in ("transforms", "dtw"):
         if args.impl == "reference":
             run_side_reference(args, rank)
@@ -845,10 +1144,18 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        backend = os.environ.get("SA_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dev = torch.device("cuda", env_int("SA_BENCH_DEVICE", local_rank))
+            torch.cuda.set_device(dev)
+            dist.init_process_group("nccl", device_id=dev)
+        else:  # tests: several ranks sharing one GPU synchronise over gloo
+            dist.init_process_group(backend)
     try:
-        run_b200(args, rank, world, local_rank)
+        if args.workload == "sweep":
+            run_sweep(args, rank, world, local_rank, True)
+        else:
+            run_b200(args, rank, world, local_rank, True)
     finally:
         if world > 1:
             import torch.distributed as dist

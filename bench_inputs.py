@@ -34,13 +34,28 @@ def config1_input(n: int = 1000, L: int = 512, seed: int = 0) -> np.ndarray:
     return x + rng.normal(0, 0.1, (n, L))
 
 
+_M64 = (1 << 64) - 1
+
+
+def _mix64(z: int) -> int:
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+def stream(seed: int, j: int = 0, i: int = 0) -> np.random.Generator:
+    """The reference's derive_stream(SeedContext(seed, j, i)) (core.py:40-82),
+    computed here in plain Python so input generation never loads the
+    product library."""
+    g = 0x9E3779B97F4A7C15
+    st = _mix64(_mix64(_mix64(seed) + g + j & _M64) + g + i & _M64)
+    return np.random.Generator(np.random.Philox(key=_mix64(st) | (_mix64(st + g & _M64) << 64)))
+
+
 def synthetic_walks(n: int, L: int, seed: int) -> np.ndarray:
     """The reference's synthetic_batch(n, L, seed): cumsum of the normals of
     stream SeedContext(seed) (reference bench.py:217-221)."""
-    from paper_2601_03159_b200.core import SeedContext, derive_stream
-
-    rng = derive_stream(SeedContext(seed))
-    return np.cumsum(rng.normal(0.0, 1.0, (n, L)), axis=1)
+    return np.cumsum(stream(seed).normal(0.0, 1.0, (n, L)), axis=1)
 
 
 def ar2_input(n: int = 50_000, L: int = 2048, seed: int = 2, phi=(0.6, -0.2)) -> np.ndarray:
@@ -86,40 +101,62 @@ def host_input(cfg: int, n: int | None = None) -> np.ndarray:
     return synthetic_walks(n, L, 5)
 
 
-def pipeline(cfg: int):
-    """The pipeline each BASELINE config names, in the reference's plugin
-    API (SURVEY.md §8(d) mapping; geometry ops at p=1 per core.py:207-211)."""
-    from paper_2601_03159_b200 import (AmplitudePhasePerturb, Convolve, Crop, Drift, Dropout, FrequencyMask,
-                                       GaussianNoise, InjectNoise, Jitter, PermuteSegments, Pipeline, Pool,
-                                       Quantize, RandomSinusoid, Resize, Reverse, Rotate, Scale, SlopeTrendNoise,
-                                       SpeedWarp, SpikeNoise, TimeWarp, UniformNoise, WindowWarp)
+def _st(kind, p=1.0, **params):
+    return {"kind": kind, "probability": p, "params": params}
 
+
+def pipeline_config(cfg: int) -> dict:
+    """The pipeline each BASELINE config names, as the reference's JSON config
+    (pipeline.py:159-201; SURVEY.md §8(d) mapping; geometry ops at p=1 per
+    core.py:207-211).  Both arms build from it: the product's Pipeline.parse
+    and the reference's (with the BASELINE-only kinds as plugins)."""
     if cfg == 1:
-        stages = (Jitter(sigma=0.05),)
-        seed = 0
+        stages, seed = [_st("jitter", sigma=0.05)], 0
     elif cfg == 2:
-        stages = (Crop(819), Drift(0.5, 5, probability=0.5), Quantize(16, probability=0.5),
-                  Dropout(0.05, probability=0.5), Pool(4, probability=0.5), Reverse(probability=0.5))
+        stages = [_st("crop", size=819), _st("drift", 0.5, max_drift=0.5, n_points=5),
+                  _st("quantize", 0.5, n_levels=16), _st("dropout", 0.5, rate=0.05), _st("pool", 0.5, size=4),
+                  _st("reverse", 0.5)]
         seed = 1
-    elif cfg == 3:
-        stages = (FrequencyMask(102), RandomSinusoid(1.0))  # 10% of the 1,025 bins of L = 2,048
-        seed = 2
+    elif cfg == 3:  # mask 10% of the 1,025 bins of L = 2,048, then the random-phase sinusoid
+        stages, seed = [_st("frequency_mask", width=102), _st("random_sinusoid", amplitude=1.0)], 2
     elif cfg == 4:
-        stages = (SpeedWarp(3, 3.0, "cubic"), Resize(1500), Convolve("hann", 7))
+        stages = [_st("speed_warp", n_speed_change=3, max_speed_ratio=3.0, interpolation="cubic"),
+                  _st("resize", target_len=1500), _st("convolve", window="hann", size=7)]
         seed = 3
     else:
-        p = 0.5
-        stages = (Jitter(0.05, probability=p), Scale(0.1, probability=p), Rotate(probability=p),
-                  PermuteSegments(4, probability=p), Reverse(probability=p), Quantize(16, probability=p),
-                  Drift(0.5, 5, probability=p), InjectNoise(UniformNoise(0.1), probability=p),
-                  InjectNoise(GaussianNoise(0.1), probability=p), InjectNoise(SpikeNoise(5, 2.0), probability=p),
-                  InjectNoise(SlopeTrendNoise(0.5), probability=p),
-                  AmplitudePhasePerturb(0.1, 0.1, probability=p), FrequencyMask(51, probability=p),
-                  TimeWarp(5, 0.5, probability=p), WindowWarp(128, 4, 0.5, probability=p),
-                  Dropout(0.05, probability=p), Pool(4, probability=p), Convolve("hann", 7, probability=p),
-                  RandomSinusoid(0.5, probability=p), SpeedWarp(3, 3.0, probability=p))
-        seed = 5
-    return Pipeline(stages=stages, master_seed=seed)
+        stages, seed = chain5_stages(1024, mask_width=51), 5
+    return {"master_seed": seed, "parallel": False, "mode": "standard", "stages": stages}
+
+
+def chain5_stages(L: int, mask_width: int | None = None) -> list:
+    """Config 5's chain of all 20 length-preserving kinds at p = 0.5; for the
+    sweep its length-dependent parameters scale with L:
+    mask width ~5% of the bins, window = min(128, L), segments <= L."""
+    p = 0.5
+    bins = L // 2 + 1
+    if mask_width is None:
+        mask_width = max(1, int(0.05 * bins))
+    return [_st("jitter", p, sigma=0.05), _st("scale", p, sigma_factor=0.1), _st("rotate", p),
+            _st("permute_segments", p, n_segments=min(4, L)), _st("reverse", p), _st("quantize", p, n_levels=16),
+            _st("drift", p, max_drift=0.5, n_points=5),
+            _st("inject_noise", p, noise={"kind": "uniform", "half_width": 0.1}),
+            _st("inject_noise", p, noise={"kind": "gaussian", "sigma": 0.1}),
+            _st("inject_noise", p, noise={"kind": "spike", "count": min(5, L), "magnitude": 2.0}),
+            _st("inject_noise", p, noise={"kind": "slope_trend", "max_offset": 0.5}),
+            _st("amplitude_phase_perturb", p, sigma_amp=0.1, sigma_phase=0.1),
+            _st("frequency_mask", p, width=mask_width),
+            _st("time_warp", p, n_knots=5, intensity=0.5),
+            _st("time_warp_window", p, window_size=min(128, L), n_knots=4, intensity=0.5),
+            _st("dropout", p, rate=0.05), _st("pool", p, size=4), _st("convolve", p, window="hann", size=7),
+            _st("random_sinusoid", p, amplitude=0.5, min_bin=min(1, L // 2)),
+            _st("speed_warp", p, n_speed_change=3, max_speed_ratio=3.0, interpolation="cubic")]
+
+
+def pipeline(cfg: int):
+    """The product Pipeline for a BASELINE config."""
+    from paper_2601_03159_b200 import Pipeline
+
+    return Pipeline.parse(pipeline_config(cfg))
 
 
 def sweep_datasets(count: int = 100, seed: int = 2026):
@@ -132,24 +169,12 @@ def sweep_datasets(count: int = 100, seed: int = 2026):
     return [(i, int(a), int(b)) for i, (a, b) in enumerate(zip(n, L))]
 
 
-def sweep_pipeline(L: int, seed: int):
-    """The config-5 chain with length-scaled parameters:
-    mask width ~5% of the bins, window = min(128, L), segments <= L."""
-    from paper_2601_03159_b200 import (AmplitudePhasePerturb, Convolve, Drift, Dropout, FrequencyMask,
-                                       GaussianNoise, InjectNoise, Jitter, PermuteSegments, Pipeline, Pool,
-                                       Quantize, RandomSinusoid, Reverse, Rotate, Scale, SlopeTrendNoise,
-                                       SpeedWarp, SpikeNoise, TimeWarp, UniformNoise, WindowWarp)
+def sweep_config(L: int, seed: int) -> dict:
+    return {"master_seed": seed, "parallel": False, "mode": "standard", "stages": chain5_stages(L)}
 
-    p = 0.5
-    bins = L // 2 + 1
-    stages = (Jitter(0.05, probability=p), Scale(0.1, probability=p), Rotate(probability=p),
-              PermuteSegments(min(4, L), probability=p), Reverse(probability=p), Quantize(16, probability=p),
-              Drift(0.5, 5, probability=p), InjectNoise(UniformNoise(0.1), probability=p),
-              InjectNoise(GaussianNoise(0.1), probability=p),
-              InjectNoise(SpikeNoise(min(5, L), 2.0), probability=p),
-              InjectNoise(SlopeTrendNoise(0.5), probability=p), AmplitudePhasePerturb(0.1, 0.1, probability=p),
-              FrequencyMask(max(1, int(0.05 * bins)), probability=p), TimeWarp(5, 0.5, probability=p),
-              WindowWarp(min(128, L), 4, 0.5, probability=p), Dropout(0.05, probability=p),
-              Pool(4, probability=p), Convolve("hann", 7, probability=p),
-              RandomSinusoid(0.5, min_bin=min(1, L // 2), probability=p), SpeedWarp(3, 3.0, probability=p))
-    return Pipeline(stages=stages, master_seed=seed)
+
+def sweep_pipeline(L: int, seed: int):
+    """The config-5 chain with length-scaled parameters for one sweep dataset."""
+    from paper_2601_03159_b200 import Pipeline
+
+    return Pipeline.parse(sweep_config(L, seed))

@@ -76,15 +76,95 @@ def run_stages(stage_arr, n_stages: int, aux: np.ndarray, seed: int, values: np.
     return out
 
 
-def run_pipeline(pipe, values: np.ndarray, threads: int = 1, series_offset: int = 0) -> np.ndarray:
-    """Oracle result of product Pipeline `pipe` on `values` (same lowering)."""
-    from paper_2601_03159_b200.pipeline import lower_stages
+class OStage(ctypes.Structure):
+    """struct sa_stage (include/seriesaug_b200.h), declared here so the oracle
+    lowers configs without the product package."""
 
-    arr, aux = lower_stages(pipe.stages, 0)
-    L_out = pipe.projected_length(values.shape[1])
-    rows = values.shape[0] * pipe.row_factor()
-    return run_stages(arr, len(pipe.stages), aux, pipe.master_seed, values, L_out, rows,
-                      series_offset=series_offset, threads=threads)
+    _fields_ = [("op", ctypes.c_int32), ("index", ctypes.c_int32), ("probability", ctypes.c_double),
+                ("f", ctypes.c_double * 6), ("i", ctypes.c_int64 * 6),
+                ("aux_off", ctypes.c_int32), ("aux_len", ctypes.c_int32)]
+
+
+# kind -> (op code, int params, float params); the header's SA_OP_* codes
+_OPS = {
+    "jitter": (1, [], ["sigma"]), "scale": (2, [], ["sigma_factor"]), "rotate": (3, [], []),
+    "permute_segments": (4, ["n_segments"], []), "crop": (5, ["size"], []), "reverse": (6, [], []),
+    "resize": (7, ["target_len"], []), "quantize": (8, ["n_levels"], []),
+    "drift": (9, ["n_points"], ["max_drift"]), "repeat": (14, ["r"], []),
+    "amplitude_phase_perturb": (15, [], ["sigma_amp", "sigma_phase"]), "frequency_mask": (16, ["width"], []),
+    "time_warp": (17, ["n_knots"], ["intensity"]), "time_warp_window": (18, ["window_size", "n_knots"], ["intensity"]),
+    "dropout": (19, [], ["rate", "fill"]), "pool": (20, ["size", "reducer"], []), "convolve": (21, [], []),
+    "speed_warp": (22, ["n_speed_change", "interpolation"], ["max_speed_ratio"]),
+    "random_sinusoid": (23, ["min_bin"], ["amplitude"]),
+}
+_NOISE = {"uniform": (10, "half_width"), "gaussian": (11, "sigma"), "spike": (12, "magnitude"),
+          "slope_trend": (13, "max_offset")}
+_ENUMS = {"reducer": ("mean", "max", "min"), "interpolation": ("linear", "cubic")}
+_DEFAULTS = {"dropout": {"fill": 0.0}, "pool": {"reducer": "mean"}, "convolve": {"window": "hann", "size": 7},
+             "speed_warp": {"n_speed_change": 3, "max_speed_ratio": 3.0, "interpolation": "cubic"},
+             "random_sinusoid": {"min_bin": 1}, "time_warp": {"n_knots": 4, "intensity": 0.5},
+             "drift": {"n_points": 6}, "time_warp_window": {"n_knots": 4, "intensity": 0.5}}
+
+
+def lower_config(config: dict, first_index: int = 0):
+    """A reference JSON pipeline config -> (stage table, aux table)."""
+    stages = config["stages"]
+    arr = (OStage * max(1, len(stages)))()
+    aux: list = []
+    for j, rec in enumerate(stages):
+        kind, p = rec["kind"], dict(_DEFAULTS.get(rec["kind"], {}), **rec.get("params", {}))
+        st = arr[j]
+        st.index, st.probability = first_index + j, float(rec.get("probability", 1.0))
+        if kind == "inject_noise":
+            nz = p["noise"]
+            st.op, name = _NOISE[nz["kind"]]
+            st.f[0] = nz[name]
+            st.i[0] = nz.get("count", 0)
+            continue
+        st.op, ints, flts = _OPS[kind]
+        for k, name in enumerate(ints):
+            st.i[k] = _ENUMS[name].index(p[name]) if name in _ENUMS else int(p[name])
+        for k, name in enumerate(flts):
+            st.f[k] = float(p[name])
+        if kind == "convolve":
+            from scipy.signal import get_window
+
+            w = get_window("boxcar" if p["window"] == "flat" else p["window"], p["size"], fftbins=False)
+            taps = w / w.sum()
+            st.aux_off, st.aux_len = len(aux), len(taps)
+            aux.extend(float(v) for v in taps)
+    return arr, np.ascontiguousarray(aux, dtype=np.float64)
+
+
+def geometry(config: dict, L: int) -> tuple[int, int]:
+    """(rows out per row in, final length): Repeat / Crop / Resize at p = 1."""
+    r, out = 1, L
+    for rec in config["stages"]:
+        if float(rec.get("probability", 1.0)) != 1.0:
+            continue
+        p = rec.get("params", {})
+        if rec["kind"] == "crop":
+            out = int(p["size"])
+        elif rec["kind"] == "resize":
+            out = int(p["target_len"])
+        elif rec["kind"] == "repeat":
+            r = int(p["r"])
+    return r, out
+
+
+def run_config(config: dict, values: np.ndarray, threads: int = 1, series_offset: int = 0,
+               first_index: int = 0) -> np.ndarray:
+    """Oracle result of a reference JSON pipeline config on `values`."""
+    arr, aux = lower_config(config, first_index)
+    r, L_out = geometry(config, values.shape[1])
+    return run_stages(arr, len(config["stages"]), aux, int(config.get("master_seed", 0)), values, L_out,
+                      values.shape[0] * r, series_offset=series_offset, threads=threads)
+
+
+def run_pipeline(pipe, values: np.ndarray, threads: int = 1, series_offset: int = 0) -> np.ndarray:
+    """Oracle result of a Pipeline (any object with the reference's
+    describe()) on `values`: lowered from its JSON config by the oracle."""
+    return run_config(pipe.describe(), values, threads=threads, series_offset=series_offset)
 
 
 def fft_forward(values: np.ndarray):

@@ -1,4 +1,4 @@
-"""The genuine reference pipeline on all host cores -- BASELINE
+"""The genuine reference pipeline on the host cores -- BASELINE
 INFRASTRUCTURE ONLY (bench.py's reference arm and cpu_baseline legs).
 
 Runs the unmodified reference (`seriesaug` from oracle/_ref, plus the
@@ -13,12 +13,14 @@ SURVEY.md §8(d) lists:
              on its own contiguous range of series (pipeline.py:143-157; bitwise
              the standard mode's result)
 
-This module imports neither torch nor the product package, so spawned worker
-processes stay light and the reference arm never loads the B200 library.
+This module imports neither torch nor the product package, so the spawned
+worker processes stay light and the reference arm never loads the B200
+library.
 """
 
 from __future__ import annotations
 
+import json
 import os
 import time
 
@@ -33,7 +35,7 @@ def walks(n: int, L: int, seed: int) -> np.ndarray:
     return np.cumsum(np.random.default_rng(seed).normal(0.0, 1.0, (n, L)), axis=1)
 
 
-def pipeline_from_config(config: dict):
+def reference_pipeline(config: dict):
     from oracle.refpkg import import_reference
 
     ref = import_reference()
@@ -42,65 +44,114 @@ def pipeline_from_config(config: dict):
     return ref.Pipeline.parse(config)
 
 
-def _init(config: dict, rows: int, L: int, seed: int) -> None:
-    _STATE["pipe"] = pipeline_from_config(config)
-    _STATE["rows"], _STATE["L"], _STATE["seed"] = rows, L, seed
+def _prepare(task) -> int:
+    """Build the task's pipeline and input block in this process (untimed).
+    A task is one (config, L, first, rows, seed) block or a list of them."""
+    if isinstance(task, list):
+        for t in task:
+            _prepare(t)
+        return os.getpid()
+    cfg, L, first, rows, seed = task
+    if cfg not in _STATE:
+        _STATE[cfg] = reference_pipeline(json.loads(cfg))
+    if (rows, L, seed) not in _STATE:
+        _STATE[(rows, L, seed)] = walks(rows, L, seed)
+    return os.getpid()
 
 
-def _work(task: tuple[int, int]) -> tuple[int, float]:
-    """Per-sample reference loop over `rows` series whose global indices start
-    at `first`; returns (output points, checksum)."""
+def _work(task: tuple) -> tuple[int, float]:
+    """One task = (config JSON, L, first global series index, rows, input
+    seed): the reference's per-sample loop over `rows` random walks; returns
+    (output points, checksum).  Pipelines and inputs are cached per process,
+    so a repeated task times the augmentation only."""
     from seriesaug.core import SeedContext
 
-    first, block = task
-    pipe = _STATE["pipe"]
-    x = _STATE.get(("x", block))
-    if x is None:
-        x = walks(_STATE["rows"], _STATE["L"], _STATE["seed"] * 1_000_003 + block)
-        _STATE[("x", block)] = x
-    seed = pipe.master_seed
+    if isinstance(task, list):
+        res = [_work(t) for t in task]
+        return sum(r[0] for r in res), sum(r[1] for r in res)
+    cfg, L, first, rows, seed = task
+    _prepare(task)
+    pipe, x = _STATE[cfg], _STATE[(rows, L, seed)]
+    ms = pipe.master_seed
     pts, chk = 0, 0.0
-    for q in range(x.shape[0]):
+    for q in range(rows):
         y = x[q]
         for j, stage in enumerate(pipe.stages):
-            y = stage.augment_one(y, SeedContext(seed, j, first + q))
+            y = stage.augment_one(y, SeedContext(ms, j, first + q))
         pts += y.size
         chk += float(y[0])
     return pts, chk
 
 
-class ProcessPoolRun:
-    """A spawn-context pool of `cores` processes, each holding `rows` input
-    series; run(step) times one pass of every process over its series."""
+def _worker_main(cmd_q, res_q, barrier) -> None:
+    task = None
+    while True:
+        cmd = cmd_q.get()
+        if cmd[0] == "task":
+            task = cmd[1]
+            _prepare(task)
+            res_q.put(("ready", os.getpid()))
+        elif cmd[0] == "run":
+            barrier.wait()
+            t0 = time.perf_counter()
+            pts, chk = _work(task)
+            res_q.put(("done", pts, time.perf_counter() - t0))
+        else:
+            return
 
-    def __init__(self, config: dict, rows: int, L: int, cores: int | None = None, seed: int = 5):
+
+class ProcessPool:
+    """`cores` persistent spawn-context worker processes, one block of series
+    each.  run() releases all workers through one barrier and returns the
+    points they produced and the slowest worker's time: the wall time of
+    the parallel pass (inputs and pipelines are built before the barrier)."""
+
+    def __init__(self, cores: int | None = None):
         import multiprocessing as mp
-        from concurrent.futures import ProcessPoolExecutor
 
+        ctx = mp.get_context("spawn")
         self.cores = cores or os.cpu_count() or 1
-        self.rows, self.L = rows, L
-        self.ex = ProcessPoolExecutor(self.cores, mp_context=mp.get_context("spawn"), initializer=_init,
-                                      initargs=(config, rows, L, seed))
-        # every worker imports the reference and generates its block (untimed)
-        list(self.ex.map(_work, [(w * rows, w) for w in range(self.cores)]))
+        self.barrier = ctx.Barrier(self.cores)
+        self.res_q = ctx.Queue()
+        self.cmd_q = [ctx.Queue() for _ in range(self.cores)]
+        self.procs = [ctx.Process(target=_worker_main, args=(q, self.res_q, self.barrier), daemon=True)
+                      for q in self.cmd_q]
+        for p in self.procs:
+            p.start()
+
+    def assign(self, tasks: list) -> None:
+        """Give worker w task w (one per worker) and wait until all are built."""
+        assert len(tasks) == self.cores
+        for q, t in zip(self.cmd_q, tasks):
+            q.put(("task", t))
+        for _ in tasks:
+            assert self.res_q.get()[0] == "ready"
 
     def run(self) -> tuple[int, float]:
-        t0 = time.perf_counter()
-        res = list(self.ex.map(_work, [(w * self.rows, w) for w in range(self.cores)]))
-        dt = time.perf_counter() - t0
-        return sum(p for p, _ in res), dt
+        for q in self.cmd_q:
+            q.put(("run",))
+        res = [self.res_q.get() for _ in range(self.cores)]
+        return sum(r[1] for r in res), max(r[2] for r in res)
 
-    def close(self):
-        self.ex.shutdown()
+    def close(self) -> None:
+        for q in self.cmd_q:
+            q.put(("stop",))
+        for p in self.procs:
+            p.join(timeout=10)
 
 
-def time_serial(config: dict, n: int, L: int, parallel: bool, seed: int = 5) -> tuple[int, float]:
+def config_tasks(config: dict, L: int, rows_per_core: int, cores: int, first: int = 0, seed: int = 5) -> list:
+    """One contiguous block of series per core (global indices from `first`)."""
+    cfg = json.dumps(config, sort_keys=True)
+    return [(cfg, L, first + w * rows_per_core, rows_per_core, seed * 1_000_003 + w) for w in range(cores)]
+
+
+def time_pipeline(config: dict, n: int, L: int, parallel: bool, seed: int = 5) -> tuple[int, float]:
     """The reference's own Pipeline.run (standard mode) on an n x L batch."""
     from oracle.refpkg import import_reference
 
     ref = import_reference()
-    cfg = dict(config, parallel=parallel)
-    pipe = pipeline_from_config(cfg)
+    pipe = reference_pipeline(dict(config, parallel=parallel))
     b = ref.Batch(walks(n, L, seed))
     t0 = time.perf_counter()
     out = pipe.run(b)

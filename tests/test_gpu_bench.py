@@ -44,3 +44,32 @@ def test_reference_arm_contract():
     d = _run("--impl", "reference", "--config", "2", "--steps", "1", "--warmup", "0")
     assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["value"] == d["value"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+
+
+def test_bench_two_ranks_shard_bitwise(tmp_path):
+    """`bench.py --gpus 2` launches its own two ranks (no torchrun env), each
+    on its contiguous series range with its global series_offset; here both
+    ranks share cuda:0 and synchronise over gloo (no kernel waits on another
+    rank: the ranks only meet at the barrier and the max-reduce).  The two
+    shards concatenated must equal the single-rank output bit for bit."""
+    env = dict(os.environ, SA_BENCH_DEVICE="0", SA_BENCH_BACKEND="gloo")
+    common = ["--config", "2", "--steps", "3", "--warmup", "3", "--no-cpu", "--no-e2e"]
+
+    def run(n, d):
+        out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(n), *common,
+                              "--check-out", str(d)], cwd=ROOT, capture_output=True, text=True, timeout=600,
+                             env=env)
+        assert out.returncode == 0, out.stderr[-2000:]
+        lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+        assert len(lines) == 1, out.stdout
+        return json.loads(lines[0])
+
+    import numpy as np
+
+    one = run(1, tmp_path / "one")
+    two = run(2, tmp_path / "two")
+    assert one["n_gpus"] == 1 and two["n_gpus"] == 2
+    assert two["config"]["n_series"] == one["config"]["n_series"] == 10_000
+    a = np.load(tmp_path / "one" / "rank0_of1.npy")
+    b = np.concatenate([np.load(tmp_path / "two" / f"rank{r}_of2.npy") for r in range(2)])
+    assert a.shape == b.shape and np.array_equal(a.view(np.uint64), b.view(np.uint64))

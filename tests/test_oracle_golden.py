@@ -146,3 +146,25 @@ def test_similarity_ordering_criterion10(golden):
         sims = [1.0 / (1.0 + O.dtw(base[i], out[i])[0] / base.shape[1]) for i in range(base.shape[0])]
         score = sum(sims) / len(sims)
         assert abs(score - case["augmented"][name]["score"]) < 1e-9, name
+
+
+def test_oracle_lowering_equals_product(golden):
+    """The oracle lowers JSON configs itself (oracle.lower_config, no product
+    code); for every golden config it must produce the product's stage table
+    byte for byte (so oracle results check the product's lowering too)."""
+    import dataclasses
+
+    from paper_2601_03159_b200 import AUGMENTER_REGISTRY
+
+    for case in _cases(golden, ("pipeline", "augment_batch")):
+        first = case["augmenter_index"] or 0
+        a1, x1 = O.lower_config(case["config"], first)
+        a2, x2 = lower_stages(Pipeline.parse(case["config"]).stages, first)
+        n = len(case["config"]["stages"])
+        assert bytes(a1)[:n * 120] == bytes(a2)[:n * 120], case["name"]
+        assert np.array_equal(x1, x2), case["name"]
+    # the oracle's parameter defaults (for configs that omit them) are the product's
+    for kind, dflt in O._DEFAULTS.items():
+        fields = {f.name: f.default for f in dataclasses.fields(AUGMENTER_REGISTRY[kind])}
+        for name, v in dflt.items():
+            assert fields[name] == v, (kind, name)
