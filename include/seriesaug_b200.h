@@ -276,6 +276,11 @@ int sa_augment_spectrum(const sa_stage* stage, uint64_t master_seed, int64_t ser
 int sa_host_copy(void* dst, const void* src, int64_t bytes);
 int sa_host_alloc(void** ptr, int64_t bytes);
 int sa_host_free(void* ptr);
+/* Batch validation on the host cores: *all_finite = 1 iff none of the n
+ * doubles at p is NaN or +-Inf.  Replaces the reference Batch's
+ * np.isfinite(values).all() (core.py:103-104) for large host batches; the
+ * result is the same predicate, evaluated on the exponent bits. */
+int sa_host_all_finite(const double* p, int64_t n, int32_t* all_finite);
 
 #ifdef __cplusplus
 }

@@ -69,7 +69,9 @@ def run_host(stages, values: np.ndarray, seed: int, first_index: int = 0, series
     rows = n * r
     L_out = L if len_out is None else int(len_out)
     if out is None:
-        out = np.empty((rows, L_out), dtype=np.float64)
+        from .memory import output_array
+
+        out = output_array((rows, L_out))
     elif out.shape != (rows, L_out) or out.dtype != np.float64 or not out.flags.c_contiguous:
         raise ValueError(f"out must be a C-contiguous float64 array of shape {(rows, L_out)}")
     devices = devices or [_native.current_device()]
@@ -209,8 +211,10 @@ def fft_forward_host(values: np.ndarray):
     n, L = x.shape
     _native.current_device()
     bins = L // 2 + 1
-    re = np.empty((n, bins), dtype=np.float64)
-    im = np.empty((n, bins), dtype=np.float64)
+    from .memory import output_array
+
+    re = output_array((n, bins))
+    im = output_array((n, bins))
     _native.check(_native.lib().sa_fft_forward_host(_ptr(x), n, L, _ptr(re), _ptr(im)), "sa_fft_forward_host")
     return re, im
 
@@ -221,7 +225,9 @@ def fft_inverse_host(re: np.ndarray, im: np.ndarray, L: int) -> np.ndarray:
     im = np.ascontiguousarray(im, dtype=np.float64)
     _native.current_device()
     n = re.shape[0]
-    out = np.empty((n, L), dtype=np.float64)
+    from .memory import output_array
+
+    out = output_array((n, L))
     _native.check(_native.lib().sa_fft_inverse_host(_ptr(re), _ptr(im), n, L, _ptr(out)), "sa_fft_inverse_host")
     return out
 
@@ -247,7 +253,9 @@ def dct_host(values: np.ndarray, inverse: bool) -> np.ndarray:
     x = np.ascontiguousarray(values, dtype=np.float64)
     n, L = x.shape
     _native.current_device()
-    out = np.empty_like(x)
+    from .memory import output_array
+
+    out = output_array((n, L))
     fn = _native.lib().sa_dct_inverse_host if inverse else _native.lib().sa_dct_forward_host
     _native.check(fn(_ptr(x), n, L, _ptr(out)), "sa_dct_host")
     return out

@@ -81,13 +81,15 @@ def lib() -> ctypes.CDLL:
         L.sa_host_copy.argtypes = [_vp, _vp, _i64]
         L.sa_host_alloc.argtypes = [ctypes.POINTER(ctypes.c_void_p), _i64]
         L.sa_host_free.argtypes = [_vp]
+        L.sa_host_all_finite.argtypes = [_vp, _i64, _vp]
         for fn in ("sa_init", "sa_derive_key", "sa_pipeline_launch", "sa_pipeline_run",
                    "sa_pipeline_run_host", "sa_fft_forward", "sa_fft_inverse",
                    "sa_augment_spectrum", "sa_host_alloc", "sa_host_free", "sa_dct_forward",
                    "sa_dct_inverse", "sa_dtw_batch", "sa_dtw_path", "sa_repr_values", "sa_parse_values", "sa_dataset_open",
                    "sa_dataset_values", "sa_dataset_labels", "sa_dataset_headers", "sa_dataset_close",
                    "sa_dataset_format_size", "sa_dataset_format_write", "sa_fft_forward_host", "sa_fft_inverse_host",
-                   "sa_dct_forward_host", "sa_dct_inverse_host", "sa_dtw_batch_host", "sa_host_copy"):
+                   "sa_dct_forward_host", "sa_dct_inverse_host", "sa_dtw_batch_host", "sa_host_copy",
+                   "sa_host_all_finite"):
             getattr(L, fn).restype = ctypes.c_int
         if L.sa_abi_version() != _abi.SA_ABI_VERSION:
             raise UnsupportedPlatformError("backend library ABI version mismatch")

@@ -14,11 +14,15 @@
 //      per-stage Batch() re-validation, core.py:259 -> :104) into a flag;
 //   5. coalesced 128-bit stores of the output row -- one HBM write per series.
 #include <cuda_runtime.h>
+#include <immintrin.h>
 
 #include <algorithm>
 #include <initializer_list>
+#include <chrono>
 #include <cmath>
+#include <atomic>
 #include <condition_variable>
+#include <deque>
 #include <thread>
 #include <cstdio>
 #include <cstring>
@@ -1902,11 +1906,7 @@ int sa_pipeline_run_host(const sa_stage* stages, int32_t n_stages, const double*
     // each slot accumulates the kernel's status bits in its own flag word
     const HostIn in{h_in, 8 * len_in};
     const HostOut out{h_out, 8 * len_out * r};
-    if (!ds.hs[0]) {
-        rc = ensure_cap(g_host_stage[dev < 0 ? 0 : (dev >= kMaxDevices ? kMaxDevices - 1 : dev)], ds, 0, 0, 0,
-                        false, 0);
-        if (rc) return rc;
-    }
+    if ((rc = ensure_streams(ds))) return rc;
     for (int k = 0; k < DeviceState::NS; ++k)  // ordered before each slot's kernels
         SA_CUDA(cudaMemsetAsync(ds.dflags + k, 0, sizeof(uint32_t), ds.hs[k]));
     rc = run_rows_host(dev, n, &in, 1, &out, 1,
@@ -2250,6 +2250,36 @@ int sa_augment_spectrum(const sa_stage* stage, uint64_t master_seed, int64_t ser
 int sa_host_copy(void* dst, const void* src, int64_t bytes) {
     if (bytes < 0 || (bytes > 0 && (!dst || !src))) return fail(SA_ERR_INVALID_ARG, "sa_host_copy: bad arguments");
     CopyPool::get().copy(dst, src, (size_t)bytes);
+    return SA_OK;
+}
+
+int sa_host_all_finite(const double* p, int64_t n, int32_t* all_finite) {
+    if (n < 0 || !all_finite || (n > 0 && !p)) return fail(SA_ERR_INVALID_ARG, "sa_host_all_finite: bad arguments");
+    // 256 KB blocks over the host cores; a block stops at its first bad word
+    // (exponent all ones: NaN or +-Inf), and later blocks see the flag
+    const int64_t kBlock = 1 << 15;
+    const int64_t blocks = (n + kBlock - 1) / kBlock;
+    std::atomic<int> bad{0};
+    const uint64_t* w = reinterpret_cast<const uint64_t*>(p);
+    auto scan = [&](size_t blk) {
+        if (bad.load(std::memory_order_relaxed)) return;
+        const int64_t lo = (int64_t)blk * kBlock, hi = std::min(n, lo + kBlock);
+        uint64_t acc = 0;
+        for (int64_t i = lo; i < hi; ++i) acc |= (uint64_t)((w[i] & 0x7ff0000000000000ull) == 0x7ff0000000000000ull);
+        if (acc) bad.store(1, std::memory_order_relaxed);
+    };
+    if (blocks <= 4) {
+        for (int64_t b = 0; b < blocks; ++b) scan((size_t)b);
+    } else {
+        // group blocks into ~4 jobs per thread so job overhead stays small
+        CopyPool& pool = CopyPool::get();
+        const int64_t jobs = std::min<int64_t>(blocks, 4 * (int64_t)pool.threads());
+        const int64_t per = (blocks + jobs - 1) / jobs;
+        pool.parallel((size_t)jobs, [&](size_t j) {
+            for (int64_t b = (int64_t)j * per; b < std::min(blocks, ((int64_t)j + 1) * per); ++b) scan((size_t)b);
+        });
+    }
+    *all_finite = bad.load() ? 0 : 1;
     return SA_OK;
 }
 

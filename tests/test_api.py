@@ -6,6 +6,7 @@ stage lowering.  Tests that compare with the reference itself skip when it is
 absent (it is only mounted in the build container).
 """
 
+import ctypes
 import json
 
 import numpy as np
@@ -211,3 +212,64 @@ def test_custom_augmenter_without_kernel_fails_loudly():
     with pytest.raises(sa.InvalidConfigError, match="not available"):
         sa.Jitter(0.1)._apply(np.zeros(4), None)
     assert sa.Pipeline(stages=(sa.Jitter(0.1), sa.FrequencyMask(3), sa.Dropout(0.1))).stages
+
+
+@pytest.mark.parametrize("where", [0, 12345, (1 << 20) + 7, -1])
+@pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf])
+def test_batch_native_finiteness_scan(where, bad):
+    """Large batches are validated by the library's multi-threaded scan
+    (sa_host_all_finite): same predicate as np.isfinite(...).all()."""
+    from paper_2601_03159_b200 import Batch, InvalidInputError
+    from paper_2601_03159_b200.core import _NATIVE_SCAN_MIN
+
+    x = np.random.default_rng(0).normal(size=(64, (_NATIVE_SCAN_MIN + 4096) // 64))
+    Batch(x)
+    x.reshape(-1)[where] = bad
+    with pytest.raises(InvalidInputError):
+        Batch(x)
+    x.reshape(-1)[where] = np.finfo(np.float64).max  # largest finite: accepted
+    Batch(x)
+    x.reshape(-1)[where] = 5e-324  # subnormal: accepted
+    Batch(x)
+
+
+def test_output_cache_policy(monkeypatch):
+    """memory.output_array: first request of a size -> numpy memory, a repeat
+    -> a page-locked block that returns to the cache with its array."""
+    import gc
+
+    from paper_2601_03159_b200 import memory
+
+    calls = []
+
+    class FakeLib:
+        def sa_host_alloc(self, pp, size):
+            buf = ctypes.create_string_buffer(size)
+            calls.append(("alloc", size, buf))
+            pp._obj.value = ctypes.addressof(buf)
+            return 0
+
+        def sa_host_free(self, ptr):
+            calls.append(("free", ptr))
+            return 0
+
+    monkeypatch.setattr(memory._native, "lib", lambda: FakeLib())
+    monkeypatch.setattr(memory, "_outputs", memory._OutputCache())
+    memory._outputs.cap = 64 << 20
+    small = memory.output_array((10, 10))
+    assert isinstance(small.base, type(None)) or not calls  # below the threshold: numpy
+    a = memory.output_array((1024, 1024))  # 8 MB, first request of this size
+    assert not calls and a.flags.owndata
+    b = memory.output_array((1024, 1024))  # repeat: page-locked block
+    assert len(calls) == 1 and calls[0][1] == 8 << 20 and b.shape == (1024, 1024) and not b.flags.owndata
+    b[...] = 1.0
+    ptr = b.ctypes.data
+    del b
+    gc.collect()
+    c = memory.output_array((1024, 1024))  # reused from the cache
+    assert len(calls) == 1 and c.ctypes.data == ptr
+    d = memory.output_array((1024, 1024))  # second live block
+    assert len(calls) == 2
+    memory._outputs.cap = 20 << 20  # no room for a third
+    e = memory.output_array((1024, 1024))
+    assert len(calls) == 2 and e.flags.owndata
