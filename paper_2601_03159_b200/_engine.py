@@ -26,7 +26,27 @@ def _row_factor(stages, repeat_rows: bool) -> int:
     return 1
 
 
+_LOWERED: dict = {}
+
+
 def _lower(stages, first_index, repeat_rows):
+    """Stage table + aux taps of a stage tuple, cached per (stages, first
+    index, repeat mode): augmenters are frozen dataclasses, so a pipeline
+    called repeatedly (a training loop, the bench protocol) lowers once.
+    The cached ctypes table is only read by the library."""
+    try:
+        key = (tuple(stages), int(first_index), bool(repeat_rows))
+        hit = _LOWERED.get(key)
+    except TypeError:  # an unhashable user-defined stage: lower every call
+        return _lower_uncached(stages, first_index, repeat_rows)
+    if hit is None:
+        if len(_LOWERED) >= 256:
+            _LOWERED.clear()
+        hit = _LOWERED[key] = _lower_uncached(stages, first_index, repeat_rows)
+    return hit
+
+
+def _lower_uncached(stages, first_index, repeat_rows):
     arr, aux = lower_stages(stages, first_index)
     if not repeat_rows:  # Repeat's per-series form is the identity (basic.py:396-397)
         for j in range(len(stages)):
