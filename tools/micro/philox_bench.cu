@@ -63,6 +63,30 @@ __device__ __forceinline__ void philox(uint64_t k0, uint64_t k1, uint64_t ctr0, 
     }
     o0 = c0; o1 = c1; o2 = c2; o3 = c3;
 }
+template <int V>
+__device__ __forceinline__ void philox2(uint64_t k0, uint64_t k1, uint64_t ca, uint64_t cb, uint64_t& a0,
+                                        uint64_t& a1, uint64_t& a2, uint64_t& a3, uint64_t& b0, uint64_t& b1,
+                                        uint64_t& b2, uint64_t& b3) {
+    uint64_t c0 = ca, c1 = 0, c2 = 0, c3 = 0, d0 = cb, d1 = 0, d2 = 0, d3 = 0;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r) {
+            k0 += 0x9E3779B97F4A7C15ULL;
+            k1 += 0xBB67AE8584CAA73BULL;
+        }
+        uint64_t hi0, lo0, hi1, lo1, hj0, lj0, hj1, lj1;
+        mulhilo<V>(0xD2E7470EE14C6C93ULL, c0, hi0, lo0);
+        mulhilo<V>(0xCA5A826395121157ULL, c2, hi1, lo1);
+        mulhilo<V>(0xD2E7470EE14C6C93ULL, d0, hj0, lj0);
+        mulhilo<V>(0xCA5A826395121157ULL, d2, hj1, lj1);
+        uint64_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+        uint64_t m0 = hj1 ^ d1 ^ k0, m2 = hj0 ^ d3 ^ k1;
+        c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+        d0 = m0; d1 = lj1; d2 = m2; d3 = lj0;
+    }
+    a0 = c0; a1 = c1; a2 = c2; a3 = c3;
+    b0 = d0; b1 = d1; b2 = d2; b3 = d3;
+}
 // precomputed round keys (the warp-uniform schedule as data, e.g. in smem)
 template <int V>
 __device__ __forceinline__ void philox_rk(const uint64_t* rk, uint64_t ctr0, uint64_t& o0, uint64_t& o1,
@@ -99,6 +123,16 @@ __global__ void __launch_bounds__(384) bench(const uint64_t* keys, uint64_t pk0,
     }
     __syncwarp();
     uint64_t acc = 0;
+    if (MODE == 3) {
+        for (int i = 0; i < iters; i += 2) {
+            uint64_t a0, a1, a2, a3, b0, b1, b2, b3;
+            const uint64_t ctr = (uint64_t)i * 32 + lane + 1;
+            philox2<V>(k0, k1, ctr, ctr + 32, a0, a1, a2, a3, b0, b1, b2, b3);
+            acc ^= a0 ^ a1 ^ a2 ^ a3 ^ b0 ^ b1 ^ b2 ^ b3;
+        }
+        out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+        return;
+    }
     for (int i = 0; i < iters; ++i) {
         uint64_t o0, o1, o2, o3;
         const uint64_t ctr = (uint64_t)i * 32 + lane + 1;
@@ -135,6 +169,7 @@ int main() {
     cudaMemset(keys, 7, 2 * 12 * sms * 8);
     cudaMalloc(&out, sms * 384 * 8);
     run<0, 0>("umul64hi, keys from memory", keys, out, sms);
+    run<0, 3>("umul64hi, 2 blocks per lane interleaved", keys, out, sms);
     run<1, 0>("ptx mad.cc chain, keys from memory", keys, out, sms);
     run<2, 0>("mul.wide pieces, keys from memory", keys, out, sms);
     run<0, 1>("umul64hi, keys as params (uniform)", keys, out, sms);
