@@ -141,6 +141,21 @@ def _profile_json(name):
     return {}
 
 
+def fp64_peak():
+    """Measured FP64 FMA peak of the box (tools/micro/fp64_peak.cu), TFLOP/s."""
+    d = _profile_json("r02_fp64_peak.json")
+    return (float(d["fp64_fma_tflops"]), "measured (profiles/r02_fp64_peak.json)") if d else \
+        (37.0, "nominal B200 FP64")
+
+
+def fft_flops_per_series(cfg, L):
+    """Algorithmic FP64 flops of the FFT-bearing configs:
+    one rfft + irfft pair, 2 x 2.5 L log2 L per series (config 3)."""
+    import math
+
+    return 2 * 2.5 * L * math.log2(L) if cfg == 3 else None
+
+
 def ncu_traffic(cfg):
     return _profile_json("ncu_traffic.json").get(cfg if isinstance(cfg, str) else f"config{cfg}")
 
@@ -417,12 +432,21 @@ def run_b200(args, rank, world, local_rank, dist_ok):
         "hbm_gbs": achieved,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": ncu_traffic(cfg), "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": bytes_launch, "kernel_ms": kern_ms},
+                     "algorithmic_bytes_per_launch": bytes_launch, "kernel_ms": kern_ms,
+                     "peak_north_star": 8000.0, "frac_north_star": achieved / 8000.0},
+        "input_points_per_s": N * L / (ms_per_step / 1e3),
         "gpu_launches": int(launches_all),
         "clocks": clk.summary(),
         "device": {"name": torch.cuda.get_device_name(dev), "sms": props.multi_processor_count,
                    "numpy": np.__version__, "torch": torch.__version__, "build_sha16": build_sha16()},
     }
+    ff = fft_flops_per_series(cfg, L)
+    if ff:  # the FFT-bearing config's compute-side bound (FP64 FMA pipe)
+        fpk, fsrc = fp64_peak()
+        ach_f = ff * n / (kern_ms / 1e3) / 1e12
+        line["fp64_roofline"] = {"achieved": ach_f, "peak": fpk, "unit": "TFLOP/s", "frac": ach_f / fpk,
+                                 "peak_source": fsrc, "flops_per_series": ff,
+                                 "note": "rfft + irfft = 2 x 2.5 L log2 L per series (SURVEY.md 8(d))"}
     # the kernel is issue bound (numpy-exact RNG and FP64 arithmetic per element):
     # warp-instructions per launch (ncu capture; valid only for the build it
     # was captured on) over the live kernel time, against 4 issue slots x SMs
@@ -651,6 +675,10 @@ def run_suite(args):
         byt = 8 * (x.numel() + pts)
         res[f"config{cfg}"] = {"ms": ms, "gpts_s": pts / ms / 1e6, "hbm_gbs": byt / ms / 1e6,
                                "hbm_frac": byt / ms / 1e6 / measured_peak()[0]}
+        ff = fft_flops_per_series(cfg, L)
+        if ff:
+            tf = ff * N / (ms / 1e3) / 1e12
+            res[f"config{cfg}"].update(fp64_tflops=tf, fp64_frac=tf / fp64_peak()[0])
         if cfg in (1, 2):  # launch-bound sizes: the same chain replayed from a CUDA graph
             run = bench_inputs.pipeline(cfg).capture_device(x.contiguous())
             for _ in range(3):
