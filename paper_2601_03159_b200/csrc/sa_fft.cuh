@@ -377,12 +377,33 @@ __device__ __forceinline__ double2* fft_any(double2* a, double2* b, const FftGeo
     return fft_passes<R16>(a, b, g.N, g.npass, g.radix, tw, L, lane);
 }
 
+// rfft split X[k] = E[k] + W_L^k O[k] from Z[k], Z[M - k] (rfft_any).
+__device__ __forceinline__ double2 cta_split(double2 zk, double2 zc, double2 w) {
+    const double er = 0.5 * (zk.x + zc.x), ei = 0.5 * (zk.y - zc.y);
+    const double orr = 0.5 * (zk.y + zc.y), oi = -0.5 * (zk.x - zc.x);
+    const double2 o = cmul(make_double2(orr, oi), w);
+    return make_double2(er + o.x, ei + o.y);
+}
+
+// irfft fold of X[k], X[M - k] into the conjugated FFT input (irfft_any).
+__device__ __forceinline__ double2 cta_fold(double2 xk, double2 xc, double2 w, bool k0) {
+    if (k0) { xk.y = 0.0; xc.y = 0.0; }
+    xc.y = -xc.y;
+    const double er = 0.5 * (xk.x + xc.x), ei = 0.5 * (xk.y + xc.y);
+    const double dr = 0.5 * (xk.x - xc.x), di = 0.5 * (xk.y - xc.y);
+    w.y = -w.y;
+    const double2 o = cmul(make_double2(dr, di), w);
+    return make_double2(er - o.y, -(ei + o.x));
+}
+
 // rfft of the real series x (length L, in buffer xa) -> X[0 .. L/2]
 // (complex, bins = L/2 + 1).  xb is scratch of the same capacity (>= 2L + 2
 // doubles for odd L).  Returns the buffer holding X; the other is free.
+// split == false (even L only): return the packed M-point transform Z itself
+// (the caller splits the bin pairs it needs, see op_spectral).
 template <bool BLUE = true, bool R16 = false>
 __device__ __forceinline__ double2* rfft_any(double* xa, double* xb, int L, const FftGeo& g, const double2* tw,
-                                            int lane) {
+                                            int lane, bool split = true) {
     double2* za = reinterpret_cast<double2*>(xa);
     double2* zb = reinterpret_cast<double2*>(xb);
     // odd L: complexify into xb and take the N = L transform; even L: view
@@ -400,6 +421,7 @@ __device__ __forceinline__ double2* rfft_any(double* xa, double* xb, int L, cons
         __syncwarp();
         return Z;
     }
+    if (!split) return Z;
     const int M = L >> 1;
     double2* X = (Z == za) ? zb : za;
     // four bins per lane step, all loads first: independent latency chains
@@ -440,11 +462,14 @@ __device__ __forceinline__ bool fin_bad(double v) {  // exponent all ones: inf o
 
 // bad (optional): OR-ed with "some output is non-finite" in the final
 // scaling loop, so callers need no separate pass over the row.
+// folded == true (even L only): `other` already holds the folded M points
+// (the conjugated inverse-FFT input); X is scratch.
 template <bool BLUE = true, bool R16 = false>
 __device__ __forceinline__ double* irfft_any(double2* X, double2* other, int L, const FftGeo& g, const double2* tw,
-                                            int lane, bool* bad = nullptr) {
+                                            int lane, bool* bad = nullptr, bool folded = false) {
     const int M = L >> 1;
-    if (!g.packed) {  // odd L: Hermitian completion, full transform, real part
+    if (folded) {
+    } else if (!g.packed) {  // odd L: Hermitian completion, full transform, real part
         const int bins = L / 2 + 1;
         for (int k = lane; k < bins; k += 32) {
             double2 v = X[k];

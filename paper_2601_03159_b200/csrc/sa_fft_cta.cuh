@@ -141,23 +141,4 @@ __device__ __forceinline__ void cta_fft(double2 (&v)[8], double2* buf, int t, co
     if (P::NP > 3) cta_pass<LGN, (P::NP > 3 ? 3 : 0)>(v, buf, t, w);
 }
 
-// rfft split X[k] = E[k] + W_L^k O[k] from Z[k], Z[M - k] (rfft_any).
-__device__ __forceinline__ double2 cta_split(double2 zk, double2 zc, double2 w) {
-    const double er = 0.5 * (zk.x + zc.x), ei = 0.5 * (zk.y - zc.y);
-    const double orr = 0.5 * (zk.y + zc.y), oi = -0.5 * (zk.x - zc.x);
-    const double2 o = cmul(make_double2(orr, oi), w);
-    return make_double2(er + o.x, ei + o.y);
-}
-
-// irfft fold of X[k], X[M - k] into the conjugated FFT input (irfft_any).
-__device__ __forceinline__ double2 cta_fold(double2 xk, double2 xc, double2 w, bool k0) {
-    if (k0) { xk.y = 0.0; xc.y = 0.0; }
-    xc.y = -xc.y;
-    const double er = 0.5 * (xk.x + xc.x), ei = 0.5 * (xk.y + xc.y);
-    const double dr = 0.5 * (xk.x - xc.x), di = 0.5 * (xk.y - xc.y);
-    w.y = -w.y;
-    const double2 o = cmul(make_double2(dr, di), w);
-    return make_double2(er - o.y, -(ei + o.x));
-}
-
 }  // namespace sa

@@ -812,7 +812,6 @@ __global__ void __launch_bounds__(CtaPlan<LGN>::T, 512 / CtaPlan<LGN>::T) spectr
     const int L = 2 * N, bins = N + 1;
     const CtaSmem sm = cta_smem(smem, N);
     __shared__ __align__(16) SpecDraw s_tab[2][64];  // this / next row's draws, stage j
-    __shared__ double2 s_nyq;
     double2 w[8];
     cta_twiddles<LGN>(w, t, tw, LGN + 1);
 #ifndef SA_SPEC_WS
@@ -859,51 +858,58 @@ __global__ void __launch_bounds__(CtaPlan<LGN>::T, 512 / CtaPlan<LGN>::T) spectr
 #pragma unroll
         for (int m = 0; m < 8; ++m) sm.buf[t + m * T] = v[m];
         __syncthreads();
-        double2 X[8];  // bins t + m T (DC / Nyquist imaginary parts pinned to 0)
+        // Bin pairs (k, N - k) that no fired stage touches go straight to the
+        // inverse FFT's input: fold(split(Z)) = conj(Z) there (irfft(rfft(x))
+        // = x), so only the pairs a mask / sinusoid reaches run the split, the
+        // stages and the fold -- on both bins of the pair, in this thread (the
+        // Nyquist bin N pairs with k = 0).  Same formulas and pins as
+        // rfft_any / _apply / irfft_any; untouched bins skip rounding-level work.
+        uint32_t affm = 0;  // bit m: pair of bin t + m T touched by a fired stage
+        for (uint64_t f = fire; f; f &= f - 1) {
+            const int j = __ffsll((long long)f) - 1;
+            const int pos = s_tab[cb][j].pos;
+            const int end = p.st[j].op == SA_OP_FREQ_MASK ? pos + (int)p.st[j].i[0] : pos + 1;
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const int k = t + m * T, kc = N - k;
+                affm |= ((k >= pos && k < end) || (kc >= pos && kc < end)) ? (1u << m) : 0u;
+            }
+        }
 #pragma unroll
         for (int m = 0; m < 8; ++m) {
-            const int k = t + m * T;
-            X[m] = cta_split(sm.buf[k], sm.buf[k == 0 ? 0 : N - k], SA_SPEC_WS ? ws[m] : __ldg(&tw[k]));
-        }
-        double2 nyq = cta_split(sm.buf[0], sm.buf[0], wn);
-        if (t == 0) X[0].y = 0.0;
-        nyq.y = 0.0;
-        for (uint64_t f = fire; f; f &= f - 1) {  // stages in chain order
-            const int j = __ffsll((long long)f) - 1;
-            const DevStage& st = p.st[j];
-            const int pos = s_tab[cb][j].pos;
-            if (st.op == SA_OP_FREQ_MASK) {
-                const int end = pos + (int)st.i[0];
-#pragma unroll
-                for (int m = 0; m < 8; ++m) {
-                    const int k = t + m * T;
-                    if (k >= pos && k < end) X[m] = make_double2(0.0, 0.0);
-                }
-                if (N >= pos && N < end) nyq = make_double2(0.0, 0.0);
+            const int k = t + m * T, kc = N - k;
+            if (((affm >> m) & 1u) == 0u) {
+                v[m] = make_double2(v[m].x, -v[m].y);
             } else {
-                const double2 a = s_tab[cb][j].add;
-                if (pos == N) {
-                    nyq.x = nyq.x + a.x;
-                } else {
-#pragma unroll
-                    for (int m = 0; m < 8; ++m) {
-                        if (t + m * T == pos) {
-                            X[m].x = X[m].x + a.x;
-                            if (pos != 0) X[m].y = X[m].y + a.y;
+                const double2 wk = SA_SPEC_WS ? ws[m] : __ldg(&tw[k]);
+                const double2 zk = v[m], zc = sm.buf[k == 0 ? 0 : kc];
+                double2 a = cta_split(zk, zc, wk);
+                double2 c = cta_split(zc, zk, k == 0 ? wn : make_double2(-wk.x, wk.y));  // W_L^{N-k} = -conj(W_L^k)
+                if (k == 0) {  // DC / Nyquist imaginary parts pinned (freqaugment.py:40-45)
+                    a.y = 0.0;
+                    c.y = 0.0;
+                }
+                for (uint64_t f = fire; f; f &= f - 1) {  // stages in chain order
+                    const int j = __ffsll((long long)f) - 1;
+                    const int pos = s_tab[cb][j].pos;
+                    if (p.st[j].op == SA_OP_FREQ_MASK) {
+                        const int end = pos + (int)p.st[j].i[0];
+                        if (k >= pos && k < end) a = make_double2(0.0, 0.0);
+                        if (kc >= pos && kc < end) c = make_double2(0.0, 0.0);
+                    } else {
+                        const double2 ad = s_tab[cb][j].add;
+                        if (k == pos) {
+                            a.x = a.x + ad.x;
+                            if (pos != 0) a.y = a.y + ad.y;
+                        }
+                        if (kc == pos) {
+                            c.x = c.x + ad.x;
+                            if (pos != N) c.y = c.y + ad.y;
                         }
                     }
                 }
+                v[m] = cta_fold(a, c, wk, k == 0);
             }
-        }
-        __syncthreads();  // the split's reads of the buffer are done
-#pragma unroll
-        for (int m = 0; m < 8; ++m) sm.buf[t + m * T] = X[m];
-        if (t == 0) s_nyq = nyq;
-        __syncthreads();
-#pragma unroll
-        for (int m = 0; m < 8; ++m) {
-            const int k = t + m * T;
-            v[m] = cta_fold(sm.buf[k], k == 0 ? s_nyq : sm.buf[N - k], SA_SPEC_WS ? ws[m] : __ldg(&tw[k]), k == 0);
         }
         cta_fft<LGN>(v, sm.buf, t, w);
         const double sc = 1.0 / (double)N;

@@ -1120,6 +1120,40 @@ __device__ __forceinline__ bool is_spectral_op(int op) {
 __device__ __forceinline__ bool op_spectral(const DevStage& st, WStream& s, double*& cur, double*& oth, int L, Warp& w,
                                             double2*& held, bool keep, bool& bad) {
     if (spectral_noop(st)) return false;
+    // A lone FrequencyMask / RandomSinusoid on an even-length row touches a
+    // few bins: its parameters are drawn first (the same draws, in the same
+    // order, as perturb_spectrum), and the split, the stage and the fold run
+    // only on the bin pairs (k, M - k) it reaches.  Elsewhere fold(split(Z))
+    // = conj(Z) (irfft(rfft(x)) = x), the inverse FFT's input directly.  Same
+    // formulas and pins as rfft_any / _apply / irfft_any; one call site per
+    // transform direction either way (the FFT code is emitted once).
+    const bool sparse = !held && !keep && (L & 1) == 0 && st.op != SA_OP_APP;
+    const int M = L >> 1;
+    int pos = 0, end = 0;
+    double2 add = make_double2(0.0, 0.0);
+    if (sparse) {
+        const int bins = M + 1;
+        if (st.op == SA_OP_FREQ_MASK) {
+            const int wd = (int)st.i[0];
+            int c = (int)bounded(s, w.lane, (uint32_t)(bins - 1));
+            pos = c - wd / 2;
+            if (pos < 0) pos = 0;
+            if (pos > bins - wd) pos = bins - wd;
+            end = pos + wd;
+        } else {  // SA_OP_SINUSOID
+            const int mb = (int)st.i[0];
+            pos = mb + (int)bounded(s, w.lane, (uint32_t)(bins - mb - 1));
+            end = pos + 1;
+            const double phi = (2.0 * 3.14159265358979323846) * next_double(s, w.lane);
+            const double A = st.f[0];
+            if (pos == 0 || pos == M) {
+                add.x = (A * (double)L) * cos(phi);
+            } else {
+                const double h = (A * (double)L) * 0.5;
+                add = make_double2(h * cos(phi), h * sin(phi));
+            }
+        }
+    }
     double2* X;
     if (held) {
         X = held;
@@ -1130,17 +1164,48 @@ __device__ __forceinline__ bool op_spectral(const DevStage& st, WStream& s, doub
         }
         __syncwarp();
     } else {
-        X = rfft_any<SA_CHAIN_BLUE>(cur, oth, L, st.fft, st.tw, w.lane);
+        X = rfft_any<SA_CHAIN_BLUE>(cur, oth, L, st.fft, st.tw, w.lane, !sparse);  // sparse: X = the packed Z
     }
     double* free_buf = (reinterpret_cast<double*>(X) == cur) ? oth : cur;
-    perturb_spectrum(st, s, X, L, free_buf, w);
-    if (keep) {
-        held = X;
-        for (int k = w.lane; k < L / 2 + 1; k += 32) bad |= nonfinite(X[k].x) | nonfinite(X[k].y);
-        return false;
+    if (sparse) {
+        double2* Y = reinterpret_cast<double2*>(free_buf);
+        const bool mask = st.op == SA_OP_FREQ_MASK;
+        for (int k = w.lane; k < M; k += 32) {
+            const int kc = M - k;  // k = 0 pairs with the Nyquist bin M
+            const bool ak = k >= pos && k < end, ac = kc >= pos && kc < end;
+            if (!ak && !ac) {
+                const double2 z = X[k];
+                Y[k] = make_double2(z.x, -z.y);
+                continue;
+            }
+            const double2 zk = X[k], zc = X[k == 0 ? 0 : kc];
+            double2 a = cta_split(zk, zc, __ldg(&st.tw[k]));
+            double2 c = cta_split(zc, zk, __ldg(&st.tw[kc]));
+            if (k == 0) {  // DC / Nyquist imaginary parts pinned (freqaugment.py:40-45)
+                a.y = 0.0;
+                c.y = 0.0;
+            }
+            if (mask) {
+                if (ak) a = make_double2(0.0, 0.0);
+                if (ac) c = make_double2(0.0, 0.0);
+            } else {
+                if (ak) a = make_double2(a.x + add.x, a.y + add.y);
+                if (ac) c = make_double2(c.x + add.x, c.y + add.y);
+            }
+            Y[k] = cta_fold(a, c, __ldg(&st.tw[k]), k == 0);
+        }
+        __syncwarp();
+    } else {
+        perturb_spectrum(st, s, X, L, free_buf, w);
+        if (keep) {
+            held = X;
+            for (int k = w.lane; k < L / 2 + 1; k += 32) bad |= nonfinite(X[k].x) | nonfinite(X[k].y);
+            return false;
+        }
     }
+    // sparse: the folded input is in free_buf and X is scratch
     double2* other = reinterpret_cast<double2*>(free_buf);
-    double* y = irfft_any<SA_CHAIN_BLUE>(X, other, L, st.fft, st.tw, w.lane, &bad);  // checks its outputs
+    double* y = irfft_any<SA_CHAIN_BLUE>(X, other, L, st.fft, st.tw, w.lane, &bad, sparse);  // checks its outputs
     if (y != cur) swapbuf(cur, oth);
     return false;
 }
