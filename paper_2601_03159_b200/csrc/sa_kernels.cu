@@ -1446,8 +1446,11 @@ double op_cost(int op) {
 }
 
 // Lower the ABI stage table into kernel parameters and a launch shape.
+// spread: the caller waits for this launch alone (synchronous entry points),
+// so a batch of less than one wave is spread over the SMs for latency; the
+// asynchronous launch keeps full CTAs (concurrent streams fill the rest).
 int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, int32_t n_aux, uint64_t seed,
-              int64_t offset, int64_t n, int64_t len_in, int64_t len_out, Plan* plan) {
+              int64_t offset, int64_t n, int64_t len_in, int64_t len_out, Plan* plan, bool spread = false) {
     if (ns < 0 || ns > SA_MAX_STAGES) return fail(SA_ERR_INVALID_ARG, "n_stages out of range");
     if (n_aux < 0 || n_aux > SA_MAX_AUX) return fail(SA_ERR_INVALID_ARG, "aux table too large");
     if (n < 0 || len_in < 1 || len_out < 1) return fail(SA_ERR_INVALID_ARG, "bad batch shape");
@@ -1547,6 +1550,10 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
     int fit = (int)((ds.smem_optin - kCtaShared) / (size_t)per_warp);
     int warps = env_int("SA_CTA_WARPS", 0);
     if (warps <= 0) warps = std::min(12, std::max(1, fit));
+    // less than one wave of rows: spread them over the SMs (a row's chain is
+    // latency bound; 38 rows on 4 SMs ran 1.6x slower than on 38)
+    if (spread && env_int("SA_CTA_WARPS", 0) <= 0 && p.rows_out < (int64_t)ds.sms * warps)
+        warps = (int)std::max<int64_t>(1, (p.rows_out + ds.sms - 1) / ds.sms);
     warps = std::max(1, std::min(warps, std::min(12, fit)));
     plan->warps = warps;
     plan->smem = (size_t)per_warp * warps + kCtaShared;
@@ -1879,7 +1886,7 @@ int sa_pipeline_run(const sa_stage* stages, int32_t n_stages, const double* aux,
     int rc = ensure_device(&dev);
     if (rc) return rc;
     Plan plan;
-    rc = make_plan(dev, stages, n_stages, aux, n_aux, master_seed, series_offset, n, len_in, len_out, &plan);
+    rc = make_plan(dev, stages, n_stages, aux, n_aux, master_seed, series_offset, n, len_in, len_out, &plan, true);
     if (rc) return rc;
     uint32_t* dflag = nullptr;
     SA_CUDA(sa_malloc_async((void**)&dflag, sizeof(uint32_t), (cudaStream_t)stream));
@@ -1903,7 +1910,7 @@ int sa_pipeline_run_host(const sa_stage* stages, int32_t n_stages, const double*
     int rc = ensure_device(&dev);
     if (rc) return rc;
     Plan plan;
-    rc = make_plan(dev, stages, n_stages, aux, n_aux, master_seed, series_offset, n, len_in, len_out, &plan);
+    rc = make_plan(dev, stages, n_stages, aux, n_aux, master_seed, series_offset, n, len_in, len_out, &plan, true);
     if (rc) return rc;
     const int64_t r = plan.p.repeat_r;
     std::lock_guard<std::mutex> lk(g_host_mu[dev < 0 ? 0 : (dev >= kMaxDevices ? kMaxDevices - 1 : dev)]);
