@@ -1127,6 +1127,43 @@ __device__ __forceinline__ bool op_spectral(const DevStage& st, WStream& s, doub
     // = conj(Z) (irfft(rfft(x)) = x), the inverse FFT's input directly.  Same
     // formulas and pins as rfft_any / _apply / irfft_any; one call site per
     // transform direction either way (the FFT code is emitted once).
+    if (st.op == SA_OP_SINUSOID && !held && !keep) {
+        // A lone RandomSinusoid: irfft(X + add e_b) = irfft(X) + irfft(add e_b)
+        // and irfft(rfft(x)) = x, so the stage adds bin b's sinusoid in the
+        // time domain -- A cos(2 pi b t / L + phi) (interior b: 2 Re(add
+        // e^{2 pi i b t / L}) / L with add = (A L / 2) e^{i phi}; DC and
+        // Nyquist: the real part only) -- with the same draws, cos / sin of
+        // 2 pi b t / L from the W_L table (exact index (b t) mod L), no
+        // transform.  Differs from the reference's round trip by its FFT
+        // rounding only (spectral tolerance).
+        const int bins = L / 2 + 1;
+        const int mb = (int)st.i[0];
+        const int b = mb + (int)bounded(s, w.lane, (uint32_t)(bins - mb - 1));
+        const double phi = (2.0 * 3.14159265358979323846) * next_double(s, w.lane);
+        const double A = st.f[0];
+        const double cph = cos(phi), sph = sin(phi);
+        if (b == 0 || ((L & 1) == 0 && b == bins - 1)) {
+            const double c0 = A * cph;
+            for (int t = w.lane; t < L; t += 32) {
+                const double v = cur[t] + ((b != 0 && (t & 1)) ? -c0 : c0);
+                cur[t] = v;
+                bad |= nonfinite(v);
+            }
+        } else {
+            const int step = (int)((32ll * b) % L);
+            int m = (int)(((int64_t)b * w.lane) % L);
+            for (int t = w.lane; t < L; t += 32) {
+                const double2 e = __ldg(&st.tw[m]);  // (cos, -sin) of 2 pi m / L
+                const double v = cur[t] + A * (cph * e.x + sph * e.y);
+                cur[t] = v;
+                bad |= nonfinite(v);
+                m += step;
+                m = m >= L ? m - L : m;
+            }
+        }
+        __syncwarp();
+        return false;
+    }
     const bool sparse = !held && !keep && (L & 1) == 0 && st.op != SA_OP_APP;
     const int M = L >> 1;
     int pos = 0, end = 0;
