@@ -803,7 +803,7 @@ __global__ void __launch_bounds__(256) spectral_draw_kernel(const __grid_constan
 }
 
 template <int LGN>
-__global__ void __launch_bounds__(CtaPlan<LGN>::T, 512 / CtaPlan<LGN>::T) spectral_cta_kernel(const __grid_constant__ ChainParams p,
+__global__ void __launch_bounds__(CtaPlan<LGN>::T, 640 / CtaPlan<LGN>::T) spectral_cta_kernel(const __grid_constant__ ChainParams p,
                                                            const double2* __restrict__ tw,
                                                            const SpecDraw* __restrict__ draws) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -814,14 +814,6 @@ __global__ void __launch_bounds__(CtaPlan<LGN>::T, 512 / CtaPlan<LGN>::T) spectr
     __shared__ __align__(16) SpecDraw s_tab[2][64];  // this / next row's draws, stage j
     double2 w[8];
     cta_twiddles<LGN>(w, t, tw, LGN + 1);
-#ifndef SA_SPEC_WS
-#define SA_SPEC_WS 1
-#endif
-    double2 ws[8];
-    if (SA_SPEC_WS) {
-#pragma unroll
-        for (int m = 0; m < 8; ++m) ws[m] = __ldg(&tw[t + m * T]);
-    }
     const double2 wn = __ldg(&tw[N]);
     auto fetch = [&](int64_t row, int b) {
         const double2* xr = reinterpret_cast<const double2*>(p.in + row * L);
@@ -881,7 +873,7 @@ __global__ void __launch_bounds__(CtaPlan<LGN>::T, 512 / CtaPlan<LGN>::T) spectr
             if (((affm >> m) & 1u) == 0u) {
                 v[m] = make_double2(v[m].x, -v[m].y);
             } else {
-                const double2 wk = SA_SPEC_WS ? ws[m] : __ldg(&tw[k]);
+                const double2 wk = __ldg(&tw[k]);  // only touched pairs: L1, not registers (5 CTAs / SM)
                 const double2 zk = v[m], zc = sm.buf[k == 0 ? 0 : kc];
                 double2 a = cta_split(zk, zc, wk);
                 double2 c = cta_split(zc, zk, k == 0 ? wn : make_double2(-wk.x, wk.y));  // W_L^{N-k} = -conj(W_L^k)
