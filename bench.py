@@ -157,7 +157,10 @@ def fft_flops_per_series(cfg, L):
 
 
 def ncu_traffic(cfg):
-    return _profile_json("ncu_traffic.json").get(cfg if isinstance(cfg, str) else f"config{cfg}")
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    capture (profiles/ncu_traffic.json, tools/ncu_record.py)."""
+    t = _profile_json("ncu_traffic.json").get(cfg if isinstance(cfg, str) else f"config{cfg}")
+    return t.get("value") if isinstance(t, dict) else t
 
 
 def build_sha16() -> str | None:
