@@ -511,6 +511,15 @@ def run_sweep(args, rank, world, local_rank, dist_ok):
     # first, each to the least-loaded stream by points) and overlap.
     K = max(1, args.sweep_streams)
     side = [torch.cuda.Stream(device=dev) for _ in range(K)]
+    # Datasets of less than one wave of rows are latency bound (one warp runs
+    # a row's whole chain): they go first, longest rows first, so their
+    # latency overlaps the large datasets instead of forming the step's tail.
+    wave = torch.cuda.get_device_properties(dev).multi_processor_count * 12
+    order = sorted(range(len(work)), key=lambda k: (work[k][2].shape[0] >= wave, -work[k][2].shape[1]
+                                                    if work[k][2].shape[0] < wave else -work[k][2].numel()))
+    if env_int("SA_SWEEP_ORDER", 1) == 0:
+        order = list(range(len(work)))
+    work = [work[k] for k in order]
     load = [0] * K
     assign = []
     for pipe, hx, x, out, low in work:

@@ -82,6 +82,16 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+// TMA 1-D bulk copy shared -> global (bulk-group completion).  The issuing
+// thread waits for the source reads (wait_read) before the buffer is reused.
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
@@ -108,7 +118,8 @@ __host__ __device__ inline Layout make_layout(int lcap, int ns, int small_words,
 
 // Dynamic shared memory shared by the CTA after the warps' slices: numpy's
 // ziggurat fast-path table and the adaptive-lockstep key slots (2 x OR, AND).
-constexpr size_t kCtaShared = 256 * sizeof(ZigEntry) + 4 * sizeof(unsigned long long);
+constexpr int kMaxSyncGroups = 4;
+constexpr size_t kCtaShared = 256 * sizeof(ZigEntry) + 4 * kMaxSyncGroups * sizeof(unsigned long long);
 
 // ------------------------------------------------------------ the kernel
 // GMEM: the row buffers live in p.gbuf (long series); the shared-memory
@@ -142,16 +153,26 @@ __global__ void __launch_bounds__(384) chain_kernel(const __grid_constant__ Chai
 
     if (lane == 0) mbar_init(bar, 1);
     __syncwarp();
-    // adaptive lockstep: OR / AND of the rows' gate keys per row iteration
+    // lockstep groups: warp w belongs to group w % G (G = 4: one group per
+    // SM sub-partition); a group's barrier is named barrier 1 + group
+    const int G = (p.sync_groups > 1 && p.sync_groups <= kMaxSyncGroups && nw % p.sync_groups == 0) ? p.sync_groups : 1;
+    const int grp = wid % G;
+    const uint32_t gthreads = (uint32_t)(nw / G) * 32u;
+    // adaptive lockstep: OR / AND of the group's gate keys per row iteration
     // (double-buffered by iteration parity)
-    unsigned long long* s_kor = reinterpret_cast<unsigned long long*>(zs + 256);
-    unsigned long long* s_kand = s_kor + 2;
-    if (threadIdx.x < 2) {
-        s_kor[threadIdx.x] = 0ull;
-        s_kand[threadIdx.x] = ~0ull;
+    unsigned long long* s_kor = reinterpret_cast<unsigned long long*>(zs + 256) + 2 * grp;
+    unsigned long long* s_kand = s_kor + 2 * kMaxSyncGroups;
+    if (threadIdx.x < 2 * kMaxSyncGroups) {
+        reinterpret_cast<unsigned long long*>(zs + 256)[threadIdx.x] = 0ull;
+        reinterpret_cast<unsigned long long*>(zs + 256)[2 * kMaxSyncGroups + threadIdx.x] = ~0ull;
     }
     __syncthreads();
+    auto group_sync = [&]() {
+        if (G == 1) __syncthreads();
+        else asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(gthreads) : "memory");
+    };
     int it = 0;
+    bool pend_store = false;  // a bulk store of this warp's row is in flight
     uint32_t phase = 0;
     uint32_t flags = 0;
     const int r = p.repeat_r;
@@ -166,6 +187,11 @@ __global__ void __launch_bounds__(384) chain_kernel(const __grid_constant__ Chai
         const int64_t in_row = (active ? row : 0) / r;
         const double* src = p.in + in_row * (int64_t)p.len_in;
         uint64_t fire_lo = 0;  // fire bits of stages 0..63
+        if (!GMEM && pend_store) {  // the previous row's bulk store has read its buffer
+            if (lane == 0) bulk_wait_read();
+            pend_store = false;
+            __syncwarp();
+        }
         if (active) {
         // 1. stage the input row
         if (p.bulk_in) {
@@ -218,11 +244,11 @@ __global__ void __launch_bounds__(384) chain_kernel(const __grid_constant__ Chai
                 atomicOr(&s_kor[b], (unsigned long long)(fire_lo & p.uni_mask));
                 atomicAnd(&s_kand[b], (unsigned long long)(fire_lo & p.uni_mask));
             }
-            if (threadIdx.x == 0) {  // reset the other parity's slots for the next iteration
+            if (wid == grp && lane == 0) {  // reset the other parity's slots for the next iteration
                 s_kor[b ^ 1] = 0ull;
                 s_kand[b ^ 1] = ~0ull;
             }
-            __syncthreads();
+            group_sync();
             uniform = p.uni_mask != ~0ull && (s_kor[b] & ~s_kand[b]) == 0ull;
             ++it;
         }
@@ -232,7 +258,7 @@ __global__ void __launch_bounds__(384) chain_kernel(const __grid_constant__ Chai
         int L = p.len_in;
         double2* held = nullptr;  // the row's half spectrum between fused spectral stages
         for (int j = 0; j < p.ns; ++j) {
-            if (!uniform && j && ((p.sync_mask >> j) & 1ull)) __syncthreads();  // j = 0: the check above
+            if (!uniform && j && ((p.sync_mask >> j) & 1ull)) group_sync();  // j = 0: the check above
             if (!active || !((fire_lo >> j) & 1ull)) continue;
             const DevStage& st = p.st[j];
             const uint64_t* c = scache + 6 * j;
@@ -292,6 +318,15 @@ __global__ void __launch_bounds__(384) chain_kernel(const __grid_constant__ Chai
         // 5. write the row
         if (!active) continue;
         double* dst = p.out + row * (int64_t)p.len_out;
+        if (!GMEM && (p.len_out & 1) == 0 && ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0)) {
+            // one TMA bulk store of the row: the generic-proxy writes are made
+            // visible to the async proxy, then lane 0 issues it
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) bulk_s2g(dst, cur, 8u * (uint32_t)p.len_out);
+            pend_store = true;
+            continue;
+        }
         if ((p.len_out & 1) == 0 && ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0)) {
             const double2* c2 = reinterpret_cast<const double2*>(cur);
             double2* d2 = reinterpret_cast<double2*>(dst);
@@ -301,6 +336,7 @@ __global__ void __launch_bounds__(384) chain_kernel(const __grid_constant__ Chai
         }
         __syncwarp();
     }
+    if (!GMEM && pend_store && lane == 0) bulk_wait_all();
     if (flags && lane == 0) atomicOr(p.flags, flags);
 }
 
@@ -856,16 +892,23 @@ __global__ void __launch_bounds__(CtaPlan<LGN>::T, 640 / CtaPlan<LGN>::T) spectr
         // stages and the fold -- on both bins of the pair, in this thread (the
         // Nyquist bin N pairs with k = 0).  Same formulas and pins as
         // rfft_any / _apply / irfft_any; untouched bins skip rounding-level work.
-        uint32_t affm = 0;  // bit m: pair of bin t + m T touched by a fired stage
+        // bit m: pair of bin t + m T touched by a fired stage.  Bins [pos, end)
+        // hold k = t + m T for m in [ceil((pos - t) / T), ceil((end - t) / T))
+        // and kc = N - k for m in [ceil((N + 1 - end - t) / T), ceil((N + 1 - pos - t) / T))
+        // (floor division by the power of two T: arithmetic shift)
+        constexpr int LGT = LGN - 3;
+        auto mbits = [&](int lo, int hi) -> uint32_t {  // m in [ceil(lo / T), ceil(hi / T)) within 0..7
+            int a = (lo + T - 1) >> LGT, b = (hi + T - 1) >> LGT;
+            a = a < 0 ? 0 : (a > 8 ? 8 : a);
+            b = b < 0 ? 0 : (b > 8 ? 8 : b);
+            return ((1u << b) - 1u) & ~((1u << a) - 1u);
+        };
+        uint32_t affm = 0;
         for (uint64_t f = fire; f; f &= f - 1) {
             const int j = __ffsll((long long)f) - 1;
             const int pos = s_tab[cb][j].pos;
             const int end = p.st[j].op == SA_OP_FREQ_MASK ? pos + (int)p.st[j].i[0] : pos + 1;
-#pragma unroll
-            for (int m = 0; m < 8; ++m) {
-                const int k = t + m * T, kc = N - k;
-                affm |= ((k >= pos && k < end) || (kc >= pos && kc < end)) ? (1u << m) : 0u;
-            }
+            affm |= mbits(pos - t, end - t) | mbits(N + 1 - end - t, N + 1 - pos - t);
         }
 #pragma unroll
         for (int m = 0; m < 8; ++m) {
@@ -1550,6 +1593,7 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
     plan->warps = warps;
     plan->smem = (size_t)per_warp * warps + kCtaShared;
     p.sync_every = ns > 1 ? env_int("SA_SYNC_EVERY", 4) : 0;
+    p.sync_groups = env_int("SA_SYNC_GROUPS", 1);
     // barrier placement (bit j: barrier before stage j).  Policy 0: every
     // `sync_every` stages; policy 1: before every stage whose operator is
     // expensive (op_cost >= threshold) and every `sync_every` cheap stages.

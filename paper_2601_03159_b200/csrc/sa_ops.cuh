@@ -34,6 +34,7 @@ struct ChainParams {
     int32_t len_in, len_out;
     int32_t lcap, small_words, iscr_words, bulk_in;
     int32_t sync_every, key_bits;  // sync_every != 0: barriers on; fire-pattern key width
+    int32_t sync_groups, pad0;     // lockstep groups of warps (warp w in group w % sync_groups)
     uint64_t sync_mask;            // bit j: CTA barrier before stage j
     uint64_t uni_mask;             // gates compared across the CTA's rows; all equal -> no in-row barriers
     const int32_t* order;          // row schedule (nullptr: identity)
@@ -845,9 +846,78 @@ __device__ __forceinline__ bool op_pool(const DevStage& st, double*& cur, int L,
 // outputs (t + 32q) as independent chains; chunks whose taps stay inside
 // the series skip the edge clamp.  Per output the taps are summed in order
 // k = 0..S-1 exactly as before.
+// Seven taps (the configs' size): lane pairs.  Each lane computes outputs
+// t, t + 1 (t even) from five aligned 16-byte loads of x[t-4 .. t+5] (2.5
+// loads per output instead of 7), four pairs per lane per step (eight
+// independent accumulation chains); the <= 4 + 5 edge outputs whose taps
+// reach past the series take the clamped path.
+__device__ __forceinline__ void convolve7(const double* __restrict__ taps, const double* cur, double* oth, int L,
+                                          Warp& w, bool& bad) {
+    double c[7];
+#pragma unroll
+    for (int k = 0; k < 7; ++k) c[k] = taps[k];
+    const int tmax = L - 6;  // last interior pair start: t + 5 <= L - 1
+    const double2* c2 = reinterpret_cast<const double2*>(cur);
+    for (int t0 = 4; t0 <= tmax; t0 += 256) {
+        double acc[8];
+        double2 v[4][5];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int t = t0 + 2 * w.lane + 64 * q;
+            const int tl = t <= tmax ? t : 4;  // idle lanes read a valid pair
+#pragma unroll
+            for (int m = 0; m < 5; ++m) v[q][m] = c2[(tl - 4) / 2 + m];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            // x[t - 4 + i] for i = 0..9
+            const double x[10] = {v[q][0].x, v[q][0].y, v[q][1].x, v[q][1].y, v[q][2].x,
+                                  v[q][2].y, v[q][3].x, v[q][3].y, v[q][4].x, v[q][4].y};
+            double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+            for (int k = 0; k < 7; ++k) {
+                a0 = a0 + c[k] * x[1 + k];  // x[t + k - 3]
+                a1 = a1 + c[k] * x[2 + k];  // x[t + 1 + k - 3]
+            }
+            acc[2 * q] = a0;
+            acc[2 * q + 1] = a1;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int t = t0 + 2 * w.lane + 64 * q;
+            if (t <= tmax) {
+                reinterpret_cast<double2*>(oth)[t / 2] = make_double2(acc[2 * q], acc[2 * q + 1]);
+                bad |= nonfinite(acc[2 * q]) | nonfinite(acc[2 * q + 1]);
+            }
+        }
+    }
+    // edges: t in [0, 4) and t > last interior pair end
+    const int e0 = tmax >= 4 ? 4 + 2 * ((tmax - 4) / 2) + 2 : 0;  // first t after the interior pairs
+    const int lo_n = tmax >= 4 ? 4 : 0;
+    const int n_edge = lo_n + (L - e0);
+    for (int i = w.lane; i < n_edge; i += 32) {
+        const int t = i < lo_n ? i : e0 + (i - lo_n);
+        double a = 0.0;
+#pragma unroll
+        for (int k = 0; k < 7; ++k) {
+            int u = t + k - 3;
+            u = u < 0 ? 0 : (u > L - 1 ? L - 1 : u);
+            a = a + c[k] * cur[u];
+        }
+        oth[t] = a;
+        bad |= nonfinite(a);
+    }
+}
+
 __device__ __forceinline__ bool op_convolve(const DevStage& st, const double* aux, double*& cur, double*& oth, int L, Warp& w, bool& bad) {
     const double* taps = aux + st.aux_off;
     const int S = st.aux_len, h = S / 2;
+    if (S == 7 && ((reinterpret_cast<uintptr_t>(cur) | reinterpret_cast<uintptr_t>(oth)) & 15u) == 0) {
+        convolve7(taps, cur, oth, L, w, bad);
+        __syncwarp();
+        swapbuf(cur, oth);
+        return false;
+    }
     const int t_hi = L - S + h;  // outputs t in [h, t_hi] read only cur[0 .. L-1]
     for (int t0 = 0; t0 < L; t0 += 128) {
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
@@ -884,6 +954,9 @@ __device__ __forceinline__ bool op_convolve(const DevStage& st, const double* au
 }
 
 // BASELINE M5 SpeedWarp
+#ifndef SW_ILP
+#define SW_ILP 4
+#endif
 __device__ __forceinline__ bool op_speed_warp(const DevStage& st, WStream& s, double*& cur, double*& oth, int L, Warp& w, bool& bad) {
     const int K = (int)st.i[0];
     const double R = st.f[0];
@@ -926,10 +999,10 @@ __device__ __forceinline__ bool op_speed_warp(const DevStage& st, WStream& s, do
     int m = 0, sbm = sbt[0];
     int nb = K > 0 ? sbt[1] : 0x7fffffff;
     double bm = base[0], spm = speeds[0];
-    for (int t0 = w.lane; t0 < L; t0 += 128) {
-        double taus[4];
+    for (int t0 = w.lane; t0 < L; t0 += 32 * SW_ILP) {
+        double taus[SW_ILP];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < SW_ILP; ++q) {
             const int t = t0 + 32 * q;
             if (t < L) {
                 while (t >= nb) {
@@ -943,9 +1016,9 @@ __device__ __forceinline__ bool op_speed_warp(const DevStage& st, WStream& s, do
             const int tt = t < L ? t : L - 1;
             taus[q] = (tt == L - 1) ? (double)L - 1.0 : (bm + spm * (double)(tt - sbm)) * f;
         }
-        double ys[4];
+        double ys[SW_ILP];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < SW_ILP; ++q) {
             const double tau = taus[q];
             int j = (int)floor(tau);
             j = j < 0 ? 0 : (j > L - 2 ? L - 2 : j);
@@ -966,7 +1039,7 @@ __device__ __forceinline__ bool op_speed_warp(const DevStage& st, WStream& s, do
             ys[q] = y;
         }
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < SW_ILP; ++q) {
             const int t = t0 + 32 * q;
             if (t < L) {
                 oth[t] = ys[q];
