@@ -250,6 +250,34 @@ __device__ __forceinline__ void generic_pass(double2* __restrict__ src, double2*
     }
     __syncwarp();
     const int G = (H + 4) >> 2;  // output pairs u = 0 .. H, four per item
+    if (Q * G < 32) {
+        // few columns (small N, e.g. a prime length): one output pair per
+        // item keeps more lanes busy; each output accumulates over m in the
+        // same order as below, so the result is the same
+        for (int idx = lane; idx < Q * (H + 1); idx += 32) {
+            const int j = idx % Q, u = idx / Q;
+            const int k = j % Ns;
+            const double2 y0 = src[j];
+            double2 A = make_double2(0.0, 0.0), B = make_double2(0.0, 0.0);
+            int id = 0;
+            for (int m = 1; m <= H; ++m) {
+                const double2 sm = src[j + m * Q], dm = src[j + (R - m) * Q];
+                id += u;
+                id = id >= R ? id - R : id;
+                const double2 w = __ldg(&tw[id * tr]);
+                A.x = fma(sm.x, w.x, A.x);
+                A.y = fma(sm.y, w.x, A.y);
+                B.x = fma(dm.x, w.y, B.x);
+                B.y = fma(dm.y, w.y, B.y);
+            }
+            const int o = (j - k) * R + k;
+            const double re = y0.x + A.x, im = y0.y + A.y;
+            dst[o + u * Ns] = make_double2(re - B.y, im + B.x);
+            if (u) dst[o + (R - u) * Ns] = make_double2(re + B.y, im - B.x);
+        }
+        __syncwarp();
+        return;
+    }
     for (int idx = lane; idx < Q * G; idx += 32) {
         const int j = idx % Q, g0 = 4 * (idx / Q);
         const int k = j % Ns;

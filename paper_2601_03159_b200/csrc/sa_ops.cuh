@@ -953,10 +953,14 @@ __device__ __forceinline__ bool op_convolve(const DevStage& st, const double* au
     return false;
 }
 
-// BASELINE M5 SpeedWarp
-#ifndef SW_ILP
-#define SW_ILP 4
-#endif
+// BASELINE M5 SpeedWarp.  Two passes over the row: (1) warped positions
+// tau_t segment by segment (loop-free per element; written to `oth` as
+// scratch), (2) the interpolation of x at tau_t, written back in place
+// over tau_t by the same lane.
+__device__ __forceinline__ int seg_start(int m, int L, int K) {  // (m L + K) // (K + 1)
+    const int64_t num = (int64_t)m * L + K;
+    return num <= 0x7fffffff ? (int)((uint32_t)num / (uint32_t)(K + 1)) : (int)(num / (K + 1));
+}
 __device__ __forceinline__ bool op_speed_warp(const DevStage& st, WStream& s, double*& cur, double*& oth, int L, Warp& w, bool& bad) {
     const int K = (int)st.i[0];
     const double R = st.f[0];
@@ -964,69 +968,56 @@ __device__ __forceinline__ bool op_speed_warp(const DevStage& st, WStream& s, do
     const int segs = K + 1;
     double* speeds = w.small;
     double* base = w.small + segs;
+    int* sbt = reinterpret_cast<int*>(w.iscr);  // segment starts sb[m], m <= K; sb[K + 1] = L
     const double lo = 1.0, range = R - lo;
     for (int m = 0; m < segs; ++m) {
         double v = lo + range * next_double(s, w.lane);
         if (w.lane == 0) speeds[m] = v;
     }
+    for (int m = w.lane; m <= K + 1; m += 32) sbt[m] = m <= K ? seg_start(m, L, K) : L;
     __syncwarp();
     if (w.lane == 0) {
         double acc = 0.0;
         base[0] = 0.0;
         for (int m = 0; m < K; ++m) {
-            int sb = (int)(((int64_t)m * L + K) / segs);
-            int sn = (int)(((int64_t)(m + 1) * L + K) / segs);
-            acc = acc + speeds[m] * (double)(sn - sb);
+            acc = acc + speeds[m] * (double)(sbt[m + 1] - sbt[m]);
             base[m + 1] = acc;
         }
     }
     __syncwarp();
-    int* sbt = reinterpret_cast<int*>(w.iscr);  // segment starts sb[m], m <= K
-    for (int m = w.lane; m <= K; m += 32) sbt[m] = (int)(((int64_t)m * L + K) / segs);
-    __syncwarp();
-    // segment of t: m = #{q in 1..K : sb[q] <= t}; a lane's t only grows, so
-    // m is tracked incrementally, with the segment's start, base and speed and
-    // the next boundary cached in registers (usually one compare per element)
     const double f = ((double)L - 1.0) / ([&] {
         int mm = 0;
         while (mm < K && L - 1 >= sbt[mm + 1]) ++mm;
         return base[mm] + speeds[mm] * (double)(L - 1 - sbt[mm]);
     }());
+    // (1) tau_t = (base[m] + speed[m] (t - sb[m])) f on segment m; tau_{L-1} = L - 1
+    for (int m = 0; m <= K; ++m) {
+        const int sbm = sbt[m], sn = sbt[m + 1];
+        const double bm = base[m], spm = speeds[m];
+#pragma unroll 4
+        for (int t = sbm + w.lane; t < sn; t += 32) oth[t] = (t == L - 1) ? (double)L - 1.0 : (bm + spm * (double)(t - sbm)) * f;
+    }
+    __syncwarp();
+    // (2) Catmull-Rom (or linear) interpolation at tau_t, four per lane step
     const bool cubic = st.i[1] != 0;
-    // four elements per lane per step: their warped positions first (a short
-    // serial walk), then four independent interpolations (ILP for the long
-    // tau -> floor -> gather -> cubic chain)
-    int m = 0, sbm = sbt[0];
-    int nb = K > 0 ? sbt[1] : 0x7fffffff;
-    double bm = base[0], spm = speeds[0];
-    for (int t0 = w.lane; t0 < L; t0 += 32 * SW_ILP) {
-        double taus[SW_ILP];
+    const double x0 = cur[0], xl = cur[L - 1];
+    for (int t0 = w.lane; t0 < L; t0 += 128) {
+        double taus[4], ys[4];
 #pragma unroll
-        for (int q = 0; q < SW_ILP; ++q) {
+        for (int q = 0; q < 4; ++q) {
             const int t = t0 + 32 * q;
-            if (t < L) {
-                while (t >= nb) {
-                    ++m;
-                    sbm = nb;
-                    bm = base[m];
-                    spm = speeds[m];
-                    nb = m < K ? sbt[m + 1] : 0x7fffffff;
-                }
-            }
-            const int tt = t < L ? t : L - 1;
-            taus[q] = (tt == L - 1) ? (double)L - 1.0 : (bm + spm * (double)(tt - sbm)) * f;
+            taus[q] = oth[t < L ? t : L - 1];
         }
-        double ys[SW_ILP];
 #pragma unroll
-        for (int q = 0; q < SW_ILP; ++q) {
+        for (int q = 0; q < 4; ++q) {
             const double tau = taus[q];
             int j = (int)floor(tau);
-            j = j < 0 ? 0 : (j > L - 2 ? L - 2 : j);
+            j = max(0, min(j, L - 2));
             const double fr = tau - (double)j;
             const double p1 = cur[j], p2 = cur[j + 1];
             double y;
             if (cubic) {
-                const double p0 = cur[j > 0 ? j - 1 : 0], p3 = cur[j + 2 < L ? j + 2 : L - 1];
+                const double p0 = cur[max(j - 1, 0)], p3 = cur[min(j + 2, L - 1)];
                 const double a = ((-0.5 * p0 + 1.5 * p1) - 1.5 * p2) + 0.5 * p3;
                 const double b = ((p0 - 2.5 * p1) + 2.0 * p2) - 0.5 * p3;
                 const double c = -0.5 * p0 + 0.5 * p2;
@@ -1034,12 +1025,12 @@ __device__ __forceinline__ bool op_speed_warp(const DevStage& st, WStream& s, do
             } else {
                 y = p1 + (p2 - p1) * fr;
             }
-            y = (tau >= (double)(L - 1)) ? cur[L - 1] : y;
-            y = (tau <= 0.0) ? cur[0] : y;
+            y = (tau >= (double)(L - 1)) ? xl : y;
+            y = (tau <= 0.0) ? x0 : y;
             ys[q] = y;
         }
 #pragma unroll
-        for (int q = 0; q < SW_ILP; ++q) {
+        for (int q = 0; q < 4; ++q) {
             const int t = t0 + 32 * q;
             if (t < L) {
                 oth[t] = ys[q];
