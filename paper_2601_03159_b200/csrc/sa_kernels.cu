@@ -118,8 +118,7 @@ __host__ __device__ inline Layout make_layout(int lcap, int ns, int small_words,
 
 // Dynamic shared memory shared by the CTA after the warps' slices: numpy's
 // ziggurat fast-path table and the adaptive-lockstep key slots (2 x OR, AND).
-constexpr int kMaxSyncGroups = 4;
-constexpr size_t kCtaShared = 256 * sizeof(ZigEntry) + 4 * kMaxSyncGroups * sizeof(unsigned long long);
+constexpr size_t kCtaShared = 256 * sizeof(ZigEntry) + 4 * sizeof(unsigned long long);
 
 // ------------------------------------------------------------ the kernel
 // GMEM: the row buffers live in p.gbuf (long series); the shared-memory
@@ -153,24 +152,17 @@ __global__ void __launch_bounds__(384) chain_kernel(const __grid_constant__ Chai
 
     if (lane == 0) mbar_init(bar, 1);
     __syncwarp();
-    // lockstep groups: warp w belongs to group w % G (G = 4: one group per
-    // SM sub-partition); a group's barrier is named barrier 1 + group
-    const int G = (p.sync_groups > 1 && p.sync_groups <= kMaxSyncGroups && nw % p.sync_groups == 0) ? p.sync_groups : 1;
-    const int grp = wid % G;
-    const uint32_t gthreads = (uint32_t)(nw / G) * 32u;
-    // adaptive lockstep: OR / AND of the group's gate keys per row iteration
-    // (double-buffered by iteration parity)
-    unsigned long long* s_kor = reinterpret_cast<unsigned long long*>(zs + 256) + 2 * grp;
-    unsigned long long* s_kand = s_kor + 2 * kMaxSyncGroups;
-    if (threadIdx.x < 2 * kMaxSyncGroups) {
-        reinterpret_cast<unsigned long long*>(zs + 256)[threadIdx.x] = 0ull;
-        reinterpret_cast<unsigned long long*>(zs + 256)[2 * kMaxSyncGroups + threadIdx.x] = ~0ull;
+    // adaptive lockstep: OR / AND of the rows' gate keys per row iteration
+    // (double-buffered by iteration parity).  One group: the whole CTA
+    // (lockstep groups smaller than the CTA multiply the instruction working
+    // set -- measured 1.6-2.8x slower).
+    unsigned long long* s_kor = reinterpret_cast<unsigned long long*>(zs + 256);
+    unsigned long long* s_kand = s_kor + 2;
+    if (threadIdx.x < 2) {
+        s_kor[threadIdx.x] = 0ull;
+        s_kand[threadIdx.x] = ~0ull;
     }
     __syncthreads();
-    auto group_sync = [&]() {
-        if (G == 1) __syncthreads();
-        else asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(gthreads) : "memory");
-    };
     int it = 0;
     bool pend_store = false;  // a bulk store of this warp's row is in flight
     uint32_t phase = 0;
@@ -227,10 +219,10 @@ __global__ void __launch_bounds__(384) chain_kernel(const __grid_constant__ Chai
         __syncwarp();
         // input finiteness (Batch invariant, core.py:104)
         {
-            bool bad = false;
+            Finite bad;
 #pragma unroll 4
-            for (int t = lane; t < p.len_in; t += 32) bad |= nonfinite(A[t]);
-            if (__any_sync(SA_FULL, bad)) flags |= SA_FLAG_NONFINITE;
+            for (int t = lane; t < p.len_in; t += 32) bad.chk(A[t]);
+            if (__any_sync(SA_FULL, bad.any())) flags |= SA_FLAG_NONFINITE;
         }
         }
         // 3. the chain (stage-major across the CTA when sync_every > 0).  When
@@ -244,21 +236,21 @@ __global__ void __launch_bounds__(384) chain_kernel(const __grid_constant__ Chai
                 atomicOr(&s_kor[b], (unsigned long long)(fire_lo & p.uni_mask));
                 atomicAnd(&s_kand[b], (unsigned long long)(fire_lo & p.uni_mask));
             }
-            if (wid == grp && lane == 0) {  // reset the other parity's slots for the next iteration
+            if (threadIdx.x == 0) {  // reset the other parity's slots for the next iteration
                 s_kor[b ^ 1] = 0ull;
                 s_kand[b ^ 1] = ~0ull;
             }
-            group_sync();
+            __syncthreads();
             uniform = p.uni_mask != ~0ull && (s_kor[b] & ~s_kand[b]) == 0ull;
             ++it;
         }
-        bool bad = false;  // per-lane: some stage output was non-finite
+        Finite bad;  // per-lane: some stage output was non-finite
         double* cur = A;
         double* oth = B;
         int L = p.len_in;
         double2* held = nullptr;  // the row's half spectrum between fused spectral stages
         for (int j = 0; j < p.ns; ++j) {
-            if (!uniform && j && ((p.sync_mask >> j) & 1ull)) group_sync();  // j = 0: the check above
+            if (!uniform && j && ((p.sync_mask >> j) & 1ull)) __syncthreads();  // j = 0: the check above
             if (!active || !((fire_lo >> j) & 1ull)) continue;
             const DevStage& st = p.st[j];
             const uint64_t* c = scache + 6 * j;
@@ -311,10 +303,10 @@ __global__ void __launch_bounds__(384) chain_kernel(const __grid_constant__ Chai
             }
             if (arith) {  // ops that do not fold the check into their writes
 #pragma unroll 4
-                for (int t = lane; t < L; t += 32) bad |= nonfinite(cur[t]);
+                for (int t = lane; t < L; t += 32) bad.chk(cur[t]);
             }
         }
-        if (__any_sync(SA_FULL, bad)) flags |= SA_FLAG_NONFINITE;
+        if (__any_sync(SA_FULL, bad.any())) flags |= SA_FLAG_NONFINITE;
         // 5. write the row
         if (!active) continue;
         double* dst = p.out + row * (int64_t)p.len_out;
@@ -838,8 +830,11 @@ __global__ void __launch_bounds__(256) spectral_draw_kernel(const __grid_constan
     }
 }
 
+#ifndef SA_SPEC_THREADS
+#define SA_SPEC_THREADS 640  // resident threads per SM the register budget targets
+#endif
 template <int LGN>
-__global__ void __launch_bounds__(CtaPlan<LGN>::T, 640 / CtaPlan<LGN>::T) spectral_cta_kernel(const __grid_constant__ ChainParams p,
+__global__ void __launch_bounds__(CtaPlan<LGN>::T, SA_SPEC_THREADS / CtaPlan<LGN>::T) spectral_cta_kernel(const __grid_constant__ ChainParams p,
                                                            const double2* __restrict__ tw,
                                                            const SpecDraw* __restrict__ draws) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -1593,7 +1588,6 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
     plan->warps = warps;
     plan->smem = (size_t)per_warp * warps + kCtaShared;
     p.sync_every = ns > 1 ? env_int("SA_SYNC_EVERY", 4) : 0;
-    p.sync_groups = env_int("SA_SYNC_GROUPS", 1);
     // barrier placement (bit j: barrier before stage j).  Policy 0: every
     // `sync_every` stages; policy 1: before every stage whose operator is
     // expensive (op_cost >= threshold) and every `sync_every` cheap stages.
