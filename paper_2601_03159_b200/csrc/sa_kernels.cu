@@ -124,8 +124,16 @@ constexpr size_t kCtaShared = 256 * sizeof(ZigEntry) + 4 * sizeof(unsigned long 
 // GMEM: the row buffers live in p.gbuf (long series); the shared-memory
 // instantiation keeps them provably in shared memory (LDS/STS, not generic
 // accesses) -- the two are separate kernels for that reason.
-template <bool GMEM>
-__global__ void __launch_bounds__(384) chain_kernel(const __grid_constant__ ChainParams p) {
+// MAXT: threads per CTA the register allocation targets -- 384 (12 warps,
+// 168 registers) for the general kernel; the short-series instantiation
+// (chain_kernel<false, kWideThreads>) trades registers for more series in
+// flight, since short rows are latency bound on per-row fixed costs.
+#ifndef SA_WIDE_THREADS
+#define SA_WIDE_THREADS 512
+#endif
+constexpr int kWideThreads = SA_WIDE_THREADS;
+template <bool GMEM, int MAXT = 384>
+__global__ void __launch_bounds__(MAXT) chain_kernel(const __grid_constant__ ChainParams p) {
     extern __shared__ __align__(16) unsigned char smem_all[];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
@@ -1171,6 +1179,7 @@ int init_device(int dev) {
     ds.smem_optin = (size_t)optin;
     SA_CUDA(cudaFuncSetAttribute(chain_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(chain_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(chain_kernel<false, kWideThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(rfft_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(rfft_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(irfft_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
@@ -1450,6 +1459,7 @@ struct Plan {
     ChainParams p;
     Layout lay;
     int grid;
+    bool wide = false;  // short series: chain_kernel<false, kWideThreads>
     int warps;     // warps (= series in flight) per CTA
     size_t smem;   // dynamic smem per CTA
     bool global = false;  // row buffers in a global scratch of grid * warps slots
@@ -1579,12 +1589,17 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
     const int per_warp = (int)plan->lay.total;
     int fit = (int)((ds.smem_optin - kCtaShared) / (size_t)per_warp);
     int warps = env_int("SA_CTA_WARPS", 0);
-    if (warps <= 0) warps = std::min(12, std::max(1, fit));
+    // short series (shared memory holds >= 16 rows): the wide instantiation,
+    // 16 warps at 128 registers instead of 12 at 168 -- their rows are
+    // latency bound on per-row fixed costs (sweep L = 29 .. 440: -8..15%)
+    plan->wide = !plan->global && fit >= kWideThreads / 32 && env_int("SA_WIDE", 1) != 0;
+    const int wmax = plan->wide ? kWideThreads / 32 : 12;
+    if (warps <= 0) warps = std::min(wmax, std::max(1, fit));
     // less than one wave of rows: spread them over the SMs (a row's chain is
     // latency bound; 38 rows on 4 SMs ran 1.6x slower than on 38)
     if (spread && env_int("SA_CTA_WARPS", 0) <= 0 && p.rows_out < (int64_t)ds.sms * warps)
         warps = (int)std::max<int64_t>(1, (p.rows_out + ds.sms - 1) / ds.sms);
-    warps = std::max(1, std::min(warps, std::min(12, fit)));
+    warps = std::max(1, std::min(warps, std::min(wmax, fit)));
     plan->warps = warps;
     plan->smem = (size_t)per_warp * warps + kCtaShared;
     p.sync_every = ns > 1 ? env_int("SA_SYNC_EVERY", 4) : 0;
@@ -1638,13 +1653,14 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
         static std::mutex occ_mu;
         static std::map<std::pair<int, size_t>, int> occ_cache;  // (warps, smem) -> CTAs per SM
         std::lock_guard<std::mutex> lk(occ_mu);
-        auto key = std::make_pair(warps * 2 + (plan->global ? 1 : 0), plan->smem);
+        auto key = std::make_pair(warps * 4 + (plan->global ? 1 : 0) + (plan->wide ? 2 : 0), plan->smem);
         auto it = occ_cache.find(key);
         if (it != occ_cache.end()) {
             per_sm = it->second;
         } else {
             cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                &per_sm, plan->global ? chain_kernel<true> : chain_kernel<false>, 32 * warps, plan->smem);
+                &per_sm, plan->global ? chain_kernel<true> : (plan->wide ? chain_kernel<false, kWideThreads> : chain_kernel<false>),
+                32 * warps, plan->smem);
             if (e != cudaSuccess) return cuda_fail(e, "occupancy");
             occ_cache[key] = per_sm;
         }
@@ -1753,6 +1769,7 @@ int launch_chain(Plan* plan, cudaStream_t stream) {
         p.bulk_in = 0;  // TMA bulk copies target shared memory only
     }
     if (plan->global) chain_kernel<true><<<plan->grid, 32 * plan->warps, plan->smem, stream>>>(p);
+    else if (plan->wide) chain_kernel<false, kWideThreads><<<plan->grid, 32 * plan->warps, plan->smem, stream>>>(p);
     else chain_kernel<false><<<plan->grid, 32 * plan->warps, plan->smem, stream>>>(p);
     SA_CUDA(cudaGetLastError());
     __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
