@@ -30,6 +30,10 @@ if len(sys.argv) > 1 and sys.argv[1] == "--child":
             import dataclasses
             c5 = bench_inputs.pipeline(5)
             pipe = Pipeline(stages=tuple(dataclasses.replace(st, probability=1.0) for st in c5.stages), master_seed=5)
+        elif name == "SWCONV":  # config 4's two working stages (no resize), any AB_L
+            pipe = Pipeline(stages=(SpeedWarp(3, 3.0), Convolve("hann", 7)), master_seed=3)
+        elif name == "CHAIN5":  # config 5's chain with length-scaled parameters, any AB_L
+            pipe = bench_inputs.sweep_pipeline(L, 5)
         elif name.startswith("REP"):  # REP<k>_<op>: k copies of one op (composition experiments)
             kk, op = name[3:].split("_", 1)
             pipe = Pipeline(stages=tuple(OPS[op] for _ in range(int(kk))), master_seed=1)
