@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(MAXT) chain_kernel(const __grid_constant__ Cha
                 bulk_g2s(A, src, in_bytes, bar);
             }
         } else {
-            for (int t = lane; t < p.len_in; t += 32) A[t] = src[t];
+            for (int t = lane; t < p.len_in; t += 32) A[t] = __ldcs(&src[t]);  // streaming: keep L2 for the row scratch
         }
         // 2. gate pre-pass (overlaps the bulk copy)
         for (int j0 = 0; j0 < p.ns; j0 += 32) {
