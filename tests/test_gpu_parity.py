@@ -636,3 +636,47 @@ def lower_single(aug, j):
     from paper_2601_03159_b200.pipeline import lower_stages
 
     return lower_stages((aug,), j)
+
+
+@pytest.mark.parametrize("L", [130, 200, 600])
+def test_short_series_instantiation_matches_oracle(monkeypatch, L):
+    """Short series run the 16-warp / 128-register instantiation of the chain
+    kernel (SA_WIDE=1, the default when 16 rows fit in shared memory): the
+    oracle and the 12-warp instantiation agree with it (bitwise for the exact
+    chain, within the spectral tolerance for config 5's length-scaled chain)."""
+    import torch
+
+    import bench_inputs as B
+
+    x = walks(2_000, L, 70 + L)
+    exact = _exact_chain(seed=8)
+    runs = {}
+    for wide in ("0", "1"):
+        monkeypatch.setenv("SA_WIDE", wide)
+        xt = torch.from_numpy(x).cuda()
+        runs[wide] = (exact.run_device(xt).cpu().numpy(), B.sweep_pipeline(L, 9).run_device(xt).cpu().numpy())
+    want = O.run_pipeline(exact, x)
+    for wide in ("0", "1"):
+        assert_bitwise(runs[wide][0], want, f"exact chain SA_WIDE={wide} L={L}")
+    # the spectral chain: the two instantiations run the same arithmetic
+    assert np.array_equal(runs["0"][1].view(np.uint64), runs["1"][1].view(np.uint64))
+
+
+@pytest.mark.parametrize("L", [1023, 1024])
+def test_output_rows_bulk_store_and_fallback(L):
+    """Even-length, 16-byte aligned output rows leave by one TMA bulk store;
+    odd lengths and misaligned outputs take the per-lane streaming stores.
+    Both agree with the oracle bitwise."""
+    import torch
+
+    pipe = _exact_chain(seed=11)
+    x = walks(700, L, 90 + L)
+    want = O.run_pipeline(pipe, x)
+    xt = torch.from_numpy(x).cuda()
+    got = pipe.run_device(xt).cpu().numpy()
+    assert_bitwise(got, want, f"L={L}")
+    # a misaligned output: a view starting one double into a larger buffer
+    big = torch.empty(want.size + 1, dtype=torch.float64, device="cuda")
+    out = big[1:].view(want.shape)
+    got2 = pipe.run_device(xt, out=out).cpu().numpy()
+    assert_bitwise(got2, want, f"misaligned out L={L}")
