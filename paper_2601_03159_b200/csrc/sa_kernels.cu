@@ -961,6 +961,243 @@ __global__ void __launch_bounds__(CtaPlan<LGN>::T, SA_SPEC_THREADS / CtaPlan<LGN
     if (__any_sync(SA_FULL, bad) && (t & 31) == 0) atomicOr(p.flags, SA_FLAG_NONFINITE);
 }
 
+// Gather-only chains (every stage SpeedWarp / Resize / Convolve / Rotate /
+// Reverse, e.g. BASELINE config 4) on a CTA per row.  The warp-per-row chain
+// kernel holds two row buffers per warp, so at L = 1,500 only 8 rows (8
+// warps) fit an SM and the gathers' dependent FP64 chains are latency bound.
+// Here the gates and SpeedWarp's speed draws come from a parallel pre-pass
+// (gather_draw_kernel: one thread per (row, stage), the stage's numpy stream
+// restated by SStream) and GT threads share each row: the same two buffers
+// per row, GT / 32 times the warps, and no RNG or lockstep code in the main
+// kernel (few registers).  Every operator's arithmetic is the chain kernel's
+// (same formulas, same order), so results are bitwise the same.
+constexpr int kGatherMaxSpeeds = 8;  // SpeedWarp n_speed_change <= 7
+#ifndef SA_GATHER_THREADS
+#define SA_GATHER_THREADS 128
+#endif
+constexpr int kGatherThreads = SA_GATHER_THREADS;  // threads per row
+struct GatherDraw {
+    double v[kGatherMaxSpeeds];  // SpeedWarp: speeds 1 + (R - 1) random()
+    int32_t fire;
+    int32_t pad[3];
+};
+__global__ void __launch_bounds__(256) gather_draw_kernel(const __grid_constant__ ChainParams p,
+                                                          GatherDraw* __restrict__ out) {
+    const int64_t total = p.rows_out * (int64_t)p.ns;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = i / p.ns;
+        const int j = (int)(i - row * p.ns);
+        const DevStage& st = p.st[j];
+        uint64_t k0, k1;
+        derive_key(p.seed, (uint64_t)st.index, (uint64_t)(p.offset + row), k0, k1);
+        SStream s;
+        s_init(s, k0, k1);
+        GatherDraw d;
+        d.fire = s_next_double(s) < st.prob ? 1 : 0;  // core.py:235
+        if (d.fire && st.op == SA_OP_SPEED_WARP) {
+            const int K = (int)st.i[0];
+            const double lo = 1.0, range = st.f[0] - lo;
+            for (int m = 0; m <= K && m < kGatherMaxSpeeds; ++m) d.v[m] = lo + range * s_next_double(s);
+        }
+        out[i] = d;
+    }
+}
+
+template <int GT>
+__global__ void __launch_bounds__(GT) gather_cta_kernel(const __grid_constant__ ChainParams p,
+                                                        const GatherDraw* __restrict__ draws) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int tid = threadIdx.x;
+    double* bufs = reinterpret_cast<double*>(smem);
+    double* sw_base = bufs + 2 * (size_t)p.lcap;  // SpeedWarp cumulative bases, then f
+    int32_t* sw_sb = reinterpret_cast<int32_t*>(sw_base + kGatherMaxSpeeds + 2);  // segment starts
+    GatherDraw* s_dr = reinterpret_cast<GatherDraw*>(sw_sb + kGatherMaxSpeeds + 8);  // this row's draws (16-B aligned)
+    Finite bad, bad2;  // two independent accumulation chains
+    for (int64_t row = blockIdx.x; row < p.rows_out; row += gridDim.x) {
+        double* cur = bufs;
+        double* oth = bufs + p.lcap;
+        int L = p.len_in;
+        const double* src = p.in + row * (int64_t)L;
+        if (((L & 1) | (reinterpret_cast<uintptr_t>(src) & 15u)) == 0) {
+            const double2* s2 = reinterpret_cast<const double2*>(src);
+            for (int t = tid; t < L / 2; t += GT) {
+                const double2 v = __ldcs(&s2[t]);
+                reinterpret_cast<double2*>(cur)[t] = v;
+                bad.chk(v.x);  // Batch invariant (core.py:104)
+                bad2.chk(v.y);
+            }
+        } else {
+            for (int t = tid; t < L; t += GT) {
+                const double v = __ldcs(&src[t]);
+                cur[t] = v;
+                bad.chk(v);
+            }
+        }
+        {  // this row's gate / speed draws into shared memory (one L2 round trip, not one per stage)
+            const uint64_t* g = reinterpret_cast<const uint64_t*>(draws + row * p.ns);
+            uint64_t* d = reinterpret_cast<uint64_t*>(s_dr);
+            for (int i = tid; i < p.ns * (int)(sizeof(GatherDraw) / 8); i += GT) d[i] = __ldcs(&g[i]);
+        }
+        __syncthreads();
+        const GatherDraw* dr = s_dr;
+        for (int j = 0; j < p.ns; ++j) {
+            const DevStage& st = p.st[j];
+            if (!dr[j].fire) continue;  // uniform across the CTA
+            switch (st.op) {
+                case SA_OP_ROTATE:  // basic.py:70-71
+                    for (int t = tid; t < L; t += GT) cur[t] = -cur[t];
+                    __syncthreads();
+                    break;
+                case SA_OP_REVERSE:  // basic.py:113-114
+                    for (int t = tid; t < L; t += GT) oth[t] = cur[L - 1 - t];
+                    __syncthreads();
+                    swapbuf(cur, oth);
+                    break;
+                case SA_OP_RESIZE: {  // basic.py Resize: np.interp on linspace(0, L - 1, T)
+                    const int T = (int)st.i[0];
+                    if (T == L) break;
+                    const Linspace ls(0.0, (double)L - 1.0, T);
+                    for (int t = tid; t < T; t += GT) {
+                        const double v = ls.fast() ? interp_grid_fast(ls.at_fast(t), cur, L) : interp_grid(ls.at(t), cur, L);
+                        oth[t] = v;
+                        bad.chk(v);
+                    }
+                    __syncthreads();
+                    swapbuf(cur, oth);
+                    L = T;
+                    break;
+                }
+                case SA_OP_CONVOLVE: {  // BASELINE M4: y_t = sum_k taps[k] x[clip(t + k - S/2)], k in order
+                    const double* taps = p.aux + st.aux_off;
+                    const int S = st.aux_len, h = S / 2;
+                    if (S == 7 && L >= 16) {
+                        // lane pairs as convolve7: outputs t, t + 1 (t even) from five
+                        // aligned 16-byte loads of x[t - 4 .. t + 5]; edges clamped
+                        double c[7];
+#pragma unroll
+                        for (int k = 0; k < 7; ++k) c[k] = taps[k];
+                        const int tmax = L - 6;  // last interior pair start
+                        const double2* c2 = reinterpret_cast<const double2*>(cur);
+                        for (int t = 4 + 2 * tid; t <= tmax; t += 2 * GT) {
+                            double2 v[5];
+#pragma unroll
+                            for (int m = 0; m < 5; ++m) v[m] = c2[(t - 4) / 2 + m];
+                            const double x[10] = {v[0].x, v[0].y, v[1].x, v[1].y, v[2].x,
+                                                  v[2].y, v[3].x, v[3].y, v[4].x, v[4].y};
+                            double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+                            for (int k = 0; k < 7; ++k) {
+                                a0 = a0 + c[k] * x[1 + k];
+                                a1 = a1 + c[k] * x[2 + k];
+                            }
+                            reinterpret_cast<double2*>(oth)[t / 2] = make_double2(a0, a1);
+                            bad.chk(a0);
+                            bad2.chk(a1);
+                        }
+                        const int e0 = 4 + 2 * ((tmax - 4) / 2) + 2;
+                        for (int i = tid; i < 4 + (L - e0); i += GT) {
+                            const int t = i < 4 ? i : e0 + (i - 4);
+                            double a = 0.0;
+#pragma unroll
+                            for (int k = 0; k < 7; ++k) {
+                                int u = t + k - 3;
+                                u = u < 0 ? 0 : (u > L - 1 ? L - 1 : u);
+                                a = a + c[k] * cur[u];
+                            }
+                            oth[t] = a;
+                            bad.chk(a);
+                        }
+                        __syncthreads();
+                        swapbuf(cur, oth);
+                        break;
+                    }
+                    for (int t = tid; t < L; t += GT) {
+                        double acc = 0.0;
+                        if (t >= h && t + S - 1 - h <= L - 1) {
+                            const double* pa = cur + t - h;
+                            for (int k = 0; k < S; ++k) acc = acc + taps[k] * pa[k];
+                        } else {
+                            for (int k = 0; k < S; ++k) {
+                                int u = t + k - h;
+                                u = u < 0 ? 0 : (u > L - 1 ? L - 1 : u);
+                                acc = acc + taps[k] * cur[u];
+                            }
+                        }
+                        oth[t] = acc;
+                        bad.chk(acc);
+                    }
+                    __syncthreads();
+                    swapbuf(cur, oth);
+                    break;
+                }
+                case SA_OP_SPEED_WARP: {  // BASELINE M5 (the chain kernel's op_speed_warp)
+                    const int K = (int)st.i[0];
+                    if (K == 0 || st.f[0] == 1.0) break;
+                    const double* speeds = dr[j].v;
+                    for (int m = tid; m <= K + 1; m += GT) sw_sb[m] = m <= K ? seg_start(m, L, K) : L;
+                    __syncthreads();
+                    if (tid == 0) {
+                        double acc = 0.0;
+                        sw_base[0] = 0.0;
+                        for (int m = 0; m < K; ++m) {
+                            acc = acc + speeds[m] * (double)(sw_sb[m + 1] - sw_sb[m]);
+                            sw_base[m + 1] = acc;
+                        }
+                        int mm = 0;
+                        while (mm < K && L - 1 >= sw_sb[mm + 1]) ++mm;
+                        sw_base[kGatherMaxSpeeds] = ((double)L - 1.0) / (sw_base[mm] + speeds[mm] * (double)(L - 1 - sw_sb[mm]));
+                    }
+                    __syncthreads();
+                    const double f = sw_base[kGatherMaxSpeeds];
+                    for (int m = 0; m <= K; ++m) {  // warped positions, segment by segment
+                        const int sbm = sw_sb[m], sn = sw_sb[m + 1];
+                        const double bm = sw_base[m], spm = speeds[m];
+                        for (int t = sbm + tid; t < sn; t += GT)
+                            oth[t] = (t == L - 1) ? (double)L - 1.0 : (bm + spm * (double)(t - sbm)) * f;
+                    }
+                    __syncthreads();
+                    const bool cubic = st.i[1] != 0;
+                    const double x0 = cur[0], xl = cur[L - 1];
+                    for (int t = tid; t < L; t += GT) {
+                        const double tau = oth[t];
+                        int jj = (int)floor(tau);
+                        jj = max(0, min(jj, L - 2));
+                        const double fr = tau - (double)jj;
+                        const double p1 = cur[jj], p2 = cur[jj + 1];
+                        double y;
+                        if (cubic) {
+                            const double p0 = cur[max(jj - 1, 0)], p3 = cur[min(jj + 2, L - 1)];
+                            const double a = ((-0.5 * p0 + 1.5 * p1) - 1.5 * p2) + 0.5 * p3;
+                            const double b = ((p0 - 2.5 * p1) + 2.0 * p2) - 0.5 * p3;
+                            const double c = -0.5 * p0 + 0.5 * p2;
+                            y = ((a * fr + b) * fr + c) * fr + p1;
+                        } else {
+                            y = p1 + (p2 - p1) * fr;
+                        }
+                        y = (tau >= (double)(L - 1)) ? xl : y;
+                        y = (tau <= 0.0) ? x0 : y;
+                        oth[t] = y;  // same thread, same index as its tau
+                        bad.chk(y);
+                    }
+                    __syncthreads();
+                    swapbuf(cur, oth);
+                    break;
+                }
+                default: break;
+            }
+        }
+        double* dst = p.out + row * (int64_t)p.len_out;
+        if (((p.len_out & 1) | (reinterpret_cast<uintptr_t>(dst) & 15u) | (reinterpret_cast<uintptr_t>(cur) & 15u)) == 0) {
+            for (int t = tid; t < p.len_out / 2; t += GT)
+                __stcs(&reinterpret_cast<double2*>(dst)[t], reinterpret_cast<const double2*>(cur)[t]);
+        } else {
+            for (int t = tid; t < p.len_out; t += GT) __stcs(&dst[t], cur[t]);
+        }
+        __syncthreads();  // the buffers are reloaded for the next row
+    }
+    if (__any_sync(SA_FULL, bad.any() || bad2.any()) && (tid & 31) == 0) atomicOr(p.flags, SA_FLAG_NONFINITE);
+}
+
 // DTW (reference dtw.py:40-106) -----------------------
 struct DtwParams {
     const double* a;
@@ -1208,6 +1445,7 @@ int init_device(int dev) {
         SA_CUDA(cudaFuncSetAttribute(spectral_cta_kernel<11>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      optin - (int)fa.sharedSizeBytes));
     }
+    SA_CUDA(cudaFuncSetAttribute(gather_cta_kernel<kGatherThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(rfft_cta_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(rfft_cta_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(rfft_cta_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
@@ -1720,9 +1958,48 @@ const double2* spectral_cta_table(const Plan* plan) {
     return tw;
 }
 
+// Gather-only chain on a CTA per row (gather_cta_kernel): every stage a
+// SpeedWarp (n_speed_change <= 7), Resize, Convolve, Rotate or Reverse, no
+// Repeat, both row buffers in shared memory.  Returns its dynamic smem or 0.
+size_t gather_cta_smem(const Plan* plan) {
+    const ChainParams& p = plan->p;
+    if (plan->global || p.repeat_r != 1 || p.ns < 1 || p.ns > 64 || env_int("SA_GATHER_CTA", 1) == 0) return 0;
+    for (int j = 0; j < p.ns; ++j) {
+        const DevStage& st = p.st[j];
+        switch (st.op) {
+            case SA_OP_SPEED_WARP:
+                if (st.i[0] > kGatherMaxSpeeds - 1) return 0;
+                break;
+            case SA_OP_RESIZE: case SA_OP_CONVOLVE: case SA_OP_ROTATE: case SA_OP_REVERSE: break;
+            default: return 0;
+        }
+    }
+    const size_t smem = 16 * (size_t)p.lcap + 8 * (kGatherMaxSpeeds + 2) + 4 * (kGatherMaxSpeeds + 8) +
+                        sizeof(GatherDraw) * (size_t)p.ns;
+    return smem <= dev_state(current_device_id()).smem_optin ? smem : 0;
+}
+
 int launch_chain(Plan* plan, cudaStream_t stream) {
     ChainParams& p = plan->p;
     if (p.rows_out == 0) return SA_OK;
+    if (const size_t gsm = gather_cta_smem(plan)) {
+        DeviceState& dsg = dev_state(current_device_id());
+        int per_sm = 0;
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gather_cta_kernel<kGatherThreads>,
+                                                                      kGatherThreads, gsm);
+        if (e != cudaSuccess) return cuda_fail(e, "occupancy");
+        const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)dsg.sms * std::max(per_sm, 1), p.rows_out));
+        p.order = nullptr;
+        StreamScratch scr(stream);
+        GatherDraw* draws;
+        SA_CUDA(scr.alloc(&draws, sizeof(GatherDraw) * (size_t)(p.rows_out * p.ns)));
+        const int gd = (int)std::min<int64_t>((int64_t)dsg.sms * 8, (p.rows_out * p.ns + 255) / 256);
+        gather_draw_kernel<<<gd, 256, 0, stream>>>(p, draws);
+        gather_cta_kernel<kGatherThreads><<<grid, kGatherThreads, gsm, stream>>>(p, draws);
+        SA_CUDA(cudaGetLastError());
+        __atomic_add_fetch(&g_launches, 2, __ATOMIC_RELAXED);
+        return SA_OK;
+    }
     if (const double2* tw = spectral_cta_table(plan)) {
         const int64_t N = p.len_in / 2;
         const void* kern = N == 256 ? (const void*)spectral_cta_kernel<8>
