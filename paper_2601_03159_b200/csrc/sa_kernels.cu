@@ -1013,32 +1013,36 @@ __global__ void __launch_bounds__(GT) gather_cta_kernel(const __grid_constant__ 
     int32_t* sw_sb = reinterpret_cast<int32_t*>(sw_base + kGatherMaxSpeeds + 2);  // segment starts
     GatherDraw* s_dr = reinterpret_cast<GatherDraw*>(sw_sb + kGatherMaxSpeeds + 8);  // this row's draws (16-B aligned)
     Finite bad, bad2;  // two independent accumulation chains
-    for (int64_t row = blockIdx.x; row < p.rows_out; row += gridDim.x) {
-        double* cur = bufs;
-        double* oth = bufs + p.lcap;
-        int L = p.len_in;
-        const double* src = p.in + row * (int64_t)L;
-        if (((L & 1) | (reinterpret_cast<uintptr_t>(src) & 15u)) == 0) {
-            const double2* s2 = reinterpret_cast<const double2*>(src);
-            for (int t = tid; t < L / 2; t += GT) {
-                const double2 v = __ldcs(&s2[t]);
-                reinterpret_cast<double2*>(cur)[t] = v;
-                bad.chk(v.x);  // Batch invariant (core.py:104)
-                bad2.chk(v.y);
-            }
+    double* cur = bufs;
+    double* oth = bufs + p.lcap;
+    // rows (and their draws) arrive by cp.async: the next row is fetched into
+    // the free buffer while the current one is stored
+    const bool vec = ((p.len_in & 1) | (reinterpret_cast<uintptr_t>(p.in) & 15u)) == 0;
+    auto fetch = [&](int64_t r, double* dst) {
+        const double* src = p.in + r * (int64_t)p.len_in;
+        if (vec) {
+            for (int t = tid; t < p.len_in / 2; t += GT) cp_async16(dst + 2 * t, src + 2 * t);
         } else {
-            for (int t = tid; t < L; t += GT) {
-                const double v = __ldcs(&src[t]);
-                cur[t] = v;
-                bad.chk(v);
-            }
+            for (int t = tid; t < p.len_in; t += GT) cp_async8(dst + t, src + t);
         }
-        {  // this row's gate / speed draws into shared memory (one L2 round trip, not one per stage)
-            const uint64_t* g = reinterpret_cast<const uint64_t*>(draws + row * p.ns);
-            uint64_t* d = reinterpret_cast<uint64_t*>(s_dr);
-            for (int i = tid; i < p.ns * (int)(sizeof(GatherDraw) / 8); i += GT) d[i] = __ldcs(&g[i]);
-        }
+        const char* g = reinterpret_cast<const char*>(draws + r * p.ns);
+        for (int i = tid; i < p.ns * (int)(sizeof(GatherDraw) / 16); i += GT)
+            cp_async16(reinterpret_cast<char*>(s_dr) + 16 * i, g + 16 * i);
+        cp_async_commit();
+    };
+    if (blockIdx.x < p.rows_out) fetch(blockIdx.x, cur);
+    for (int64_t row = blockIdx.x; row < p.rows_out; row += gridDim.x) {
+        cp_async_wait_all();
         __syncthreads();
+        int L = p.len_in;
+        for (int t = tid; t < L / 2; t += GT) {  // Batch invariant (core.py:104)
+            const double2 v = reinterpret_cast<const double2*>(cur)[t];
+            bad.chk(v.x);
+            bad2.chk(v.y);
+        }
+        if (L & 1) {
+            if (tid == 0) bad.chk(cur[L - 1]);
+        }
         const GatherDraw* dr = s_dr;
         for (int j = 0; j < p.ns; ++j) {
             const DevStage& st = p.st[j];
@@ -1186,6 +1190,8 @@ __global__ void __launch_bounds__(GT) gather_cta_kernel(const __grid_constant__ 
                 default: break;
             }
         }
+        __syncthreads();  // the draws and the free buffer are no longer read
+        if (row + gridDim.x < p.rows_out) fetch(row + gridDim.x, oth);
         double* dst = p.out + row * (int64_t)p.len_out;
         if (((p.len_out & 1) | (reinterpret_cast<uintptr_t>(dst) & 15u) | (reinterpret_cast<uintptr_t>(cur) & 15u)) == 0) {
             for (int t = tid; t < p.len_out / 2; t += GT)
@@ -1193,7 +1199,7 @@ __global__ void __launch_bounds__(GT) gather_cta_kernel(const __grid_constant__ 
         } else {
             for (int t = tid; t < p.len_out; t += GT) __stcs(&dst[t], cur[t]);
         }
-        __syncthreads();  // the buffers are reloaded for the next row
+        swapbuf(cur, oth);  // the prefetched row (the loop head waits for it and barriers)
     }
     if (__any_sync(SA_FULL, bad.any() || bad2.any()) && (tid & 31) == 0) atomicOr(p.flags, SA_FLAG_NONFINITE);
 }
