@@ -211,6 +211,7 @@ struct FftGeo {
     int32_t packed;    // 1: even L, N = L/2 (real input viewed as complex)
     int32_t npass;
     int32_t blue;      // 1: Bluestein
+    int32_t oddreal;   // 1: odd composite L on the paired-column real transform (rfft_any)
     int16_t radix[SA_FFT_MAXPASS];
     int32_t M, mpass;  // Bluestein convolution length and its radix plan
     int16_t mradix[16];
@@ -230,20 +231,32 @@ struct FftGeo {
 // `src` (this pass's input is scratch afterwards); step 2 accumulates four
 // output pairs per work item over the folded column, cos / sin exact from the
 // W_L table (index m u mod R kept incrementally).
-__device__ __forceinline__ void generic_pass(double2* __restrict__ src, double2* __restrict__ dst, int N, int Ns,
-                                             int R, const double2* __restrict__ tw, int L, int lane) {
-    const int Q = N / R;
-    const int ts = L / N;  // W_N stride in the W_L table
+//
+// Q columns of R points; tsa = L / (Ns R), the W_{Ns R} stride in the W_L
+// table (0: the columns arrive twiddled).  hl >= 0 (the last pass of the
+// odd-length real transform, rfft_any): only the columns j <= (Ns - 1) / 2 are
+// present, and an output index above hl = (L - 1) / 2 is stored as the
+// conjugate at L - index (the spectrum of a real series is Hermitian; the
+// mirrors are the columns Ns - j that were left out).
+__device__ __forceinline__ void generic_pass(double2* __restrict__ src, double2* __restrict__ dst, int Q, int Ns,
+                                             int R, const double2* __restrict__ tw, int L, int lane, int tsa,
+                                             int hl) {
     const int tr = L / R;  // W_R stride
-    const int a = N / (Ns * R);
     const int H = (R - 1) >> 1;
+    auto put = [&](int i, double re, double im) {
+        if (hl >= 0 && i > hl) {
+            i = L - i;
+            im = -im;
+        }
+        dst[i] = make_double2(re, im);
+    };
     for (int idx = lane; idx < Q * H; idx += 32) {
         const int j = idx % Q, m = 1 + idx / Q;
-        const int ka = (j % Ns) * a;  // < N / R
+        const int ka = (j % Ns) * tsa;  // exponents r ka < L: no reduction
         double2 y1 = src[j + m * Q], y2 = src[j + (R - m) * Q];
-        if (ka) {  // exponents r ka < R * (N / R): no reduction
-            y1 = cmul(y1, __ldg(&tw[m * ka * ts]));
-            y2 = cmul(y2, __ldg(&tw[(R - m) * ka * ts]));
+        if (ka) {
+            y1 = cmul(y1, __ldg(&tw[m * ka]));
+            y2 = cmul(y2, __ldg(&tw[(R - m) * ka]));
         }
         src[j + m * Q] = cadd(y1, y2);
         src[j + (R - m) * Q] = csub(y1, y2);
@@ -272,8 +285,8 @@ __device__ __forceinline__ void generic_pass(double2* __restrict__ src, double2*
             }
             const int o = (j - k) * R + k;
             const double re = y0.x + A.x, im = y0.y + A.y;
-            dst[o + u * Ns] = make_double2(re - B.y, im + B.x);
-            if (u) dst[o + (R - u) * Ns] = make_double2(re + B.y, im - B.x);
+            put(o + u * Ns, re - B.y, im + B.x);
+            if (u) put(o + (R - u) * Ns, re + B.y, im - B.x);
         }
         __syncwarp();
         return;
@@ -310,8 +323,8 @@ __device__ __forceinline__ void generic_pass(double2* __restrict__ src, double2*
             if (u > H) break;
             const double re = y0.x + A[c].x, im = y0.y + A[c].y;
             // -i * (-B) = (-B.y, B.x) for V[u]; its negation for V[R - u]
-            dst[o + u * Ns] = make_double2(re - B[c].y, im + B[c].x);
-            if (u) dst[o + (R - u) * Ns] = make_double2(re + B[c].y, im - B[c].x);
+            put(o + u * Ns, re - B[c].y, im + B[c].x);
+            if (u) put(o + (R - u) * Ns, re + B[c].y, im - B[c].x);
         }
     }
     __syncwarp();
@@ -320,9 +333,34 @@ __device__ __forceinline__ void generic_pass(double2* __restrict__ src, double2*
 // The Stockham passes of an N-point plan (radix list `radix`, npass passes)
 // over a table of W_L (N | L); data in a, b is scratch; returns the buffer
 // holding the result.
-template <bool R16 = false>
+//
+// real_last (odd composite L = P q, P the last radix; rfft_any's paired-column
+// real transform): N = (P + 1) / 2 * q, the passes before the last leave the
+// q-point transforms Z_c of the column pairs z_c[m] = x[2c + m P] + i x[2c + 1
+// + m P]; real_unpack separates and twiddles them into the columns j <= (q -
+// 1) / 2 of the last pass, which then runs on half the columns.
+__device__ __forceinline__ void real_unpack(const double2* __restrict__ Z, double2* __restrict__ Y, int P, int q,
+                                            const double2* __restrict__ tw, int lane) {
+    const int Pp = (P + 1) >> 1, Qh = (q + 1) >> 1;
+    for (int idx = lane; idx < Pp * Qh; idx += 32) {
+        const int c = idx / Qh, j = idx - c * Qh;
+        const double2 zj = Z[c * q + j], zc = Z[c * q + (j ? q - j : 0)];
+        // F_2c = (Z[j] + conj Z[q - j]) / 2, F_2c+1 = (Z[j] - conj Z[q - j]) / 2i
+        const double2 fe = make_double2(0.5 * (zj.x + zc.x), 0.5 * (zj.y - zc.y));
+        const double2 fo = make_double2(0.5 * (zj.y + zc.y), -0.5 * (zj.x - zc.x));
+        const int r = 2 * c;
+        Y[j + r * Qh] = (r * j) ? cmul(fe, __ldg(&tw[r * j])) : fe;  // W_L^{r j}, r j < L
+        if (r + 1 < P) Y[j + (r + 1) * Qh] = j ? cmul(fo, __ldg(&tw[(r + 1) * j])) : fo;
+    }
+    __syncwarp();
+}
+
+// ODD: the odd-length real transform is compiled in (the chain kernel keeps it
+// out of the instantiation that runs the even lengths -- its code generation
+// is sensitive to everything inlined into it).
+template <bool R16 = false, bool ODD = true>
 __device__ __forceinline__ double2* fft_passes(double2* a, double2* b, int N, int npass, const int16_t* radix,
-                                               const double2* tw, int L, int lane) {
+                                               const double2* tw, int L, int lane, bool real_last = false) {
     int Ns = 1;
     double2* src = a;
     double2* dst = b;
@@ -344,7 +382,17 @@ __device__ __forceinline__ double2* fft_passes(double2* a, double2* b, int N, in
             carry = out;
             lns += lr;
         } else {
-            generic_pass(src, dst, N, Ns, R, tw, L, lane);
+            int Qc = N / R, tsa = L / (Ns * R), hl = -1;
+            if (ODD && real_last && p == npass - 1) {  // Ns = q here
+                real_unpack(src, dst, R, Ns, tw, lane);
+                double2* t = src;
+                src = dst;
+                dst = t;
+                Qc = (Ns + 1) >> 1;
+                tsa = 0;
+                hl = (L - 1) >> 1;
+            }
+            generic_pass(src, dst, Qc, Ns, R, tw, L, lane, tsa, hl);
         }
         Ns *= R;
         double2* t = src;
@@ -361,13 +409,13 @@ __device__ __forceinline__ double2* bluestein(double2* a, double2* b, const FftG
     const int N = g.N, M = g.M;
     for (int n = lane; n < M; n += 32) b[n] = n < N ? cmul(a[n], __ldg(&g.chirp[n])) : make_double2(0.0, 0.0);
     __syncwarp();
-    double2* Y = fft_passes(b, a, M, g.mpass, g.mradix, g.twM, M, lane);
+    double2* Y = fft_passes<false, false>(b, a, M, g.mpass, g.mradix, g.twM, M, lane);
     for (int k = lane; k < M; k += 32) {
         const double2 v = cmul(Y[k], __ldg(&g.bfft[k]));
         Y[k] = make_double2(v.x, -v.y);
     }
     __syncwarp();
-    double2* Z = fft_passes(Y, Y == a ? b : a, M, g.mpass, g.mradix, g.twM, M, lane);
+    double2* Z = fft_passes<false, false>(Y, Y == a ? b : a, M, g.mpass, g.mradix, g.twM, M, lane);
     const double inv = 1.0 / (double)M;
     for (int k = lane; k < N; k += 32) {
         const double2 z = Z[k];
@@ -397,12 +445,16 @@ __device__ __forceinline__ bool is_fft_512(const FftGeo& g, int L) {
 }
 
 // FIN (irfft of the fft_512 plan only): see fft_512.
-template <bool BLUE = true, bool R16 = false, bool FIN = false>
+template <bool BLUE = true, bool R16 = false, bool FIN = false, bool ODD = true>
 __device__ __forceinline__ double2* fft_any(double2* a, double2* b, const FftGeo& g, const double2* tw, int L,
                                             int lane, bool* fin_bad_out = nullptr) {
     if (BLUE && g.blue) return bluestein(a, b, g, lane);
     if (is_fft_512(g, L)) return fft_512<FIN>(a, b, tw, lane, fin_bad_out);
-    return fft_passes<R16>(a, b, g.N, g.npass, g.radix, tw, L, lane);
+    // oddreal: a holds the (P + 1) / 2 * q packed column pairs (rfft_any)
+    const bool odd = ODD && g.oddreal;
+    const int P = odd ? g.radix[g.npass - 1] : 1;
+    const int N = odd ? ((P + 1) >> 1) * (g.N / P) : g.N;
+    return fft_passes<R16, ODD>(a, b, N, g.npass, g.radix, tw, L, lane, odd);
 }
 
 // rfft split X[k] = E[k] + W_L^k O[k] from Z[k], Z[M - k] (rfft_any).
@@ -424,12 +476,64 @@ __device__ __forceinline__ double2 cta_fold(double2 xk, double2 xc, double2 w, b
     return make_double2(er - o.y, -(ei + o.x));
 }
 
+// Odd composite L = P q (P the plan's last radix): the P decimated series
+// x[r + m P] are real, so they are transformed two at a time, z_c[m] =
+// x[2c + m P] + i x[2c + 1 + m P] (the last one alone), laid out as
+// u[c + m (P + 1) / 2] for the plan's first passes; the last pass separates
+// the pairs and runs on half the columns (fft_passes).
+__device__ __forceinline__ void oddreal_pack(const double* __restrict__ x, double2* __restrict__ u, int L, int P,
+                                          int lane) {
+    const int Pp = (P + 1) >> 1, Np = Pp * (L / P);
+    for (int n = lane; n < Np; n += 32) {
+        const int m = n / Pp, c = n - m * Pp;
+        const int i = 2 * c + m * P;
+        u[n] = make_double2(x[i], 2 * c + 1 < P ? x[i + 1] : 0.0);
+    }
+    __syncwarp();
+}
+// x = irfft(X) through ONE forward real transform: h[k] = Re X[k] - Im X[k]
+// over the Hermitian completion (h[L - k] = Re X[k] + Im X[k]) is real; its
+// transform H has Re H[t] = sum_k Re X[k] cos(2 pi k t / L) and Im H[t] =
+// sum_k Im X[k] sin(2 pi k t / L), so L x[t] = Re H[t] - Im H[t] and
+// L x[L - t] = Re H[t] + Im H[t].
+__device__ __forceinline__ void oddreal_fold(const double2* __restrict__ X, double* __restrict__ h, int L, int lane) {
+    for (int k = lane; k <= L / 2; k += 32) {
+        const double2 v = X[k];
+        if (k == 0) {
+            h[0] = v.x;
+        } else {
+            h[k] = v.x - v.y;
+            h[L - k] = v.x + v.y;
+        }
+    }
+    __syncwarp();
+}
+__device__ __forceinline__ bool fin_bad(double v);
+__device__ __forceinline__ bool oddreal_unfold(const double2* __restrict__ H, double* __restrict__ out, int L,
+                                            int lane) {
+    const double s = 1.0 / (double)L;
+    bool b = false;
+    for (int t = lane; t <= L / 2; t += 32) {
+        const double2 hv = H[t];
+        const double v0 = (t ? hv.x - hv.y : hv.x) * s;
+        out[t] = v0;
+        b |= fin_bad(v0);
+        if (t) {
+            const double v1 = (hv.x + hv.y) * s;
+            out[L - t] = v1;
+            b |= fin_bad(v1);
+        }
+    }
+    __syncwarp();
+    return b;
+}
+
 // rfft of the real series x (length L, in buffer xa) -> X[0 .. L/2]
 // (complex, bins = L/2 + 1).  xb is scratch of the same capacity (>= 2L + 2
 // doubles for odd L).  Returns the buffer holding X; the other is free.
 // split == false (even L only): return the packed M-point transform Z itself
 // (the caller splits the bin pairs it needs, see op_spectral).
-template <bool BLUE = true, bool R16 = false>
+template <bool BLUE = true, bool R16 = false, bool ODD = true>
 __device__ __forceinline__ double2* rfft_any(double* xa, double* xb, int L, const FftGeo& g, const double2* tw,
                                             int lane, bool split = true) {
     double2* za = reinterpret_cast<double2*>(xa);
@@ -437,13 +541,15 @@ __device__ __forceinline__ double2* rfft_any(double* xa, double* xb, int L, cons
     // odd L: complexify into xb and take the N = L transform; even L: view
     // the real series as N = L/2 complex points (one call site either way,
     // to keep the FFT's code emitted once)
-    if (!g.packed) {
+    if (ODD && g.oddreal) {
+        oddreal_pack(xa, zb, L, g.radix[g.npass - 1], lane);
+    } else if (!g.packed) {
         for (int n = lane; n < L; n += 32) zb[n] = make_double2(xa[n], 0.0);
         __syncwarp();
     }
     double2* s0 = g.packed ? za : zb;
     double2* d0 = g.packed ? zb : za;
-    double2* Z = fft_any<BLUE, R16>(s0, d0, g, tw, L, lane);  // one call site: the FFT is emitted once
+    double2* Z = fft_any<BLUE, R16, false, ODD>(s0, d0, g, tw, L, lane);  // one call site: the FFT is emitted once
     if (!g.packed) {
         if (lane == 0) Z[0].y = 0.0;
         __syncwarp();
@@ -492,11 +598,14 @@ __device__ __forceinline__ bool fin_bad(double v) {  // exponent all ones: inf o
 // scaling loop, so callers need no separate pass over the row.
 // folded == true (even L only): `other` already holds the folded M points
 // (the conjugated inverse-FFT input); X is scratch.
-template <bool BLUE = true, bool R16 = false>
+template <bool BLUE = true, bool R16 = false, bool ODD = true>
 __device__ __forceinline__ double* irfft_any(double2* X, double2* other, int L, const FftGeo& g, const double2* tw,
                                             int lane, bool* bad = nullptr, bool folded = false) {
     const int M = L >> 1;
     if (folded) {
+    } else if (ODD && g.oddreal) {
+        oddreal_fold(X, reinterpret_cast<double*>(other), L, lane);
+        oddreal_pack(reinterpret_cast<const double*>(other), X, L, g.radix[g.npass - 1], lane);
     } else if (!g.packed) {  // odd L: Hermitian completion, full transform, real part
         const int bins = L / 2 + 1;
         for (int k = lane; k < bins; k += 32) {
@@ -531,11 +640,19 @@ __device__ __forceinline__ double* irfft_any(double2* X, double2* other, int L, 
     }
     __syncwarp();
     bool fb = false;
-    double2* Z = fft_any<BLUE, R16, true>(other, X, g, tw, L, lane, &fb);  // one call site: the FFT is emitted once
+    const bool odd = ODD && g.oddreal;
+    double2* Z = fft_any<BLUE, R16, true, ODD>(odd ? X : other, odd ? other : X, g, tw, L, lane,
+                                              &fb);  // one call site: the FFT is emitted once
     if (g.packed && is_fft_512(g, L)) {  // scaled and checked by the last pass
         if (bad) *bad |= fb;
         __syncwarp();
         return reinterpret_cast<double*>(Z);
+    }
+    if (odd) {
+        double* out = reinterpret_cast<double*>(Z == X ? other : X);
+        const bool b = oddreal_unfold(Z, out, L, lane);
+        if (bad) *bad |= b;
+        return out;
     }
     if (!g.packed) {
         double* out = reinterpret_cast<double*>(Z == X ? other : X);

@@ -132,7 +132,10 @@ constexpr size_t kCtaShared = 256 * sizeof(ZigEntry) + 4 * sizeof(unsigned long 
 #define SA_WIDE_THREADS 512
 #endif
 constexpr int kWideThreads = SA_WIDE_THREADS;
-template <bool GMEM, int MAXT = 384>
+// ODD: odd composite lengths on the paired-column real transform
+// (sa_fft.cuh); a separate instantiation, so the kernel the even lengths run
+// is generated without that code (measured: inlining it cost config 5 1%).
+template <bool GMEM, int MAXT = 384, bool ODD = false>
 __global__ void __launch_bounds__(MAXT) chain_kernel(const __grid_constant__ ChainParams p) {
     extern __shared__ __align__(16) unsigned char smem_all[];
     const int lane = threadIdx.x & 31;
@@ -298,7 +301,7 @@ __global__ void __launch_bounds__(MAXT) chain_kernel(const __grid_constant__ Cha
                     const uint64_t later = (j + 1 < 64) ? (fire_lo >> (j + 1)) : 0;
                     const int nx = later ? j + 1 + __ffsll((long long)later) - 1 : p.ns;
                     const bool keep = nx < p.ns && is_spectral_op(p.st[nx].op) && !spectral_noop(p.st[nx]);
-                    arith = op_spectral(st, s, cur, oth, L, w, held, keep, bad);
+                    arith = op_spectral<ODD>(st, s, cur, oth, L, w, held, keep, bad);
                     break;
                 }
                 case SA_OP_TIME_WARP: arith = op_time_warp(st, s, cur, oth, L, w, flags, bad); break;
@@ -1423,6 +1426,9 @@ int init_device(int dev) {
     SA_CUDA(cudaFuncSetAttribute(chain_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(chain_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(chain_kernel<false, kWideThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(chain_kernel<false, 384, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(chain_kernel<true, 384, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    SA_CUDA(cudaFuncSetAttribute(chain_kernel<false, kWideThreads, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(rfft_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(rfft_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     SA_CUDA(cudaFuncSetAttribute(irfft_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
@@ -1521,7 +1527,7 @@ int env_int(const char* k, int d);
 
 // allow16: the plan may use radix-16 passes (the standalone transform
 // kernels; the chain kernel has no register room for them)
-bool make_fft_geo(int64_t L, FftGeo* g, bool allow16 = false) {
+bool make_fft_geo(int64_t L, FftGeo* g, bool allow16 = false, int64_t odd_min = 0) {
     std::memset(g, 0, sizeof(*g));
     if (L < 1) return false;
     g->packed = (L % 2 == 0) ? 1 : 0;
@@ -1571,6 +1577,11 @@ bool make_fft_geo(int64_t L, FftGeo* g, bool allow16 = false) {
     int64_t gen = 0;
     for (int q = 0; q < np; ++q)
         if (g->radix[q] != 2 && g->radix[q] != 4 && g->radix[q] != 8) gen += N * (int64_t)g->radix[q];
+    // odd composite L: the paired-column real transform (sa_fft.cuh rfft_any)
+    // runs the last, largest-radix pass on half the columns and the earlier
+    // ones on (P + 1) / 2P of the points
+    const bool oddreal = !g->packed && np >= 2 && L >= odd_min && env_int("SA_ODDREAL", 1);
+    if (oddreal) gen = (gen * 11) / 20;
     if (gen > 0 && env_int("SA_BLUESTEIN", 1)) {
         int64_t M = 1;
         while (M < 2 * N - 1) M <<= 1;
@@ -1590,6 +1601,7 @@ bool make_fft_geo(int64_t L, FftGeo* g, bool allow16 = false) {
             g->mpass = mp;
         }
     }
+    g->oddreal = (oddreal && !g->blue) ? 1 : 0;
     return true;
 }
 
@@ -1693,6 +1705,12 @@ int get_dct_twiddles(int dev, int N, const double2** out) {
 // doubles per buffer a spectral stage needs at length L
 // doubles per row buffer for an L-point real transform (Bluestein: M complex)
 int64_t fft_lcap(int64_t L, const FftGeo* g = nullptr) {
+    if (g && g->oddreal) {
+        // paired-column real transform of L = P q: (P + 1) / 2 * q complex
+        // points through the first passes, P * (q + 1) / 2 into the last
+        const int64_t P = g->radix[g->npass - 1], q = L / P;
+        return L + std::max(P, q) + 2;
+    }
     const int64_t base = (L % 2 == 0) ? L + 2 : 2 * L + 2;
     return (g && g->blue) ? std::max<int64_t>(base, 2 * (int64_t)g->M + 2) : base;
 }
@@ -1704,6 +1722,7 @@ struct Plan {
     Layout lay;
     int grid;
     bool wide = false;  // short series: chain_kernel<false, kWideThreads>
+    bool odd = false;   // some spectral stage runs the odd-length real transform: chain_kernel<*, *, true>
     int warps;     // warps (= series in flight) per CTA
     size_t smem;   // dynamic smem per CTA
     bool global = false;  // row buffers in a global scratch of grid * warps slots
@@ -1775,8 +1794,9 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
         if (s.op == SA_OP_CONVOLVE && (s.aux_off < 0 || s.aux_len < 1 || s.aux_off + s.aux_len > n_aux))
             return fail(SA_ERR_INVALID_ARG, "convolve taps out of range");
         if (is_spectral(s.op) && s.probability > 0.0) {
-            if (!make_fft_geo(L, &d.fft))
+            if (!make_fft_geo(L, &d.fft, false, env_int("SA_ODDREAL_MIN", 0)))
                 return fail(SA_ERR_UNSUPPORTED, "no FFT plan for length " + std::to_string(L));
+            plan->odd = plan->odd || d.fft.oddreal;
             int rc = get_twiddles(dev, (int)L, &d.tw);
             if (!rc) rc = finish_geo(dev, &d.fft);
             if (rc) return rc;
@@ -1816,12 +1836,20 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
     // then the buffers move to global memory (L2 resident), which lets 12
     // warps per SM run (sweep: L = 2369 1.9x, Bluestein 541 / 1707 1.3-2x).
     const size_t smem_fit = (ds.smem_optin - kCtaShared) / std::max<size_t>(plan->lay.total, 1);
-    const bool starved = smem_fit >= 1 && smem_fit <= 3 && env_int("SA_AUTO_GLOBAL", 1) &&
+    // With 4-5 warps the answer depends on the chain: compute-heavy chains
+    // (APP-level work per row) gain 8-16% from 12 warps over the L2-resident
+    // scratch, light ones (one Jitter, one TimeWarp) lose 25-130% to its
+    // traffic (L = 2300 .. 2900, tools/oddreal_session3.sh).
+    double work = 0.0;
+    for (int j = 0; j < ns; ++j) work += stages[j].probability * op_cost(stages[j].op);
+    const int starved_fit = env_int("SA_STARVED_FIT", work >= 8.0 ? 5 : 3);
+    const bool starved = smem_fit >= 1 && smem_fit <= (size_t)starved_fit && env_int("SA_AUTO_GLOBAL", 1) &&
                          p.rows_out > 3 * (int64_t)ds.sms * (int64_t)smem_fit;
     if (plan->lay.total + kCtaShared > ds.smem_optin || starved || env_int("SA_FORCE_GLOBAL", 0)) {
         // long series: the two row buffers move to global memory (L2 / HBM
         // resident, same code); shared memory keeps the window and scratch
         plan->global = true;
+        if (env_int("SA_GLOBAL_ALIGN", 1)) p.lcap = (p.lcap + 15) & ~15;  // 128-byte rows in the scratch
         plan->lay = make_layout(0, ns, small, iscr);
         if (plan->lay.total + kCtaShared > ds.smem_optin)
             return fail(SA_ERR_UNSUPPORTED, "stage scratch too large for shared memory");
@@ -1903,7 +1931,11 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
             per_sm = it->second;
         } else {
             cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                &per_sm, plan->global ? chain_kernel<true> : (plan->wide ? chain_kernel<false, kWideThreads> : chain_kernel<false>),
+                &per_sm,
+                plan->odd ? (plan->global ? chain_kernel<true, 384, true>
+                                          : (plan->wide ? chain_kernel<false, kWideThreads, true> : chain_kernel<false, 384, true>))
+                          : (plan->global ? chain_kernel<true>
+                                          : (plan->wide ? chain_kernel<false, kWideThreads> : chain_kernel<false>)),
                 32 * warps, plan->smem);
             if (e != cudaSuccess) return cuda_fail(e, "occupancy");
             occ_cache[key] = per_sm;
@@ -2051,7 +2083,10 @@ int launch_chain(Plan* plan, cudaStream_t stream) {
         SA_CUDA(scratch.alloc(&p.gbuf, sizeof(double) * 2 * (size_t)p.lcap * (size_t)plan->grid * plan->warps));
         p.bulk_in = 0;  // TMA bulk copies target shared memory only
     }
-    if (plan->global) chain_kernel<true><<<plan->grid, 32 * plan->warps, plan->smem, stream>>>(p);
+    if (plan->odd && plan->global) chain_kernel<true, 384, true><<<plan->grid, 32 * plan->warps, plan->smem, stream>>>(p);
+    else if (plan->odd && plan->wide) chain_kernel<false, kWideThreads, true><<<plan->grid, 32 * plan->warps, plan->smem, stream>>>(p);
+    else if (plan->odd) chain_kernel<false, 384, true><<<plan->grid, 32 * plan->warps, plan->smem, stream>>>(p);
+    else if (plan->global) chain_kernel<true><<<plan->grid, 32 * plan->warps, plan->smem, stream>>>(p);
     else if (plan->wide) chain_kernel<false, kWideThreads><<<plan->grid, 32 * plan->warps, plan->smem, stream>>>(p);
     else chain_kernel<false><<<plan->grid, 32 * plan->warps, plan->smem, stream>>>(p);
     SA_CUDA(cudaGetLastError());

@@ -106,6 +106,27 @@ __device__ __forceinline__ double u53(uint64_t w) {  // Generator.random()
     return (double)(w >> 11) * (1.0 / 9007199254740992.0);
 }
 
+// (double)v for v < 2^52 without I2F.F64.U64: splice v into the mantissa of
+// 2^52 and subtract 2^52 (exact: both are integers below 2^53).
+__device__ __forceinline__ double u52_to_double(uint64_t v) {
+    return __longlong_as_double((long long)(v | 0x4330000000000000ULL)) - 4503599627370496.0;
+}
+// x with its sign bit XORed by bit 8 of the ziggurat word (numpy's
+// `sign ? -x : x`; x >= 0 here, so the XOR is the negation, -0.0 included).
+__device__ __forceinline__ double zig_signed(double x, uint64_t w) {
+    return __longlong_as_double(__double_as_longlong(x) ^ (long long)((w << 55) & 0x8000000000000000ULL));
+}
+// Two consecutive window words (16-byte aligned) by a shared-memory load: the
+// window and the cached gate block both live in shared memory.
+__device__ __forceinline__ ulonglong2 lds_u64x2(const uint64_t* p) {
+    ulonglong2 v;
+    asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];"
+                 : "=l"(v.x), "=l"(v.y)
+                 : "r"((uint32_t)__cvta_generic_to_shared(p))
+                 : "memory");
+    return v;
+}
+
 // Warp-uniform stream state.  `win` points at the words currently buffered:
 // either the 4 words of block 0 cached by the gate pre-pass (wn = 4) or the
 // warp's 128-word window (wn = SA_WIN).
@@ -372,8 +393,7 @@ __device__ __forceinline__ void normals(WStream& s, int lane, int count, const Z
         const uint32_t p0 = 4u * lane;
         uint64_t wv[4];
         if (p0 < wn) {
-            const ulonglong2* w2 = reinterpret_cast<const ulonglong2*>(s.win) + 2 * lane;
-            ulonglong2 a = w2[0], b = w2[1];
+            const ulonglong2 a = lds_u64x2(s.win + 4 * lane), b = lds_u64x2(s.win + 4 * lane + 2);
             wv[0] = a.x; wv[1] = a.y; wv[2] = b.x; wv[3] = b.y;
         } else {
             wv[0] = wv[1] = wv[2] = wv[3] = 0;
@@ -387,8 +407,7 @@ __device__ __forceinline__ void normals(WStream& s, int lane, int count, const Z
             const uint64_t rr = w >> 8;
             const uint64_t rabs = (rr >> 1) & 0x000fffffffffffffULL;
             const ZigEntry ze = zig[w & 0xff];
-            const double x = (double)rabs * ze.wi;
-            z[r] = (rr & 1) ? -x : x;
+            z[r] = zig_signed(u52_to_double(rabs) * ze.wi, w);
             const uint32_t pb = (p0 + r - sp < wn - sp) ? 1u : 0u;  // sp <= p < wn
             const uint32_t sb = pb & (rabs < ze.ki ? 0u : 1u);
             pres |= pb << r;

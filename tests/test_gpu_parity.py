@@ -520,6 +520,41 @@ def test_bluestein_forced_matches_generic(monkeypatch):
     assert_matches(b.im, a.im, exact=False, what="im")
 
 
+@pytest.mark.parametrize("L", [9, 15, 21, 45, 75, 121, 219, 343, 459, 909, 1221, 1435, 2369, 2475])
+def test_odd_composite_lengths_real_transform(L, monkeypatch):
+    """Odd composite lengths run the paired-column real transform (the last,
+    largest-radix pass on half the columns; the inverse through one forward
+    transform of Re X - Im X): transforms, DCT, APP and a mask / sinusoid chain
+    stay within the FFT tolerance of the oracle, and agree with the
+    complexified plan (SA_ODDREAL=0) to the same tolerance."""
+    from oracle import oracle as O
+    from paper_2601_03159_b200 import AmplitudePhasePerturb, Batch, FrequencyMask, Pipeline, RandomSinusoid
+    from paper_2601_03159_b200 import dct_forward, dct_inverse, fft_forward, fft_inverse
+    from sa_testutil import assert_matches
+
+    x = np.cumsum(np.random.default_rng(L).normal(0, 1, (37, L)), axis=1)
+    spec = fft_forward(Batch(x))
+    re, im = O.fft_forward(x)
+    assert_matches(spec.re, re, exact=False, what="re")
+    assert_matches(spec.im, im, exact=False, what="im")
+    assert np.all(spec.im[:, 0] == 0.0)
+    assert np.abs(fft_inverse(spec).values - x).max() <= 1e-9 * np.abs(x).max()
+    assert np.abs(dct_forward(Batch(x)).coeffs - O.dct(x)).max() <= 1e-10 * max(1.0, np.abs(x).max() * L)
+    assert np.abs(dct_inverse(dct_forward(Batch(x))).values - x).max() <= 1e-9 * np.abs(x).max()
+    pipe = Pipeline(stages=(AmplitudePhasePerturb(0.1, 0.1), FrequencyMask(max(1, L // 40)), RandomSinusoid(1.0)),
+                    master_seed=6)
+    got = pipe.run(Batch(x)).values
+    assert_matches(got, O.run_pipeline(pipe, x), exact=False, what="chain")
+    monkeypatch.setenv("SA_ODDREAL", "0")
+    assert_matches(pipe.run(Batch(x)).values, got, exact=False, what="complexified plan")
+    b = fft_forward(Batch(x))
+    assert_matches(b.re, spec.re, exact=False, what="re (complexified)")
+    assert_matches(b.im, spec.im, exact=False, what="im (complexified)")
+    monkeypatch.delenv("SA_ODDREAL")
+    monkeypatch.setenv("SA_FORCE_GLOBAL", "1")  # row buffers in the global scratch: the same code, bitwise
+    assert np.array_equal(pipe.run(Batch(x)).values, got)
+
+
 def test_parallel_shards_across_devices_bitwise(monkeypatch):
     """parallel=True shards rows over the visible GPUs (one host thread per
     range, global series offsets); SA_DEVICES=0,0,0 runs three shards on one
