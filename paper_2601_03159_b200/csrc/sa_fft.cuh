@@ -211,7 +211,7 @@ struct FftGeo {
     int32_t packed;    // 1: even L, N = L/2 (real input viewed as complex)
     int32_t npass;
     int32_t blue;      // 1: Bluestein
-    int32_t oddreal;   // 1: odd composite L on the paired-column real transform (rfft_any)
+    int32_t oddreal;   // odd L as a real transform (rfft_any): 1 paired columns, 2 Bluestein on the bins k <= L/2
     int16_t radix[SA_FFT_MAXPASS];
     int32_t M, mpass;  // Bluestein convolution length and its radix plan
     int16_t mradix[16];
@@ -451,7 +451,7 @@ __device__ __forceinline__ double2* fft_any(double2* a, double2* b, const FftGeo
     if (BLUE && g.blue) return bluestein(a, b, g, lane);
     if (is_fft_512(g, L)) return fft_512<FIN>(a, b, tw, lane, fin_bad_out);
     // oddreal: a holds the (P + 1) / 2 * q packed column pairs (rfft_any)
-    const bool odd = ODD && g.oddreal;
+    const bool odd = ODD && g.oddreal == 1;
     const int P = odd ? g.radix[g.npass - 1] : 1;
     const int N = odd ? ((P + 1) >> 1) * (g.N / P) : g.N;
     return fft_passes<R16, ODD>(a, b, N, g.npass, g.radix, tw, L, lane, odd);
@@ -541,7 +541,7 @@ __device__ __forceinline__ double2* rfft_any(double* xa, double* xb, int L, cons
     // odd L: complexify into xb and take the N = L transform; even L: view
     // the real series as N = L/2 complex points (one call site either way,
     // to keep the FFT's code emitted once)
-    if (ODD && g.oddreal) {
+    if (ODD && g.oddreal == 1) {
         oddreal_pack(xa, zb, L, g.radix[g.npass - 1], lane);
     } else if (!g.packed) {
         for (int n = lane; n < L; n += 32) zb[n] = make_double2(xa[n], 0.0);
@@ -605,7 +605,12 @@ __device__ __forceinline__ double* irfft_any(double2* X, double2* other, int L, 
     if (folded) {
     } else if (ODD && g.oddreal) {
         oddreal_fold(X, reinterpret_cast<double*>(other), L, lane);
-        oddreal_pack(reinterpret_cast<const double*>(other), X, L, g.radix[g.npass - 1], lane);
+        if (g.oddreal == 1) {
+            oddreal_pack(reinterpret_cast<const double*>(other), X, L, g.radix[g.npass - 1], lane);
+        } else {  // Bluestein on the half range of bins: the real series complexified
+            const double* h = reinterpret_cast<const double*>(other);
+            for (int n = lane; n < L; n += 32) X[n] = make_double2(h[n], 0.0);
+        }
     } else if (!g.packed) {  // odd L: Hermitian completion, full transform, real part
         const int bins = L / 2 + 1;
         for (int k = lane; k < bins; k += 32) {

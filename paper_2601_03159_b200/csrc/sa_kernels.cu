@@ -1580,11 +1580,17 @@ bool make_fft_geo(int64_t L, FftGeo* g, bool allow16 = false, int64_t odd_min = 
     // odd composite L: the paired-column real transform (sa_fft.cuh rfft_any)
     // runs the last, largest-radix pass on half the columns and the earlier
     // ones on (P + 1) / 2P of the points
-    const bool oddreal = !g->packed && np >= 2 && L >= odd_min && env_int("SA_ODDREAL", 1);
+    const bool oddon = !g->packed && L >= odd_min && env_int("SA_ODDREAL", 1);
+    const bool oddreal = oddon && np >= 2;
     if (oddreal) gen = (gen * 11) / 20;
     if (gen > 0 && env_int("SA_BLUESTEIN", 1)) {
+        // odd L (oddon): the real transform needs the bins k <= (N - 1) / 2
+        // only, so the circular convolution may wrap the kernel's positive
+        // range above (N - 1) / 2: M >= (3N - 1) / 2 instead of 2N - 1 (the
+        // inverse runs the same forward transform, irfft_any)
+        const int64_t span = oddon ? (3 * N - 1) / 2 : 2 * N - 1;
         int64_t M = 1;
-        while (M < 2 * N - 1) M <<= 1;
+        while (M < span) M <<= 1;
         int lg = 0;
         while ((1ll << lg) < M) ++lg;
         const double blu = 4.5 * (double)M * (double)lg;
@@ -1601,7 +1607,8 @@ bool make_fft_geo(int64_t L, FftGeo* g, bool allow16 = false, int64_t odd_min = 
             g->mpass = mp;
         }
     }
-    g->oddreal = (oddreal && !g->blue) ? 1 : 0;
+    // 1: paired columns; 2: Bluestein on the half range of bins
+    g->oddreal = g->blue ? (oddon ? 2 : 0) : (oddreal ? 1 : 0);
     return true;
 }
 
@@ -1643,7 +1650,8 @@ int finish_geo(int dev, FftGeo* g) {
     int rc = get_twiddles(dev, g->M, &g->twM);
     if (rc) return rc;
     std::lock_guard<std::mutex> lk(g_mu);
-    auto key = std::make_pair(dev, g->N);
+    const bool half = g->oddreal == 2;  // kernel indices -(N - 1) .. (N - 1) / 2 only
+    auto key = std::make_pair(dev, half ? -g->N : g->N);
     auto it = g_blue.find(key);
     if (it == g_blue.end()) {
         const int64_t N = g->N, M = g->M;
@@ -1655,8 +1663,10 @@ int finish_geo(int dev, FftGeo* g) {
             const long double a = -pi * (long double)q / (long double)N;
             const long double c = cosl(a), sn = sinl(a);
             ch[(size_t)n] = make_double2((double)c, (double)sn);
-            hr[(size_t)n] = c;  // conj(c[n])
-            hi[(size_t)n] = -sn;
+            if (!half || 2 * n <= N - 1) {
+                hr[(size_t)n] = c;  // conj(c[n])
+                hi[(size_t)n] = -sn;
+            }
             if (n > 0) {
                 hr[(size_t)(M - n)] = c;
                 hi[(size_t)(M - n)] = -sn;
@@ -1705,7 +1715,7 @@ int get_dct_twiddles(int dev, int N, const double2** out) {
 // doubles per buffer a spectral stage needs at length L
 // doubles per row buffer for an L-point real transform (Bluestein: M complex)
 int64_t fft_lcap(int64_t L, const FftGeo* g = nullptr) {
-    if (g && g->oddreal) {
+    if (g && g->oddreal == 1) {
         // paired-column real transform of L = P q: (P + 1) / 2 * q complex
         // points through the first passes, P * (q + 1) / 2 into the last
         const int64_t P = g->radix[g->npass - 1], q = L / P;
@@ -1842,7 +1852,8 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
     // traffic (L = 2300 .. 2900, tools/oddreal_session3.sh).
     double work = 0.0;
     for (int j = 0; j < ns; ++j) work += stages[j].probability * op_cost(stages[j].op);
-    const int starved_fit = env_int("SA_STARVED_FIT", work >= 8.0 ? 5 : 3);
+    // (6 warps: config 5's chain at L = 541 1.83 ms in the scratch against 2.05, a lone APP 1.97 against 1.50)
+    const int starved_fit = env_int("SA_STARVED_FIT", work >= 15.0 ? 6 : (work >= 8.0 ? 5 : 3));
     const bool starved = smem_fit >= 1 && smem_fit <= (size_t)starved_fit && env_int("SA_AUTO_GLOBAL", 1) &&
                          p.rows_out > 3 * (int64_t)ds.sms * (int64_t)smem_fit;
     if (plan->lay.total + kCtaShared > ds.smem_optin || starved || env_int("SA_FORCE_GLOBAL", 0)) {

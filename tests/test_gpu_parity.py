@@ -520,13 +520,16 @@ def test_bluestein_forced_matches_generic(monkeypatch):
     assert_matches(b.im, a.im, exact=False, what="im")
 
 
-@pytest.mark.parametrize("L", [9, 15, 21, 45, 75, 121, 219, 343, 459, 909, 1221, 1435, 2369, 2475])
-def test_odd_composite_lengths_real_transform(L, monkeypatch):
+@pytest.mark.parametrize("L", [9, 15, 21, 45, 75, 121, 219, 343, 459, 541, 909, 997, 1221, 1361, 1435, 1707, 2369,
+                               2475])
+def test_odd_lengths_real_transform(L, monkeypatch):
     """Odd composite lengths run the paired-column real transform (the last,
-    largest-radix pass on half the columns; the inverse through one forward
-    transform of Re X - Im X): transforms, DCT, APP and a mask / sinusoid chain
-    stay within the FFT tolerance of the oracle, and agree with the
-    complexified plan (SA_ODDREAL=0) to the same tolerance."""
+    largest-radix pass on half the columns), odd lengths with a large prime
+    factor (541, 997, 1361, 1707 = 3 * 569) Bluestein on the bins k <= L/2 (a
+    convolution of (3L - 1) / 2 instead of 2L - 1 points); the inverse is one
+    forward transform of Re X - Im X.  Transforms, DCT, APP and a mask /
+    sinusoid chain stay within the FFT tolerance of the oracle, and agree with
+    the complexified plan (SA_ODDREAL=0) to the same tolerance."""
     from oracle import oracle as O
     from paper_2601_03159_b200 import AmplitudePhasePerturb, Batch, FrequencyMask, Pipeline, RandomSinusoid
     from paper_2601_03159_b200 import dct_forward, dct_inverse, fft_forward, fft_inverse
