@@ -355,9 +355,10 @@ __device__ __forceinline__ void real_unpack(const double2* __restrict__ Z, doubl
     __syncwarp();
 }
 
-// ODD: the odd-length real transform is compiled in (the chain kernel keeps it
-// out of the instantiation that runs the even lengths -- its code generation
-// is sensitive to everything inlined into it).
+// ODD: the generic (odd prime) passes and the odd-length real transform are
+// compiled in.  The chain kernel keeps them -- and Bluestein -- out of the
+// instantiation that runs the power-of-two plans: its code generation is
+// sensitive to everything inlined into it.
 template <bool R16 = false, bool ODD = true>
 __device__ __forceinline__ double2* fft_passes(double2* a, double2* b, int N, int npass, const int16_t* radix,
                                                const double2* tw, int L, int lane, bool real_last = false) {
@@ -381,7 +382,7 @@ __device__ __forceinline__ double2* fft_passes(double2* a, double2* b, int N, in
             else stockham_pass<2, false>(src, dst, N, lns, tw, tstep, lane, carry, out);
             carry = out;
             lns += lr;
-        } else {
+        } else if (ODD) {  // (plans with a generic pass run the ODD instantiations)
             int Qc = N / R, tsa = L / (Ns * R), hl = -1;
             if (ODD && real_last && p == npass - 1) {  // Ns = q here
                 real_unpack(src, dst, R, Ns, tw, lane);

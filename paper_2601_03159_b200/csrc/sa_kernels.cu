@@ -132,9 +132,11 @@ constexpr size_t kCtaShared = 256 * sizeof(ZigEntry) + 4 * sizeof(unsigned long 
 #define SA_WIDE_THREADS 512
 #endif
 constexpr int kWideThreads = SA_WIDE_THREADS;
-// ODD: odd composite lengths on the paired-column real transform
-// (sa_fft.cuh); a separate instantiation, so the kernel the even lengths run
-// is generated without that code (measured: inlining it cost config 5 1%).
+// ODD: spectral stages whose FFT plan is not plain radix-8/4/2 (generic
+// odd-prime passes, Bluestein, the odd-length real transforms of sa_fft.cuh);
+// separate instantiations, so the kernel the power-of-two lengths run is
+// generated without that code (measured: inlining the odd-length transform
+// alone cost config 5 1%).
 template <bool GMEM, int MAXT = 384, bool ODD = false>
 __global__ void __launch_bounds__(MAXT) chain_kernel(const __grid_constant__ ChainParams p) {
     extern __shared__ __align__(16) unsigned char smem_all[];
@@ -1732,7 +1734,7 @@ struct Plan {
     Layout lay;
     int grid;
     bool wide = false;  // short series: chain_kernel<false, kWideThreads>
-    bool odd = false;   // some spectral stage runs the odd-length real transform: chain_kernel<*, *, true>
+    bool odd = false;   // some spectral stage has a non-power-of-two FFT plan: chain_kernel<*, *, true>
     int warps;     // warps (= series in flight) per CTA
     size_t smem;   // dynamic smem per CTA
     bool global = false;  // row buffers in a global scratch of grid * warps slots
@@ -1806,7 +1808,11 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
         if (is_spectral(s.op) && s.probability > 0.0) {
             if (!make_fft_geo(L, &d.fft, false, env_int("SA_ODDREAL_MIN", 0)))
                 return fail(SA_ERR_UNSUPPORTED, "no FFT plan for length " + std::to_string(L));
-            plan->odd = plan->odd || d.fft.oddreal;
+            // anything but a plain radix-8/4/2 plan runs the ODD instantiations
+            bool plain = !d.fft.blue && !d.fft.oddreal;
+            for (int q = 0; q < d.fft.npass; ++q)
+                plain = plain && (d.fft.radix[q] == 2 || d.fft.radix[q] == 4 || d.fft.radix[q] == 8);
+            plan->odd = plan->odd || !plain;
             int rc = get_twiddles(dev, (int)L, &d.tw);
             if (!rc) rc = finish_geo(dev, &d.fft);
             if (rc) return rc;

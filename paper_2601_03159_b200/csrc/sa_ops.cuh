@@ -1279,7 +1279,7 @@ __device__ __forceinline__ bool op_spectral(const DevStage& st, WStream& s, doub
         }
         __syncwarp();
     } else {
-        X = rfft_any<SA_CHAIN_BLUE, false, ODD>(cur, oth, L, st.fft, st.tw, w.lane, !sparse);  // sparse: X = the packed Z
+        X = rfft_any<SA_CHAIN_BLUE && ODD, false, ODD>(cur, oth, L, st.fft, st.tw, w.lane, !sparse);  // sparse: X = the packed Z
     }
     double* free_buf = (reinterpret_cast<double*>(X) == cur) ? oth : cur;
     if (sparse) {
@@ -1321,7 +1321,7 @@ __device__ __forceinline__ bool op_spectral(const DevStage& st, WStream& s, doub
     // sparse: the folded input is in free_buf and X is scratch
     double2* other = reinterpret_cast<double2*>(free_buf);
     bool ybad = false;
-    double* y = irfft_any<SA_CHAIN_BLUE, false, ODD>(X, other, L, st.fft, st.tw, w.lane, &ybad, sparse);  // checks its outputs
+    double* y = irfft_any<SA_CHAIN_BLUE && ODD, false, ODD>(X, other, L, st.fft, st.tw, w.lane, &ybad, sparse);  // checks its outputs
     bad.merge(ybad);
     if (y != cur) swapbuf(cur, oth);
     return false;
