@@ -1858,8 +1858,12 @@ int make_plan(int dev, const sa_stage* stages, int32_t ns, const double* aux, in
     // traffic (L = 2300 .. 2900, tools/oddreal_session3.sh).
     double work = 0.0;
     for (int j = 0; j < ns; ++j) work += stages[j].probability * op_cost(stages[j].op);
-    // (6 warps: config 5's chain at L = 541 1.83 ms in the scratch against 2.05, a lone APP 1.97 against 1.50)
-    const int starved_fit = env_int("SA_STARVED_FIT", work >= 15.0 ? 6 : (work >= 8.0 ? 5 : 3));
+    // At 6 warps only Bluestein chains gain (their rows run four M-point FFTs
+    // per spectral stage: config 5's chain at L = 541 1.83 ms in the scratch
+    // against 2.05; the same chain at L = 2136, generic passes, 2.88 against 2.80).
+    bool blue = false;
+    for (int j = 0; j < ns; ++j) blue = blue || (is_spectral(stages[j].op) && stages[j].probability > 0.0 && p.st[j].fft.blue);
+    const int starved_fit = env_int("SA_STARVED_FIT", (work >= 15.0 && blue) ? 6 : (work >= 8.0 ? 5 : 3));
     const bool starved = smem_fit >= 1 && smem_fit <= (size_t)starved_fit && env_int("SA_AUTO_GLOBAL", 1) &&
                          p.rows_out > 3 * (int64_t)ds.sms * (int64_t)smem_fit;
     if (plan->lay.total + kCtaShared > ds.smem_optin || starved || env_int("SA_FORCE_GLOBAL", 0)) {
