@@ -383,17 +383,15 @@ __device__ __forceinline__ double2* fft_passes(double2* a, double2* b, int N, in
             carry = out;
             lns += lr;
         } else if (ODD) {  // (plans with a generic pass run the ODD instantiations)
-            int Qc = N / R, tsa = L / (Ns * R), hl = -1;
             if (ODD && real_last && p == npass - 1) {  // Ns = q here
                 real_unpack(src, dst, R, Ns, tw, lane);
                 double2* t = src;
                 src = dst;
                 dst = t;
-                Qc = (Ns + 1) >> 1;
-                tsa = 0;
-                hl = (L - 1) >> 1;
+                generic_pass(src, dst, (Ns + 1) >> 1, Ns, R, tw, L, lane, 0, (L - 1) >> 1);
+            } else {  // (its own copy: hl = -1 folds the mirrored store away)
+                generic_pass(src, dst, N / R, Ns, R, tw, L, lane, L / (Ns * R), -1);
             }
-            generic_pass(src, dst, Qc, Ns, R, tw, L, lane, tsa, hl);
         }
         Ns *= R;
         double2* t = src;
