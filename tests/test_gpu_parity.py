@@ -558,6 +558,34 @@ def test_odd_lengths_real_transform(L, monkeypatch):
     assert np.array_equal(pipe.run(Batch(x)).values, got)
 
 
+def test_every_odd_length_to_599_vs_numpy():
+    """Every odd length 3 .. 599 (primes on one direct pass or Bluestein's half
+    range, composites on paired columns, every factor structure in between):
+    rfft against numpy's pocketfft and the irfft round trip."""
+    from paper_2601_03159_b200 import Batch, fft_forward, fft_inverse
+
+    g = np.random.default_rng(599)
+    for L in range(3, 600, 2):
+        x = np.cumsum(g.normal(0, 1, (5, L)), axis=1)
+        want = np.fft.rfft(x, axis=1)
+        sb = fft_forward(Batch(x))
+        tol = spectral_tol(want.real)
+        assert np.abs(sb.re - want.real).max() <= tol and np.abs(sb.im - want.imag).max() <= tol, L
+        assert np.abs(fft_inverse(sb).values - x).max() <= spectral_tol(x), L
+
+
+def test_every_odd_length_to_399_chain_vs_oracle():
+    """The chain kernel's ODD instantiations on every odd length 3 .. 399: APP
+    (all bins drawn and perturbed) and a sinusoid against the oracle."""
+    g = np.random.default_rng(399)
+    pipe = Pipeline(stages=(AmplitudePhasePerturb(0.1, 0.1), RandomSinusoid(0.5, min_bin=0)), master_seed=9)
+    for L in range(3, 400, 2):
+        x = np.cumsum(g.normal(0, 1, (5, L)), axis=1)
+        want = O.run_pipeline(pipe, x)
+        err = np.abs(gpu_run(pipe, x) - want).max()
+        assert err <= spectral_tol(want), (L, err)
+
+
 def test_parallel_shards_across_devices_bitwise(monkeypatch):
     """parallel=True shards rows over the visible GPUs (one host thread per
     range, global series offsets); SA_DEVICES=0,0,0 runs three shards on one
