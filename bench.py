@@ -165,10 +165,24 @@ def ncu_traffic(cfg):
 
 def build_sha16() -> str | None:
     """Identity of the library under test (the ncu instruction counts carry
-    the hash of the build they were captured on)."""
+    the hash of the build they were captured on): the kernel sources and build
+    recipe -- nvcc's output is not byte-reproducible, so hashing the .so would
+    mark every rebuild of the same sources stale.  An alternative build named
+    by SA_LIB_PATH (A/B runs) is identified by its bytes."""
+    alt = os.environ.get("SA_LIB_PATH")
+    h = hashlib.sha256()
     try:
-        with open(LIB_PATH, "rb") as fh:
-            return hashlib.sha256(fh.read()).hexdigest()[:16]
+        if alt:
+            with open(alt, "rb") as fh:
+                h.update(fh.read())
+        else:
+            src = os.path.join(ROOT, "paper_2601_03159_b200", "csrc")
+            for name in sorted(os.listdir(src)):
+                with open(os.path.join(src, name), "rb") as fh:
+                    h.update(name.encode() + b"\0" + fh.read())
+            with open(os.path.join(ROOT, "include", "seriesaug_b200.h"), "rb") as fh:
+                h.update(fh.read())
+        return h.hexdigest()[:16]
     except OSError:
         return None
 

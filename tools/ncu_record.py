@@ -27,8 +27,10 @@ def num(k):
 traffic = num("dram__bytes_read.sum") * scale.get(u.get("dram__bytes_read.sum"), 1) + \
     num("dram__bytes_write.sum") * scale.get(u.get("dram__bytes_write.sum"), 1)
 ins = num("smsp__inst_executed.sum")
-lib = os.path.join(ROOT, "paper_2601_03159_b200", "_lib", "libseriesaug_b200.so")
-sha = hashlib.sha256(open(lib, "rb").read()).hexdigest()[:16]
+sys.path.insert(0, ROOT)
+import bench  # noqa: E402  (the build identity bench.py compares against: the kernel sources)
+
+sha = bench.build_sha16()
 for name, val in (("ncu_traffic.json", traffic), ("ncu_instructions.json", ins)):
     path = os.path.join(ROOT, "profiles", name)
     cur = json.load(open(path)) if os.path.exists(path) else {}
